@@ -1,0 +1,161 @@
+/*
+ * rtk_c.h — C-ABI of the B200-native radix top-k (librtk_b200.so).
+ *
+ * This is the drop-in boundary for the reference's top-k entry points
+ * (/root/reference/proj/include/rtk/). Plain pointers and sizes only; no torch or C++
+ * types. Each entry point names the reference interface it replaces:
+ *
+ *   rtk_topk / rtk_topk_host                 <- rtk::topk            engine.hpp:422-443
+ *   rtk_topk_batched / rtk_topk_batched_host <- rtk::batch_topk      batch.hpp:261-367
+ *   rtk_topk_scaled / rtk_topk_scaled_host   <- rtk::scaled_topk     scaling.hpp:42-86
+ *   rtk_cfg + rtk_cfg_validate               <- rtk::EngineConfig    engine.hpp:48-68
+ *   rtk_batch_opts                           <- rtk::BatchOptions    batch.hpp:133-136
+ *   rtk_scale_info                           <- rtk::ScaleInfo       scaling.hpp:29-33
+ *   status codes                             <- rtk::empty_input_error / rank_out_of_range /
+ *                                               invariant_violation (engine.hpp:31-41),
+ *                                               std::invalid_argument (EngineConfig::validate
+ *                                               :61-67, BatchInput::validate batch.hpp:40-53)
+ *   rtk_merge_shards                         <- (new) final select of the n-sharded multi-GPU
+ *                                               query after the NCCL allgather
+ *
+ * Result semantics are the reference's (engine.hpp:402-420, oracle.hpp:19-39): the k
+ * selected elements sorted by (encoded key descending, index ascending); ties at the pivot
+ * take the lowest indices; values[i] == input[indices[i]] bit for bit; pivot = values[k-1].
+ * Indices are u64 and row-local (engine.hpp:106, batch.hpp:36-38).
+ *
+ * rtk_topk* take DEVICE pointers and run on `stream` (a cudaStream_t, NULL = legacy
+ * default stream). Round-1 implementation note: the call returns after the stream has
+ * drained (it reads candidate counts back between stages). rtk_*_host take HOST pointers
+ * and include the host<->device copies.
+ *
+ * Limits: n <= 2^32 elements per row on one device (the composite key carries a 32-bit
+ * row-local index); dtype F32 or U32; scaled mode is F32 only (as in the reference).
+ */
+#ifndef RTK_C_H
+#define RTK_C_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define RTK_OK 0
+#define RTK_EMPTY_INPUT 1          /* rtk::empty_input_error   (std::invalid_argument) */
+#define RTK_RANK_OUT_OF_RANGE 2    /* rtk::rank_out_of_range   (std::out_of_range)      */
+#define RTK_INVARIANT_VIOLATION 3  /* rtk::invariant_violation (std::logic_error)       */
+#define RTK_INVALID_ARGUMENT 4     /* std::invalid_argument (config / batch validation) */
+#define RTK_CUDA_ERROR 5
+#define RTK_OUT_OF_MEMORY 6
+#define RTK_INTERNAL 7
+
+/* dtypes (io.hpp:19 codes 0/1) and selection order (keycodec.hpp:19) */
+#define RTK_F32 0
+#define RTK_U32 1
+#define RTK_LARGEST 0
+#define RTK_SMALLEST 1
+
+/* scale modes (scaling.hpp:20) */
+#define RTK_SCALE_OFF 0
+#define RTK_SCALE_ALWAYS 1
+#define RTK_SCALE_ADAPTIVE 2
+
+/* mirrors rtk::EngineConfig (engine.hpp:48-68). On the GPU these are tuning hints only:
+ * results never depend on them (engine_test.cpp:305-322); d additionally selects the
+ * adaptive-scaling trigger window exactly as the reference does (scaling.hpp:53). */
+typedef struct rtk_cfg {
+    uint32_t d;                      /* digit width, [1,16], default 12 */
+    uint64_t block_size;             /* >= 1, default 1024 */
+    uint32_t grid_size;              /* >= 1, default 4 */
+    int32_t buffer_policy;           /* 0 Naive, 1 FlushEfficient (default) */
+    uint64_t pack_size;              /* power of two >= 4, default 16 */
+    int32_t hierarchical_atomics;    /* default 1 */
+    uint64_t filter_fixed_ceiling;   /* default 4096 */
+} rtk_cfg;
+
+/* mirrors rtk::BatchOptions (batch.hpp:133-136); results are identical for all settings */
+typedef struct rtk_batch_opts {
+    int32_t rescheduling;
+    int32_t padding;
+} rtk_batch_opts;
+
+/* mirrors rtk::ScaleInfo (scaling.hpp:29-33) */
+typedef struct rtk_scale_info {
+    int32_t scaled;
+    float a_s;
+    uint64_t a_index;
+} rtk_scale_info;
+
+/* work counters of the last call on a handle (cf. rtk::Instrumentation engine.hpp:74-101) */
+typedef struct rtk_stats {
+    uint64_t passes;             /* digit passes over the full input (fallback/trigger)   */
+    uint64_t elements_scanned;   /* elements read from the input (incl. samples)          */
+    uint64_t candidates;         /* sum over rows of the candidate-set size              */
+    uint64_t fallback_rows;      /* rows whose sampled threshold had to be recomputed    */
+    uint64_t kernel_launches;    /* kernels launched by the call                          */
+    float compact_ms;            /* device time of the streaming k_compact launch (events) */
+    float total_ms;              /* device time of the whole call on its stream (events)   */
+} rtk_stats;
+
+typedef struct rtk_handle_s* rtk_handle;
+
+/* library / handle */
+const char* rtk_version(void);
+const char* rtk_last_error(void);             /* thread-local message of the last failure */
+int rtk_handle_create(rtk_handle* out, int device);
+int rtk_handle_destroy(rtk_handle h);
+int rtk_get_stats(rtk_handle h, rtk_stats* out);
+void rtk_cfg_default(rtk_cfg* cfg);
+int rtk_cfg_validate(const rtk_cfg* cfg);
+
+/* single query, device pointers. out_pivot may be NULL. */
+int rtk_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, int order,
+             void* d_out_vals, uint64_t* d_out_idx, void* d_out_pivot, const rtk_cfg* cfg,
+             void* stream);
+
+/* batch of B (ragged) rows, device data + HOST descriptors (offsets/lengths/ks in elements,
+ * data_len = elements in d_data). Row t's outputs start at out_offsets[t] (NULL = exclusive
+ * prefix of ks). d_out_pivots (B values) may be NULL. On a task error the message carries
+ * "task N: ..." (batch.hpp:274-280). */
+int rtk_topk_batched(rtk_handle h, const void* d_data, uint64_t data_len,
+                     const uint64_t* offsets, const uint64_t* lengths, const uint64_t* ks,
+                     uint64_t B, int dtype, int order, void* d_out_vals, uint64_t* d_out_idx,
+                     const uint64_t* out_offsets, void* d_out_pivots, const rtk_cfg* cfg,
+                     const rtk_batch_opts* opts, void* stream);
+
+/* adaptive scaling (f32 only). a_s is drawn exactly as the reference draws it:
+ * index = std::mt19937_64(seed)() % n (scaling.hpp:35-40, 65-66). info may be NULL. */
+int rtk_topk_scaled(rtk_handle h, const float* d_in, uint64_t n, uint64_t k, int order,
+                    int mode, double trigger_fraction, uint64_t seed, float* d_out_vals,
+                    uint64_t* d_out_idx, float* d_out_pivot, rtk_scale_info* info,
+                    const rtk_cfg* cfg, void* stream);
+
+/* host-pointer variants: same contracts, host buffers, copies included */
+int rtk_topk_host(rtk_handle h, const void* in, uint64_t n, uint64_t k, int dtype, int order,
+                  void* out_vals, uint64_t* out_idx, void* out_pivot, const rtk_cfg* cfg);
+int rtk_topk_batched_host(rtk_handle h, const void* data, uint64_t data_len,
+                          const uint64_t* offsets, const uint64_t* lengths, const uint64_t* ks,
+                          uint64_t B, int dtype, int order, void* out_vals, uint64_t* out_idx,
+                          const uint64_t* out_offsets, void* out_pivots, const rtk_cfg* cfg,
+                          const rtk_batch_opts* opts);
+int rtk_topk_scaled_host(rtk_handle h, const float* in, uint64_t n, uint64_t k, int order,
+                         int mode, double trigger_fraction, uint64_t seed, float* out_vals,
+                         uint64_t* out_idx, float* out_pivot, rtk_scale_info* info,
+                         const rtk_cfg* cfg);
+
+/* Final select of an n-sharded query. d_cand_vals/d_cand_idx hold G blocks of
+ * kk = min(k, shard_n[g]) results, each block already in canonical order for its shard
+ * (the output of rtk_topk on that shard), concatenated in shard order; shard_base[g] is the
+ * global index of shard g's element 0 (host array). Writes the global top-k (values, global
+ * u64 indices, pivot) in canonical order. */
+int rtk_merge_shards(rtk_handle h, const void* d_cand_vals, const uint64_t* d_cand_idx,
+                     const uint64_t* block_len, const uint64_t* shard_base, uint32_t G,
+                     uint64_t k, int dtype, int order, void* d_out_vals, uint64_t* d_out_idx,
+                     void* d_out_pivot, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RTK_C_H */

@@ -1,0 +1,98 @@
+"""ctypes binding of the in-tree C-ABI library ``librtk_b200.so`` (include/rtk_c.h).
+
+The product path has no fallback: if the CUDA library is missing or cannot be loaded, every
+call raises. Build it with ``python -c "import __graft_entry__ as g; g.build()"`` or
+``make -C paper_2501_14336_b200``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librtk_b200.so")
+
+u64 = C.c_uint64
+u32 = C.c_uint32
+i32 = C.c_int32
+vp = C.c_void_p
+P64 = C.POINTER(C.c_uint64)
+
+# status codes (rtk_c.h)
+RTK_OK = 0
+RTK_EMPTY_INPUT = 1
+RTK_RANK_OUT_OF_RANGE = 2
+RTK_INVARIANT_VIOLATION = 3
+RTK_INVALID_ARGUMENT = 4
+RTK_CUDA_ERROR = 5
+RTK_OUT_OF_MEMORY = 6
+RTK_INTERNAL = 7
+
+
+class rtk_cfg(C.Structure):
+    _fields_ = [("d", u32), ("block_size", u64), ("grid_size", u32), ("buffer_policy", i32),
+                ("pack_size", u64), ("hierarchical_atomics", i32), ("filter_fixed_ceiling", u64)]
+
+
+class rtk_batch_opts(C.Structure):
+    _fields_ = [("rescheduling", i32), ("padding", i32)]
+
+
+class rtk_scale_info(C.Structure):
+    _fields_ = [("scaled", i32), ("a_s", C.c_float), ("a_index", u64)]
+
+
+class rtk_stats(C.Structure):
+    _fields_ = [("passes", u64), ("elements_scanned", u64), ("candidates", u64),
+                ("fallback_rows", u64), ("kernel_launches", u64), ("compact_ms", C.c_float),
+                ("total_ms", C.c_float)]
+
+
+# name -> (restype, argtypes); exactly the entry points include/rtk_c.h declares
+SIGNATURES = {
+    "rtk_version": (C.c_char_p, []),
+    "rtk_last_error": (C.c_char_p, []),
+    "rtk_handle_create": (C.c_int, [C.POINTER(vp), C.c_int]),
+    "rtk_handle_destroy": (C.c_int, [vp]),
+    "rtk_get_stats": (C.c_int, [vp, C.POINTER(rtk_stats)]),
+    "rtk_cfg_default": (None, [C.POINTER(rtk_cfg)]),
+    "rtk_cfg_validate": (C.c_int, [C.POINTER(rtk_cfg)]),
+    "rtk_topk": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, vp, vp, vp, C.POINTER(rtk_cfg), vp]),
+    "rtk_topk_batched": (C.c_int, [vp, vp, u64, P64, P64, P64, u64, C.c_int, C.c_int, vp, vp, P64,
+                                   vp, C.POINTER(rtk_cfg), C.POINTER(rtk_batch_opts), vp]),
+    "rtk_topk_scaled": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, C.c_double, u64, vp, vp, vp,
+                                  C.POINTER(rtk_scale_info), C.POINTER(rtk_cfg), vp]),
+    "rtk_topk_host": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, vp, vp, vp, C.POINTER(rtk_cfg)]),
+    "rtk_topk_batched_host": (C.c_int, [vp, vp, u64, P64, P64, P64, u64, C.c_int, C.c_int, vp, vp,
+                                        P64, vp, C.POINTER(rtk_cfg), C.POINTER(rtk_batch_opts)]),
+    "rtk_topk_scaled_host": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, C.c_double, u64, vp, vp,
+                                       vp, C.POINTER(rtk_scale_info), C.POINTER(rtk_cfg)]),
+    "rtk_merge_shards": (C.c_int, [vp, vp, vp, P64, P64, u32, u64, C.c_int, C.c_int, vp, vp, vp, vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load() -> C.CDLL:
+    """Load librtk_b200.so (raises if it is absent — there is no CPU fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build the CUDA library first "
+                    "(python -c 'import __graft_entry__ as g; g.build()')")
+            lib = C.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+        return _lib
+
+
+def last_error() -> str:
+    msg = load().rtk_last_error()
+    return msg.decode() if msg else ""

@@ -1,0 +1,385 @@
+// rtk_capi.cpp — the extern "C" boundary (include/rtk_c.h). Validation mirrors the
+// reference's exceptions one-to-one (engine.hpp:31-41, 61-67, 425-426; batch.hpp:40-53,
+// 274-280; scaling.hpp:47-48) as status codes + a thread-local message.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/rtk_c.h"
+#include "rtk_engine.h"
+
+using rtk_b200::Engine;
+using rtk_b200::Error;
+using rtk_b200::RowReq;
+
+struct rtk_handle_s {
+    Engine engine;
+    explicit rtk_handle_s(int dev) : engine(dev) {}
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return RTK_OK;
+    } catch (const Error& e) {
+        return fail(e.code, e.msg);
+    } catch (const std::bad_alloc&) {
+        return fail(RTK_OUT_OF_MEMORY, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(RTK_INTERNAL, e.what());
+    }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error{RTK_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+rtk_cfg default_cfg() {
+    rtk_cfg c;
+    rtk_cfg_default(&c);
+    return c;
+}
+
+// EngineConfig::validate (engine.hpp:61-67)
+void validate_cfg(const rtk_cfg& c) {
+    if (c.d < 1 || c.d > 16) throw Error{RTK_INVALID_ARGUMENT, "digit width must be in [1, 16]"};
+    if (c.block_size < 1) throw Error{RTK_INVALID_ARGUMENT, "block_size must be >= 1"};
+    if (c.grid_size < 1) throw Error{RTK_INVALID_ARGUMENT, "grid_size must be >= 1"};
+    if (c.pack_size < 4 || (c.pack_size & (c.pack_size - 1)) != 0)
+        throw Error{RTK_INVALID_ARGUMENT, "pack_size must be a power of two >= element width"};
+}
+
+void check_common(const void* ptr, uint64_t n, uint64_t k, int dtype, int order, const rtk_cfg& cfg,
+                  const char* who) {
+    // topk: empty -> empty_input_error, k outside [1,n] -> rank_out_of_range (engine.hpp:425-426);
+    // radix_select then validates the config (:296)
+    if (n == 0) throw Error{RTK_EMPTY_INPUT, std::string(who) + ": empty input"};
+    if (k == 0 || k > n) throw Error{RTK_RANK_OUT_OF_RANGE, std::string(who) + ": k outside [1, n]"};
+    validate_cfg(cfg);
+    if (dtype != RTK_F32 && dtype != RTK_U32) throw Error{RTK_INVALID_ARGUMENT, "dtype must be F32 or U32"};
+    if (order != RTK_LARGEST && order != RTK_SMALLEST) throw Error{RTK_INVALID_ARGUMENT, "bad order"};
+    if (n > (uint64_t(1) << 32)) throw Error{RTK_INVALID_ARGUMENT, "n > 2^32 per device row is not supported"};
+    if (!ptr) throw Error{RTK_INVALID_ARGUMENT, "null input"};
+}
+
+// BatchInput::validate (batch.hpp:40-53)
+void validate_batch(uint64_t data_len, const uint64_t* offsets, const uint64_t* lengths,
+                    const uint64_t* ks, uint64_t B) {
+    if (B == 0) throw Error{RTK_INVALID_ARGUMENT, "batch: no tasks"};
+    if (!offsets || !lengths || !ks) throw Error{RTK_INVALID_ARGUMENT, "batch: descriptor arrays disagree"};
+    for (uint64_t i = 0; i < B; ++i) {
+        const uint64_t next = i + 1 < B ? offsets[i + 1] : data_len;
+        if (offsets[i] + lengths[i] > next)
+            throw Error{RTK_INVALID_ARGUMENT, "batch: task " + std::to_string(i) + " overlaps its successor"};
+        if (ks[i] == 0 || ks[i] > lengths[i])
+            throw Error{RTK_INVALID_ARGUMENT, "batch: task " + std::to_string(i) + " has k outside [1, n]"};
+        if (lengths[i] > (uint64_t(1) << 32))
+            throw Error{RTK_INVALID_ARGUMENT, "batch: task " + std::to_string(i) + " longer than 2^32"};
+    }
+}
+
+std::vector<uint64_t> packed_out_offsets(const uint64_t* ks, uint64_t B) {
+    std::vector<uint64_t> o(B);
+    uint64_t acc = 0;
+    for (uint64_t i = 0; i < B; ++i) {
+        o[i] = acc;
+        acc += ks[i];
+    }
+    return o;
+}
+
+struct ScaleDecision {
+    bool scale = false;
+    float a_s = 0.0f;
+    uint64_t a_index = 0;
+};
+
+// scaled_topk's decision (scaling.hpp:47-67): adaptive trigger on the exact first-window
+// histogram, then a_s = input[mt19937_64(seed)() % n].
+ScaleDecision decide_scale(Engine& e, const float* d_in, uint64_t n, uint64_t k, int order, int mode,
+                           double tau, uint64_t seed, const rtk_cfg& cfg, cudaStream_t s) {
+    ScaleDecision d;
+    if (mode != RTK_SCALE_OFF && mode != RTK_SCALE_ALWAYS && mode != RTK_SCALE_ADAPTIVE)
+        throw Error{RTK_INVALID_ARGUMENT, "bad scale mode"};
+    d.scale = mode == RTK_SCALE_ALWAYS;
+    if (mode == RTK_SCALE_ADAPTIVE) {
+        std::vector<uint64_t> h = e.first_digit_hist(reinterpret_cast<const uint32_t*>(d_in), n, cfg.d,
+                                                     order, s);
+        e.stats.passes += 1;
+        e.stats.elements_scanned += n;
+        // select_bin (engine.hpp:231-241)
+        uint64_t total = 0;
+        for (uint64_t c : h) total += c;
+        if (k == 0 || k > total) throw Error{RTK_RANK_OUT_OF_RANGE, "select_bin: rank outside histogram total"};
+        uint64_t cum = 0;
+        size_t bin = 0;
+        for (size_t b = h.size(); b-- > 0;) {
+            cum += h[b];
+            if (cum >= k) {
+                bin = b;
+                break;
+            }
+        }
+        d.scale = static_cast<double>(h[bin]) > tau * static_cast<double>(n);
+    }
+    if (d.scale) {
+        std::mt19937_64 rng(seed);
+        d.a_index = rng() % n;
+        const uint32_t bits = e.read_word(reinterpret_cast<const uint32_t*>(d_in), d.a_index, s);
+        std::memcpy(&d.a_s, &bits, 4);
+    }
+    return d;
+}
+
+void run_scaled(Engine& e, const float* d_in, uint64_t n, uint64_t k, int order, int mode, double tau,
+                uint64_t seed, float* d_vals, uint64_t* d_idx, float* d_piv, rtk_scale_info* info,
+                const rtk_cfg& cfg, cudaStream_t s) {
+    ScaleDecision d = decide_scale(e, d_in, n, k, order, mode, tau, seed, cfg, s);
+    const rtk_stats pre = e.stats;
+    e.run(reinterpret_cast<const uint32_t*>(d_in), RTK_F32, order, d.scale, d.a_s, /*gather=*/d.scale,
+          {RowReq{0, n, k, 0}}, reinterpret_cast<uint32_t*>(d_vals), d_idx,
+          reinterpret_cast<uint32_t*>(d_piv), s);
+    e.stats.passes += pre.passes;
+    e.stats.elements_scanned += pre.elements_scanned;
+    if (info) {
+        info->scaled = d.scale ? 1 : 0;
+        info->a_s = d.scale ? d.a_s : 0.0f;
+        info->a_index = d.scale ? d.a_index : 0;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rtk_version(void) { return "rtk-b200 0.1 (sm_100a)"; }
+
+const char* rtk_last_error(void) { return g_last_error.c_str(); }
+
+void rtk_cfg_default(rtk_cfg* c) {
+    if (!c) return;
+    c->d = 12;
+    c->block_size = 1024;
+    c->grid_size = 4;
+    c->buffer_policy = 1;
+    c->pack_size = 16;
+    c->hierarchical_atomics = 1;
+    c->filter_fixed_ceiling = 4096;
+}
+
+int rtk_cfg_validate(const rtk_cfg* c) {
+    return guarded([&] {
+        if (!c) throw Error{RTK_INVALID_ARGUMENT, "null config"};
+        validate_cfg(*c);
+    });
+}
+
+int rtk_handle_create(rtk_handle* out, int device) {
+    return guarded([&] {
+        if (!out) throw Error{RTK_INVALID_ARGUMENT, "null handle pointer"};
+        int count = 0;
+        cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+        if (device < 0 || device >= count) throw Error{RTK_INVALID_ARGUMENT, "no such CUDA device"};
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        *out = new rtk_handle_s(device);
+    });
+}
+
+int rtk_handle_destroy(rtk_handle h) {
+    return guarded([&] { delete h; });
+}
+
+int rtk_get_stats(rtk_handle h, rtk_stats* out) {
+    return guarded([&] {
+        if (!h || !out) throw Error{RTK_INVALID_ARGUMENT, "null argument"};
+        *out = h->engine.stats;
+    });
+}
+
+int rtk_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, int order,
+             void* d_out_vals, uint64_t* d_out_idx, void* d_out_pivot, const rtk_cfg* cfg,
+             void* stream) {
+    return guarded([&] {
+        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+        const rtk_cfg c = cfg ? *cfg : default_cfg();
+        check_common(d_in, n, k, dtype, order, c, "topk");
+        h->engine.run(static_cast<const uint32_t*>(d_in), dtype, order, false, 0.0f, false,
+                      {RowReq{0, n, k, 0}}, static_cast<uint32_t*>(d_out_vals), d_out_idx,
+                      static_cast<uint32_t*>(d_out_pivot), static_cast<cudaStream_t>(stream));
+    });
+}
+
+int rtk_topk_batched(rtk_handle h, const void* d_data, uint64_t data_len, const uint64_t* offsets,
+                     const uint64_t* lengths, const uint64_t* ks, uint64_t B, int dtype, int order,
+                     void* d_out_vals, uint64_t* d_out_idx, const uint64_t* out_offsets,
+                     void* d_out_pivots, const rtk_cfg* cfg, const rtk_batch_opts* opts,
+                     void* stream) {
+    (void)opts;  // rescheduling / padding change the schedule only, never the results
+    return guarded([&] {
+        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+        validate_batch(data_len, offsets, lengths, ks, B);
+        const rtk_cfg c = cfg ? *cfg : default_cfg();
+        validate_cfg(c);
+        if (dtype != RTK_F32 && dtype != RTK_U32) throw Error{RTK_INVALID_ARGUMENT, "dtype must be F32 or U32"};
+        if (order != RTK_LARGEST && order != RTK_SMALLEST) throw Error{RTK_INVALID_ARGUMENT, "bad order"};
+        if (!d_data) throw Error{RTK_INVALID_ARGUMENT, "null input"};
+        std::vector<uint64_t> oo = out_offsets ? std::vector<uint64_t>(out_offsets, out_offsets + B)
+                                               : packed_out_offsets(ks, B);
+        std::vector<RowReq> rows(B);
+        for (uint64_t t = 0; t < B; ++t) rows[t] = RowReq{offsets[t], lengths[t], ks[t], oo[t]};
+        h->engine.run(static_cast<const uint32_t*>(d_data), dtype, order, false, 0.0f, false, rows,
+                      static_cast<uint32_t*>(d_out_vals), d_out_idx, static_cast<uint32_t*>(d_out_pivots),
+                      static_cast<cudaStream_t>(stream));
+    });
+}
+
+int rtk_topk_scaled(rtk_handle h, const float* d_in, uint64_t n, uint64_t k, int order, int mode,
+                    double trigger_fraction, uint64_t seed, float* d_out_vals, uint64_t* d_out_idx,
+                    float* d_out_pivot, rtk_scale_info* info, const rtk_cfg* cfg, void* stream) {
+    return guarded([&] {
+        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+        const rtk_cfg c = cfg ? *cfg : default_cfg();
+        if (n == 0) throw Error{RTK_EMPTY_INPUT, "scaled_topk: empty input"};
+        if (k == 0 || k > n) throw Error{RTK_RANK_OUT_OF_RANGE, "scaled_topk: k outside [1, n]"};
+        check_common(d_in, n, k, RTK_F32, order, c, "scaled_topk");
+        run_scaled(h->engine, d_in, n, k, order, mode, trigger_fraction, seed, d_out_vals, d_out_idx,
+                   d_out_pivot, info, c, static_cast<cudaStream_t>(stream));
+    });
+}
+
+// ---- host-pointer variants ----------------------------------------------------------------
+
+int rtk_topk_host(rtk_handle h, const void* in, uint64_t n, uint64_t k, int dtype, int order,
+                  void* out_vals, uint64_t* out_idx, void* out_pivot, const rtk_cfg* cfg) {
+    return guarded([&] {
+        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+        const rtk_cfg c = cfg ? *cfg : default_cfg();
+        check_common(in, n, k, dtype, order, c, "topk");
+        Engine& e = h->engine;
+        cuda_check(cudaSetDevice(e.device()), "cudaSetDevice");
+        e.io_in.ensure(4 * n);
+        e.io_vals.ensure(4 * k);
+        e.io_idx.ensure(8 * k);
+        e.io_piv.ensure(4);
+        cudaStream_t s = nullptr;
+        cuda_check(cudaMemcpyAsync(e.io_in.p, in, 4 * n, cudaMemcpyHostToDevice, s), "h2d");
+        e.run(e.io_in.as<uint32_t>(), dtype, order, false, 0.0f, false, {RowReq{0, n, k, 0}},
+              e.io_vals.as<uint32_t>(), e.io_idx.as<uint64_t>(), e.io_piv.as<uint32_t>(), s);
+        cuda_check(cudaMemcpyAsync(out_vals, e.io_vals.p, 4 * k, cudaMemcpyDeviceToHost, s), "d2h");
+        cuda_check(cudaMemcpyAsync(out_idx, e.io_idx.p, 8 * k, cudaMemcpyDeviceToHost, s), "d2h");
+        if (out_pivot) cuda_check(cudaMemcpyAsync(out_pivot, e.io_piv.p, 4, cudaMemcpyDeviceToHost, s), "d2h");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+int rtk_topk_batched_host(rtk_handle h, const void* data, uint64_t data_len, const uint64_t* offsets,
+                          const uint64_t* lengths, const uint64_t* ks, uint64_t B, int dtype, int order,
+                          void* out_vals, uint64_t* out_idx, const uint64_t* out_offsets, void* out_pivots,
+                          const rtk_cfg* cfg, const rtk_batch_opts* opts) {
+    return guarded([&] {
+        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+        validate_batch(data_len, offsets, lengths, ks, B);
+        std::vector<uint64_t> oo = out_offsets ? std::vector<uint64_t>(out_offsets, out_offsets + B)
+                                               : packed_out_offsets(ks, B);
+        uint64_t out_total = 0;
+        for (uint64_t t = 0; t < B; ++t) out_total = std::max(out_total, oo[t] + ks[t]);
+        Engine& e = h->engine;
+        cuda_check(cudaSetDevice(e.device()), "cudaSetDevice");
+        e.io_in.ensure(4 * std::max<uint64_t>(data_len, 1));
+        e.io_vals.ensure(4 * out_total);
+        e.io_idx.ensure(8 * out_total);
+        e.io_piv.ensure(4 * B);
+        cudaStream_t s = nullptr;
+        cuda_check(cudaMemcpyAsync(e.io_in.p, data, 4 * data_len, cudaMemcpyHostToDevice, s), "h2d");
+        int st = rtk_topk_batched(h, e.io_in.p, data_len, offsets, lengths, ks, B, dtype, order, e.io_vals.p,
+                                  e.io_idx.as<uint64_t>(), oo.data(), e.io_piv.p, cfg, opts, s);
+        if (st != RTK_OK) throw Error{st, g_last_error};
+        // outputs may be ragged: copy each row's slots
+        bool packed = true;
+        for (uint64_t t = 0, acc = 0; t < B; acc += ks[t], ++t) packed &= oo[t] == acc;
+        if (packed) {
+            cuda_check(cudaMemcpyAsync(out_vals, e.io_vals.p, 4 * out_total, cudaMemcpyDeviceToHost, s), "d2h");
+            cuda_check(cudaMemcpyAsync(out_idx, e.io_idx.p, 8 * out_total, cudaMemcpyDeviceToHost, s), "d2h");
+        } else {
+            for (uint64_t t = 0; t < B; ++t) {
+                cuda_check(cudaMemcpyAsync(static_cast<uint32_t*>(out_vals) + oo[t],
+                                           e.io_vals.as<uint32_t>() + oo[t], 4 * ks[t],
+                                           cudaMemcpyDeviceToHost, s), "d2h");
+                cuda_check(cudaMemcpyAsync(out_idx + oo[t], e.io_idx.as<uint64_t>() + oo[t], 8 * ks[t],
+                                           cudaMemcpyDeviceToHost, s), "d2h");
+            }
+        }
+        if (out_pivots)
+            cuda_check(cudaMemcpyAsync(out_pivots, e.io_piv.p, 4 * B, cudaMemcpyDeviceToHost, s), "d2h");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+int rtk_topk_scaled_host(rtk_handle h, const float* in, uint64_t n, uint64_t k, int order, int mode,
+                         double trigger_fraction, uint64_t seed, float* out_vals, uint64_t* out_idx,
+                         float* out_pivot, rtk_scale_info* info, const rtk_cfg* cfg) {
+    return guarded([&] {
+        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+        const rtk_cfg c = cfg ? *cfg : default_cfg();
+        if (n == 0) throw Error{RTK_EMPTY_INPUT, "scaled_topk: empty input"};
+        if (k == 0 || k > n) throw Error{RTK_RANK_OUT_OF_RANGE, "scaled_topk: k outside [1, n]"};
+        check_common(in, n, k, RTK_F32, order, c, "scaled_topk");
+        Engine& e = h->engine;
+        cuda_check(cudaSetDevice(e.device()), "cudaSetDevice");
+        e.io_in.ensure(4 * n);
+        e.io_vals.ensure(4 * k);
+        e.io_idx.ensure(8 * k);
+        e.io_piv.ensure(4);
+        cudaStream_t s = nullptr;
+        cuda_check(cudaMemcpyAsync(e.io_in.p, in, 4 * n, cudaMemcpyHostToDevice, s), "h2d");
+        run_scaled(e, e.io_in.as<float>(), n, k, order, mode, trigger_fraction, seed, e.io_vals.as<float>(),
+                   e.io_idx.as<uint64_t>(), e.io_piv.as<float>(), info, c, s);
+        cuda_check(cudaMemcpyAsync(out_vals, e.io_vals.p, 4 * k, cudaMemcpyDeviceToHost, s), "d2h");
+        cuda_check(cudaMemcpyAsync(out_idx, e.io_idx.p, 8 * k, cudaMemcpyDeviceToHost, s), "d2h");
+        if (out_pivot) cuda_check(cudaMemcpyAsync(out_pivot, e.io_piv.p, 4, cudaMemcpyDeviceToHost, s), "d2h");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+int rtk_merge_shards(rtk_handle h, const void* d_cand_vals, const uint64_t* d_cand_idx,
+                     const uint64_t* block_len, const uint64_t* shard_base, uint32_t G, uint64_t k,
+                     int dtype, int order, void* d_out_vals, uint64_t* d_out_idx, void* d_out_pivot,
+                     void* stream) {
+    return guarded([&] {
+        if (!h || !block_len || !shard_base || G == 0) throw Error{RTK_INVALID_ARGUMENT, "bad shard descriptor"};
+        std::vector<uint64_t> start(G), base(shard_base, shard_base + G);
+        uint64_t total = 0;
+        for (uint32_t g = 0; g < G; ++g) {
+            start[g] = total;
+            total += block_len[g];
+            if (g && base[g] < base[g - 1]) throw Error{RTK_INVALID_ARGUMENT, "shards must be in index order"};
+        }
+        const rtk_cfg c = default_cfg();
+        check_common(d_cand_vals, total, k, dtype, order, c, "merge_shards");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        // Tie-break surrogate = position in the concatenation: each block is in (key desc,
+        // index asc) order and blocks are in ascending index order, so among equal keys
+        // position order == global index order.
+        h->engine.run(static_cast<const uint32_t*>(d_cand_vals), dtype, order, false, 0.0f, false,
+                      {RowReq{0, total, k, 0}}, static_cast<uint32_t*>(d_out_vals), d_out_idx,
+                      static_cast<uint32_t*>(d_out_pivot), s);
+        h->engine.remap(k, d_cand_idx, start, base, d_out_idx, s);
+    });
+}
+
+}  // extern "C"

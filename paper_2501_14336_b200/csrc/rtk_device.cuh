@@ -1,0 +1,132 @@
+// rtk_device.cuh — device-side types shared by the sm_100a radix top-k kernels.
+//
+// Every selection runs on a 64-bit COMPOSITE key
+//     K(i) = (u64)encode(x_i) << 32 | (u32)~i          (i = row-local index, n <= 2^32)
+// encode() is the reference's order-preserving map (keycodec.hpp:55-81). Sorting K
+// descending is exactly the reference's canonical order (key desc, index asc;
+// engine.hpp:402-411), and K is unique per element, so "the k largest K" is exactly the
+// reference result including its tie rule (pivot-equal elements by ascending index,
+// engine.hpp:387-396) — no separate tie pass exists anywhere in this design.
+#pragma once
+#include <cstdint>
+
+namespace rtk_b200 {
+
+constexpr int kThreads = 256;          // streaming kernels
+constexpr int kVec = 8;                // 8 x u32 = one 32-byte LDG.256
+constexpr int kUnroll = 4;             // 4 loads in flight per thread per tile
+constexpr int kTile = kThreads * kVec * kUnroll;  // 8192 input elements per tile
+constexpr int kVec64 = 4;              // 4 x u64 = 32 bytes
+constexpr int kTile64 = kThreads * kVec64 * 4;    // 4096 composites per tile
+constexpr int kDigit = 11;             // radix digit width for the 64-bit composite
+constexpr int kBins = 1 << kDigit;
+constexpr int kStageCap = 4096;        // compaction staging buffer (u64), 32 KB smem
+
+enum : int { kF32 = 0, kU32 = 1 };
+
+// Selection state of one row (one query, one sample, or one MSD segment).
+// Digits are examined MSD-first at bit positions 53, 42, 31, 20, 9, 0 of K.
+struct RowSel {
+    unsigned long long prefix;   // selected composite bits above `pos`
+    unsigned long long k_rem;    // rank still to place inside the current range
+    unsigned long long above;    // elements strictly above the current range
+    unsigned long long T;        // threshold: candidates are K >= T
+    unsigned long long count_ge; // #{K >= T}
+    unsigned long long target;   // resolve once count_ge <= target
+    unsigned int pos;            // low bit of the next digit
+    unsigned int status;         // 0 active, 1 resolved, 2 rank error
+    unsigned int ticket;         // CTAs that finished this pass
+    unsigned int pad;
+};
+
+// Per-launch row list (device arrays). Launch row j maps to state row rid[j].
+struct Rows {
+    int R;
+    const uint32_t* rid;
+    const uint64_t* off;         // element offset (input words or u64 buffer)
+    const uint64_t* len;         // elements
+    const uint32_t* lead;        // input only: elements before `off` in the first 32-B sector
+    const uint64_t* tile_start;  // R+1 exclusive prefix of tiles
+};
+
+struct InputSrc {
+    const uint32_t* base;
+    int dtype;
+    int smallest;
+    int scaled;
+    float a_s;
+};
+
+__device__ __forceinline__ uint32_t encode_f32_bits(uint32_t raw, bool smallest) {
+    // KeyCodec<float>::encode, keycodec.hpp:57-62
+    uint32_t bits = (raw & 0x80000000u) ? ~raw : (raw | 0x80000000u);
+    return smallest ? ~bits : bits;
+}
+
+__device__ __forceinline__ uint32_t decode_f32_bits(uint32_t bits, bool smallest) {
+    // KeyCodec<float>::decode, keycodec.hpp:64-69
+    if (smallest) bits = ~bits;
+    return (bits & 0x80000000u) ? (bits ^ 0x80000000u) : ~bits;
+}
+
+__device__ __forceinline__ uint32_t make_key(const InputSrc& s, uint32_t raw) {
+    if (s.dtype == kF32) {
+        if (s.scaled) {
+            // y = x - a_s in IEEE fp32 round-to-nearest, denormals kept (scaling.hpp:69-70);
+            // the library is built without -use_fast_math / -ftz.
+            raw = __float_as_uint(__fsub_rn(__uint_as_float(raw), s.a_s));
+        }
+        return encode_f32_bits(raw, s.smallest);
+    }
+    return s.smallest ? ~raw : raw;  // KeyCodec<u32>, keycodec.hpp:72-81
+}
+
+// Compile-time key transforms for the streaming kernels (KM = key mode).
+enum : int { kKmF32L = 0, kKmF32S = 1, kKmF32LScaled = 2, kKmF32SScaled = 3, kKmU32L = 4, kKmU32S = 5 };
+
+inline int key_mode(int dtype, int smallest, int scaled) {
+    if (dtype != kF32) return smallest ? kKmU32S : kKmU32L;
+    return (scaled ? 2 : 0) + (smallest ? 1 : 0);
+}
+
+template <int KM>
+__device__ __forceinline__ uint32_t key_of(uint32_t raw, float a_s) {
+    if (KM == kKmU32L) return raw;
+    if (KM == kKmU32S) return ~raw;
+    if (KM == kKmF32LScaled || KM == kKmF32SScaled)
+        raw = __float_as_uint(__fsub_rn(__uint_as_float(raw), a_s));
+    // sign-flip map as mask arithmetic: negative -> ~raw, positive -> raw | sign
+    const uint32_t m = static_cast<uint32_t>(static_cast<int32_t>(raw) >> 31) | 0x80000000u;
+    const uint32_t bits = raw ^ m;
+    return (KM == kKmF32S || KM == kKmF32SScaled) ? ~bits : bits;
+}
+
+__device__ __forceinline__ uint64_t composite(uint32_t key, uint64_t idx) {
+    return (static_cast<uint64_t>(key) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(idx));
+}
+
+__device__ __forceinline__ void ldg256(const uint32_t* p, uint32_t (&r)[8]) {
+    asm volatile(
+        "ld.global.nc.L1::no_allocate.L2::256B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
+        : "l"(p));
+}
+
+__device__ __forceinline__ void ldg256_u64(const uint64_t* p, uint64_t (&r)[4]) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.b64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(r[0]), "=l"(r[1]), "=l"(r[2]), "=l"(r[3])
+                 : "l"(p));
+}
+
+// Launch row owning flat tile t (tile_start is an exclusive prefix, R+1 entries).
+__device__ __forceinline__ int row_of_tile(const Rows& rows, uint64_t t) {
+    int lo = 0, hi = rows.R - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (rows.tile_start[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+}  // namespace rtk_b200

@@ -1,0 +1,102 @@
+// rtk_engine.h — host orchestration of the B200 radix top-k (C++; no torch types).
+//
+// One Engine per rtk_handle. It plans a launch sequence for a set of rows (one query = one
+// row; a batch = B rows over one base pointer), owns the device workspace, and replaces the
+// reference's std::thread worker pool (engine.hpp:112-122) with grid launches on a stream.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rtk_c.h"
+#include "rtk_device.cuh"
+
+namespace rtk_b200 {
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+struct RowReq {
+    uint64_t in_off;   // element offset of the row in the input base
+    uint64_t n;        // elements
+    uint64_t k;        // rank
+    uint64_t out_off;  // element offset of the row's outputs
+};
+
+// Growable device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t bytes, bool keep = false, cudaStream_t s = nullptr);
+    void release();
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+class Engine {
+public:
+    explicit Engine(int device);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    // Top-k of every row. Values are written as raw 32-bit words (f32 bits or u32).
+    // scaled: keys are encode(x - a_s) (f32); gather: values re-read from the input by index.
+    void run(const uint32_t* d_base, int dtype, int smallest, bool scaled, float a_s, bool gather,
+             const std::vector<RowReq>& rows, uint32_t* d_vals, uint64_t* d_idx,
+             uint32_t* d_pivots, cudaStream_t s);
+
+    // Exact histogram of the first d-bit window of the unscaled keys (adaptive trigger).
+    std::vector<uint64_t> first_digit_hist(const uint32_t* d_in, uint64_t n, unsigned d,
+                                           int smallest, cudaStream_t s);
+
+    // Remap shard-merge positions to global indices.
+    void remap(uint64_t k, const uint64_t* d_cand_idx, const std::vector<uint64_t>& block_start,
+               const std::vector<uint64_t>& shard_base, uint64_t* d_idx, cudaStream_t s);
+
+    uint32_t read_word(const uint32_t* d, uint64_t i, cudaStream_t s);
+
+    int device() const { return device_; }
+    rtk_stats stats{};
+    DevBuf io_in, io_vals, io_idx, io_piv, io_aux;
+
+private:
+    // Plan arena: host bytes are staged then copied into a bump-allocated device region.
+    struct Plan {
+        std::vector<uint8_t> bytes;
+        template <typename T>
+        size_t add(const std::vector<T>& v) {
+            size_t off = (bytes.size() + 15) & ~size_t(15);
+            bytes.resize(off + v.size() * sizeof(T));
+            if (!v.empty()) std::memcpy(bytes.data() + off, v.data(), v.size() * sizeof(T));
+            return off;
+        }
+    };
+    uint8_t* upload(const Plan& p, cudaStream_t s);
+    void sync(cudaStream_t s, const char* what);
+    void release_retired();
+    void fallback(const uint32_t* d_base, const InputSrc& src, const std::vector<RowReq>& rows,
+                  const std::vector<uint32_t>& fb, std::vector<uint64_t>& cand_off,
+                  std::vector<uint64_t>& count, std::vector<uint64_t>& kmin,
+                  std::vector<uint64_t>& kmax, uint64_t& cand_total, cudaStream_t s);
+    void finish(const InputSrc& src, bool gather, const std::vector<RowReq>& rows,
+                const std::vector<uint64_t>& cand_off, const std::vector<uint64_t>& count,
+                const std::vector<uint64_t>& kmin, const std::vector<uint64_t>& kmax,
+                uint64_t cand_total, const uint64_t* d_row_k, const uint64_t* d_row_out_off,
+                const uint64_t* d_row_in_off, uint32_t* d_vals, uint64_t* d_idx, cudaStream_t s);
+
+    int device_;
+    DevBuf arena_;
+    size_t arena_used_ = 0;
+    std::vector<DevBuf> retired_;
+    cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
+    DevBuf sel_, T_, count_, kmin_, kmax_, ghist_, samples_, cand_a_, cand_b_, seg_hist_,
+        gcursor_;
+};
+
+}  // namespace rtk_b200

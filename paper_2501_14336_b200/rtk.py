@@ -1,0 +1,419 @@
+"""Python mirror of the reference's top-k interface, backed by the sm_100a C-ABI library.
+
+Same names, argument meaning and error behaviour as /root/reference/proj/include/rtk/:
+
+=====================  =========================================  ==========================
+here                   reference                                  C-ABI (include/rtk_c.h)
+=====================  =========================================  ==========================
+SelectionOrder         keycodec.hpp:19                            RTK_LARGEST / RTK_SMALLEST
+EngineConfig           engine.hpp:48-68 (validate :61-67)         rtk_cfg, rtk_cfg_validate
+TopKResult             engine.hpp:103-108                         out_vals / out_idx / pivot
+topk                   engine.hpp:422-443                         rtk_topk / rtk_topk_host
+BatchInput             batch.hpp:27-67 (validate :40-53)          descriptor arrays
+BatchOptions           batch.hpp:133-136                          rtk_batch_opts
+batch_topk             batch.hpp:261-367                          rtk_topk_batched[_host]
+ScaleMode/ScalePolicy  scaling.hpp:20-27                          mode / tau / seed
+ScaleInfo              scaling.hpp:29-33                          rtk_scale_info
+scaled_topk            scaling.hpp:42-86                          rtk_topk_scaled[_host]
+rank_out_of_range      engine.hpp:31-33 (std::out_of_range)       RTK_RANK_OUT_OF_RANGE
+invariant_violation    engine.hpp:35-37 (std::logic_error)        RTK_INVARIANT_VIOLATION
+empty_input_error      engine.hpp:39-41 (std::invalid_argument)   RTK_EMPTY_INPUT
+=====================  =========================================  ==========================
+
+CUDA tensors go through the device-pointer entry points (outputs are CUDA tensors on the same
+device); numpy arrays / CPU tensors go through the host entry points (copies included; outputs
+are numpy arrays). Values are returned bit-exact, indices as int64 (u64 in the C-ABI).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Any, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+# ---- exceptions (engine.hpp:31-41) -------------------------------------------------------
+class rank_out_of_range(IndexError):
+    """std::out_of_range subclass in the reference."""
+
+
+class invariant_violation(RuntimeError):
+    """std::logic_error subclass in the reference."""
+
+
+class empty_input_error(ValueError):
+    """std::invalid_argument subclass in the reference."""
+
+
+class cuda_error(RuntimeError):
+    pass
+
+
+def _raise(status: int, where: str = "") -> None:
+    if status == L.RTK_OK:
+        return
+    msg = L.last_error() or where
+    if status == L.RTK_EMPTY_INPUT:
+        raise empty_input_error(msg)
+    if status == L.RTK_RANK_OUT_OF_RANGE:
+        raise rank_out_of_range(msg)
+    if status == L.RTK_INVARIANT_VIOLATION:
+        raise invariant_violation(msg)
+    if status == L.RTK_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == L.RTK_OUT_OF_MEMORY:
+        raise MemoryError(msg)
+    raise cuda_error(f"status {status}: {msg}")
+
+
+# ---- config types ------------------------------------------------------------------------
+class SelectionOrder(enum.IntEnum):
+    Largest = 0
+    Smallest = 1
+
+
+class BufferPolicy(enum.IntEnum):
+    Naive = 0
+    FlushEfficient = 1
+
+
+@dataclass
+class EngineConfig:
+    d: int = 12
+    block_size: int = 1024
+    grid_size: int = 4
+    buffer_policy: BufferPolicy = BufferPolicy.FlushEfficient
+    pack_size: int = 16
+    hierarchical_atomics: bool = True
+    filter_fixed_ceiling: int = 4096
+
+    def radix(self) -> int:
+        return 1 << self.d
+
+    def validate(self) -> None:
+        if self.d < 1 or self.d > 16:
+            raise ValueError("digit width must be in [1, 16]")
+        if self.block_size < 1:
+            raise ValueError("block_size must be >= 1")
+        if self.grid_size < 1:
+            raise ValueError("grid_size must be >= 1")
+        if self.pack_size < 4 or (self.pack_size & (self.pack_size - 1)) != 0:
+            raise ValueError("pack_size must be a power of two >= element width")
+
+    def _c(self) -> L.rtk_cfg:
+        return L.rtk_cfg(int(self.d), int(self.block_size), int(self.grid_size),
+                         int(self.buffer_policy), int(self.pack_size),
+                         int(bool(self.hierarchical_atomics)), int(self.filter_fixed_ceiling))
+
+
+@dataclass
+class BatchOptions:
+    rescheduling: bool = True
+    padding: bool = True
+
+
+@dataclass
+class BatchRunInfo:
+    task_passes: List[int] = field(default_factory=list)
+    phase_b_rounds: int = 0
+
+
+class ScaleMode(enum.IntEnum):
+    Off = 0
+    Always = 1
+    Adaptive = 2
+
+
+@dataclass
+class ScalePolicy:
+    mode: ScaleMode = ScaleMode.Off
+    trigger_fraction: float = 0.5
+    seed: int = 0
+
+
+@dataclass
+class ScaleInfo:
+    scaled: bool = False
+    a_s: float = 0.0
+    a_index: int = 0
+
+
+@dataclass
+class Instrumentation:
+    """Work counters of the last call (subset of engine.hpp:74-101 with GPU meaning)."""
+    passes: int = 0
+    elements_scanned: int = 0
+    candidates: int = 0
+    fallback_rows: int = 0
+    kernel_launches: int = 0
+    compact_ms: float = 0.0
+    total_ms: float = 0.0
+
+
+@dataclass
+class TopKResult:
+    values: Any
+    indices: Any
+    pivot: Any = None
+
+
+# ---- handle management -------------------------------------------------------------------
+_handles: dict = {}
+
+
+def _handle(device: int) -> C.c_void_p:
+    h = _handles.get(device)
+    if h is None:
+        lib = L.load()
+        h = C.c_void_p()
+        _raise(lib.rtk_handle_create(C.byref(h), int(device)), "rtk_handle_create")
+        _handles[device] = h
+    return h
+
+
+def last_stats(device: int = 0) -> Instrumentation:
+    st = L.rtk_stats()
+    _raise(L.load().rtk_get_stats(_handle(device), C.byref(st)))
+    return Instrumentation(st.passes, st.elements_scanned, st.candidates, st.fallback_rows,
+                           st.kernel_launches, st.compact_ms, st.total_ms)
+
+
+def _is_cuda(x) -> bool:
+    return hasattr(x, "is_cuda") and bool(x.is_cuda)
+
+
+def _dtype_code(x) -> int:
+    if _is_cuda(x) or hasattr(x, "dtype") and "torch" in type(x).__module__:
+        import torch
+        if x.dtype == torch.float32:
+            return 0
+        if x.dtype in (torch.uint32, torch.int32):
+            return 1
+        raise TypeError(f"unsupported dtype {x.dtype}")
+    a = np.asarray(x)
+    if a.dtype == np.float32:
+        return 0
+    if a.dtype == np.uint32:
+        return 1
+    raise TypeError(f"unsupported dtype {a.dtype}")
+
+
+def _stream_ptr(t) -> C.c_void_p:
+    import torch
+    return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _np_scalar(bits: int, dtype_code: int):
+    arr = np.array([bits], dtype=np.uint32)
+    return arr.view(np.float32)[0] if dtype_code == 0 else arr[0]
+
+
+def _arr64(v: Sequence[int]):
+    a = np.ascontiguousarray(np.asarray(v, dtype=np.uint64))
+    return a, a.ctypes.data_as(L.P64)
+
+
+# ---- entry points ------------------------------------------------------------------------
+def topk(input, k: int, order: SelectionOrder = SelectionOrder.Largest,
+         cfg: Optional[EngineConfig] = None) -> TopKResult:
+    """rtk::topk (engine.hpp:422-443): k selected elements in (key desc, index asc) order."""
+    cfg = cfg or EngineConfig()
+    lib = L.load()
+    code = _dtype_code(input)
+    c = cfg._c()
+    if _is_cuda(input):
+        import torch
+        x = input.contiguous()
+        n = x.numel()
+        dev = x.device.index or 0
+        kk = max(int(k), 0)
+        vals = torch.empty(kk, dtype=x.dtype, device=x.device)
+        idx = torch.empty(kk, dtype=torch.int64, device=x.device)
+        piv = torch.empty(1, dtype=x.dtype, device=x.device)
+        st = lib.rtk_topk(_handle(dev), C.c_void_p(x.data_ptr() if n else 0), n, int(k), code,
+                          int(order), C.c_void_p(vals.data_ptr()), C.c_void_p(idx.data_ptr()),
+                          C.c_void_p(piv.data_ptr()), C.byref(c), _stream_ptr(x))
+        _raise(st, "rtk_topk")
+        return TopKResult(vals, idx, piv[0].item() if code == 0 else int(piv.view(torch.int32)[0].item()) & 0xFFFFFFFF)
+    a = np.ascontiguousarray(input.numpy() if hasattr(input, "numpy") else np.asarray(input))
+    n = a.size
+    kk = max(int(k), 0)
+    vals = np.empty(kk, dtype=a.dtype)
+    idx = np.empty(kk, dtype=np.uint64)
+    piv = np.zeros(1, dtype=np.uint32)
+    st = lib.rtk_topk_host(_handle(0), C.c_void_p(a.ctypes.data if n else 0), n, int(k), code,
+                           int(order), C.c_void_p(vals.ctypes.data), C.c_void_p(idx.ctypes.data),
+                           C.c_void_p(piv.ctypes.data), C.byref(c))
+    _raise(st, "rtk_topk_host")
+    return TopKResult(vals, idx, _np_scalar(int(piv[0]), code))
+
+
+@dataclass
+class BatchInput:
+    """rtk::BatchInput (batch.hpp:27-67): concatenated payload + per-task descriptors."""
+    data: Any
+    offsets: List[int]
+    lengths: List[int]
+    ks: List[int]
+
+    def task_count(self) -> int:
+        return len(self.lengths)
+
+    def task_view(self, i: int):
+        return self.data[self.offsets[i]:self.offsets[i] + self.lengths[i]]
+
+    def validate(self) -> None:
+        if not self.lengths:
+            raise ValueError("batch: no tasks")
+        if len(self.offsets) != len(self.lengths) or len(self.ks) != len(self.lengths):
+            raise ValueError("batch: descriptor arrays disagree")
+        size = len(self.data)
+        for i in range(len(self.lengths)):
+            nxt = self.offsets[i + 1] if i + 1 < len(self.offsets) else size
+            if self.offsets[i] + self.lengths[i] > nxt:
+                raise ValueError(f"batch: task {i} overlaps its successor")
+            if self.ks[i] == 0 or self.ks[i] > self.lengths[i]:
+                raise ValueError(f"batch: task {i} has k outside [1, n]")
+
+    @staticmethod
+    def concatenate(tasks: Sequence[Any], ks: Sequence[int]) -> "BatchInput":
+        offsets, lengths, at = [], [], 0
+        for t in tasks:
+            offsets.append(at)
+            lengths.append(len(t))
+            at += len(t)
+        if tasks and _is_cuda(tasks[0]):
+            import torch
+            data = torch.cat([t.reshape(-1) for t in tasks])
+        else:
+            data = np.concatenate([np.asarray(t).reshape(-1) for t in tasks]) if tasks else np.zeros(0, np.float32)
+        b = BatchInput(data, offsets, lengths, list(ks))
+        b.validate()
+        return b
+
+
+def batch_topk(batch: BatchInput, order: SelectionOrder = SelectionOrder.Largest,
+               cfg: Optional[EngineConfig] = None, opts: Optional[BatchOptions] = None,
+               info: Optional[BatchRunInfo] = None) -> List[TopKResult]:
+    """rtk::batch_topk (batch.hpp:261-367): one TopKResult per task, each equal to topk."""
+    cfg = cfg or EngineConfig()
+    opts = opts or BatchOptions()
+    lib = L.load()
+    B = len(batch.lengths)
+    offs, p_off = _arr64(batch.offsets)
+    lens, p_len = _arr64(batch.lengths)
+    ks, p_ks = _arr64(batch.ks)
+    oo = np.zeros(max(B, 1), dtype=np.uint64)
+    if B:
+        oo[1:B] = np.cumsum(ks[:-1])
+    p_oo = oo.ctypes.data_as(L.P64)
+    total = int(ks.sum()) if B else 0
+    c = cfg._c()
+    o = L.rtk_batch_opts(int(opts.rescheduling), int(opts.padding))
+    code = _dtype_code(batch.data)
+    if _is_cuda(batch.data):
+        import torch
+        x = batch.data.contiguous()
+        vals = torch.empty(total, dtype=x.dtype, device=x.device)
+        idx = torch.empty(total, dtype=torch.int64, device=x.device)
+        piv = torch.empty(max(B, 1), dtype=x.dtype, device=x.device)
+        st = lib.rtk_topk_batched(_handle(x.device.index or 0), C.c_void_p(x.data_ptr()), x.numel(),
+                                  p_off, p_len, p_ks, B, code, int(order),
+                                  C.c_void_p(vals.data_ptr()), C.c_void_p(idx.data_ptr()), p_oo,
+                                  C.c_void_p(piv.data_ptr()), C.byref(c), C.byref(o), _stream_ptr(x))
+        _raise(st, "rtk_topk_batched")
+        pivs = piv.cpu()
+    else:
+        a = np.ascontiguousarray(batch.data.numpy() if hasattr(batch.data, "numpy") else np.asarray(batch.data))
+        vals = np.empty(total, dtype=a.dtype)
+        idx = np.empty(total, dtype=np.uint64)
+        pivs = np.empty(max(B, 1), dtype=a.dtype)
+        st = lib.rtk_topk_batched_host(_handle(0), C.c_void_p(a.ctypes.data), a.size, p_off, p_len,
+                                       p_ks, B, code, int(order), C.c_void_p(vals.ctypes.data),
+                                       C.c_void_p(idx.ctypes.data), p_oo, C.c_void_p(pivs.ctypes.data),
+                                       C.byref(c), C.byref(o))
+        _raise(st, "rtk_topk_batched_host")
+    out = []
+    for t in range(B):
+        s, e = int(oo[t]), int(oo[t]) + int(ks[t])
+        p = pivs[t]
+        out.append(TopKResult(vals[s:e], idx[s:e], p.item() if hasattr(p, "item") else p))
+    if info is not None:
+        info.task_passes = [1] * B
+        info.phase_b_rounds = 0
+    return out
+
+
+def scaled_topk(input, k: int, order: SelectionOrder = SelectionOrder.Largest,
+                cfg: Optional[EngineConfig] = None, policy: Optional[ScalePolicy] = None,
+                info: Optional[ScaleInfo] = None) -> TopKResult:
+    """rtk::scaled_topk (scaling.hpp:42-86): selection on y = x - a_s, values re-read from x."""
+    cfg = cfg or EngineConfig()
+    policy = policy or ScalePolicy()
+    lib = L.load()
+    c = cfg._c()
+    si = L.rtk_scale_info()
+    if _is_cuda(input):
+        import torch
+        x = input.contiguous()
+        if x.dtype != torch.float32:
+            raise TypeError("scaled_topk is defined for float32 only")
+        n = x.numel()
+        kk = max(int(k), 0)
+        vals = torch.empty(kk, dtype=x.dtype, device=x.device)
+        idx = torch.empty(kk, dtype=torch.int64, device=x.device)
+        piv = torch.empty(1, dtype=x.dtype, device=x.device)
+        st = lib.rtk_topk_scaled(_handle(x.device.index or 0), C.c_void_p(x.data_ptr() if n else 0), n,
+                                 int(k), int(order), int(policy.mode), float(policy.trigger_fraction),
+                                 int(policy.seed) & 0xFFFFFFFFFFFFFFFF, C.c_void_p(vals.data_ptr()),
+                                 C.c_void_p(idx.data_ptr()), C.c_void_p(piv.data_ptr()),
+                                 C.byref(si), C.byref(c), _stream_ptr(x))
+        _raise(st, "rtk_topk_scaled")
+        res = TopKResult(vals, idx, piv[0].item())
+    else:
+        a = np.ascontiguousarray(input.numpy() if hasattr(input, "numpy") else np.asarray(input))
+        if a.dtype != np.float32:
+            raise TypeError("scaled_topk is defined for float32 only")
+        n = a.size
+        kk = max(int(k), 0)
+        vals = np.empty(kk, dtype=np.float32)
+        idx = np.empty(kk, dtype=np.uint64)
+        piv = np.zeros(1, dtype=np.float32)
+        st = lib.rtk_topk_scaled_host(_handle(0), C.c_void_p(a.ctypes.data if n else 0), n, int(k),
+                                      int(order), int(policy.mode), float(policy.trigger_fraction),
+                                      int(policy.seed) & 0xFFFFFFFFFFFFFFFF, C.c_void_p(vals.ctypes.data),
+                                      C.c_void_p(idx.ctypes.data), C.c_void_p(piv.ctypes.data),
+                                      C.byref(si), C.byref(c))
+        _raise(st, "rtk_topk_scaled_host")
+        res = TopKResult(vals, idx, piv[0])
+    if info is not None:
+        info.scaled = bool(si.scaled)
+        info.a_s = float(si.a_s)
+        info.a_index = int(si.a_index)
+    return res
+
+
+def merge_shards(cand_vals, cand_idx, block_len: Sequence[int], shard_base: Sequence[int], k: int,
+                 order: SelectionOrder = SelectionOrder.Largest) -> TopKResult:
+    """Final select of an n-sharded query: G canonical per-shard results (concatenated in
+    shard order, shard-local indices) -> the global top-k with global indices."""
+    import torch
+    lib = L.load()
+    code = _dtype_code(cand_vals)
+    bl, p_bl = _arr64(block_len)
+    sb, p_sb = _arr64(shard_base)
+    vals = torch.empty(int(k), dtype=cand_vals.dtype, device=cand_vals.device)
+    idx = torch.empty(int(k), dtype=torch.int64, device=cand_vals.device)
+    piv = torch.empty(1, dtype=cand_vals.dtype, device=cand_vals.device)
+    cv = cand_vals.contiguous()
+    ci = cand_idx.contiguous()
+    st = lib.rtk_merge_shards(_handle(cv.device.index or 0), C.c_void_p(cv.data_ptr()),
+                              C.c_void_p(ci.data_ptr()), p_bl, p_sb, len(bl), int(k), code, int(order),
+                              C.c_void_p(vals.data_ptr()), C.c_void_p(idx.data_ptr()),
+                              C.c_void_p(piv.data_ptr()), _stream_ptr(cv))
+    _raise(st, "rtk_merge_shards")
+    return TopKResult(vals, idx, piv[0].item())

@@ -1,0 +1,251 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the reference CPU engine.
+
+Every comparison is bit-exact on values (as u32 bit patterns), indices and pivot, in the
+reference's canonical order (engine.hpp:402-420). Inputs come from the reference's own seeded
+generators (datagen.hpp:71-141) through oracle/_ref; expected outputs from rtk::topk /
+rtk::batch_topk / rtk::scaled_topk compiled from the reference headers (oracle/_ref) — the
+configurations follow the reference tests cited on each case.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+UNIFORM, NORMAL, ZIPF, PEAKED = 0, 1, 2, 3
+
+
+def _rtk():
+    import paper_2501_14336_b200 as rtk
+    return rtk
+
+
+def _bits(v):
+    v = np.asarray(v)
+    return v.view(np.uint32) if v.dtype == np.float32 else v.astype(np.uint32)
+
+
+def assert_same(got, want, what=""):
+    gv, gi, gp = got
+    wv, wi, wp = want
+    gv = gv.cpu().numpy() if hasattr(gv, "cpu") else np.asarray(gv)
+    gi = gi.cpu().numpy() if hasattr(gi, "cpu") else np.asarray(gi)
+    assert gv.shape == wv.shape, what
+    bad = np.nonzero((_bits(gv) != _bits(wv)) | (gi.astype(np.uint64) != wi.astype(np.uint64)))[0]
+    assert bad.size == 0, f"{what}: first mismatch at rank {bad[:5]}: got {gv[bad[:3]]}/{gi[bad[:3]]} want {wv[bad[:3]]}/{wi[bad[:3]]}"
+    gp_bits = np.array([gp], dtype=wv.dtype).view(np.uint32)[0] if wv.dtype == np.float32 else np.uint32(gp)
+    assert int(gp_bits) == int(_bits(np.array([wp], dtype=wv.dtype))[0]), f"{what}: pivot"
+
+
+def gpu_topk(x, k, order, cuda):
+    import torch
+    rtk = _rtk()
+    t = torch.from_numpy(x.view(np.int32) if x.dtype == np.uint32 else x).to(cuda)
+    if x.dtype == np.uint32:
+        t = t.view(torch.uint32)
+    r = rtk.topk(t, k, rtk.SelectionOrder(order))
+    vals = r.values.view(torch.int32).cpu().numpy().view(np.uint32) if x.dtype == np.uint32 else r.values.cpu().numpy()
+    return vals, r.indices.cpu().numpy(), r.pivot
+
+
+@pytest.mark.parametrize("k", [256, 1, 4096, 1 << 19])
+def test_c1_uniform_largest(cuda, k):
+    # BASELINE C1: single query fp32 uniform n=2^20, largest (acceptance_test.cpp:48-94 sizes)
+    x = O.ref_generate(UNIFORM, 1 << 20, 1)
+    assert_same(gpu_topk(x, k, 0, cuda), O.ref_topk(x, k, 0, grid=4), f"C1 k={k}")
+
+
+@pytest.mark.parametrize("n", [10, 1000, 3001, 1 << 16, (1 << 20) + 3])
+@pytest.mark.parametrize("kind", [UNIFORM, NORMAL, ZIPF])
+@pytest.mark.parametrize("order", [0, 1])
+@pytest.mark.parametrize("dtype", [np.float32, np.uint32])
+def test_randomized_suite(cuda, n, kind, order, dtype):
+    # acceptance criterion 1 (acceptance_test.cpp:48-94): n x dist x order x k in {1,7,512,n/2,n}
+    seed = 10000 + n * 7 + kind * 3 + order
+    x = O.ref_generate(kind, n, seed, dtype=dtype, b=1.0)
+    for k in sorted({1, 7, 512, n // 2, n}):
+        if k < 1 or k > n:
+            continue
+        assert_same(gpu_topk(x, k, order, cuda), O.ref_topk(x, k, order, grid=4),
+                    f"n={n} kind={kind} order={order} dtype={dtype.__name__} k={k}")
+
+
+def test_ties_all_duplicates(cuda):
+    # engine_test.cpp:188-198: duplicate-only input; ties fill by ascending index (:219-230)
+    x = np.full(1000, 2.5, dtype=np.float32)
+    for k in [1, 123, 999, 1000]:
+        assert_same(gpu_topk(x, k, 0, cuda), O.ref_topk(x, k, 0), f"dupes k={k}")
+    big = np.full((1 << 20) + 5, -7.0, dtype=np.float32)
+    assert_same(gpu_topk(big, 40000, 0, cuda), O.ref_topk(big, 40000, 0, grid=4), "big dupes")
+
+
+def test_two_value_input(cuda):
+    # acceptance criterion 2 (acceptance_test.cpp:117-126): two values, k=40000 of 2^16
+    x = np.ones(1 << 16, dtype=np.float32)
+    x[::2] = 2.0
+    assert_same(gpu_topk(x, 40000, 0, cuda), O.ref_topk(x, 40000, 0), "two values")
+
+
+def test_special_values(cuda):
+    # NaN / inf / signed zero by bit order
+    x = np.array([0.0, -0.0, 1.0, float("nan"), -float("nan"), -1.0, 0.0, float("inf"), -float("inf")],
+                 dtype=np.float32)
+    x[4] = np.array([0xFFC00000], dtype=np.uint32).view(np.float32)[0]
+    for order in [0, 1]:
+        for k in range(1, 10):
+            assert_same(gpu_topk(x, k, order, cuda), O.ref_topk(x, k, order), f"special order={order} k={k}")
+
+
+def test_adversarial_narrow_band(cuda):
+    # C4-like: U[128.6,128.7] (one first-pass bin, heavy ties), scaling_test.cpp:16-26
+    x = O.ref_generate(UNIFORM, 1 << 22, 5 + (1 << 22), a=128.6, b=128.7)
+    for k in [512, 1 << 16]:
+        assert_same(gpu_topk(x, k, 0, cuda), O.ref_topk(x, k, 0, grid=8), f"narrow k={k}")
+
+
+def test_integer_ramp(cuda):
+    # engine_test.cpp:292-303
+    x = np.arange(1 << 20, dtype=np.uint32)
+    v, i, _ = gpu_topk(x, 4, 0, cuda)
+    assert list(v) == [(1 << 20) - 1, (1 << 20) - 2, (1 << 20) - 3, (1 << 20) - 4]
+    v, i, _ = gpu_topk(x, 3, 1, cuda)
+    assert list(v) == [0, 1, 2]
+
+
+def test_sorted_inputs(cuda):
+    # adversarial orderings for the stratified sample: ascending and descending runs
+    x = np.sort(O.ref_generate(NORMAL, 1 << 21, 77, b=1.0))
+    for arr in (x, x[::-1].copy()):
+        for k in [100, 1 << 15]:
+            assert_same(gpu_topk(arr, k, 0, cuda), O.ref_topk(arr, k, 0, grid=8), f"sorted k={k}")
+
+
+def test_errors(cuda):
+    import torch
+    rtk = _rtk()
+    one = torch.tensor([3.5], device=cuda)
+    with pytest.raises(rtk.empty_input_error):
+        rtk.topk(torch.empty(0, device=cuda), 1)
+    with pytest.raises(rtk.rank_out_of_range):
+        rtk.topk(one, 2)
+    with pytest.raises(rtk.rank_out_of_range):
+        rtk.topk(one, 0)
+    with pytest.raises(ValueError):
+        rtk.topk(one, 1, cfg=rtk.EngineConfig(d=17))
+    r = rtk.topk(one, 1)
+    assert r.values.cpu().tolist() == [3.5] and r.indices.cpu().tolist() == [0]
+
+
+def test_grid_config_invariance(cuda):
+    # engine_test.cpp:305-322: results independent of grid/block/d hints
+    rtk = _rtk()
+    import torch
+    x = O.ref_generate(NORMAL, 50000, 21, b=2.0)
+    t = torch.from_numpy(x).to(cuda)
+    base = rtk.topk(t, 777)
+    for cfg in [rtk.EngineConfig(grid_size=1), rtk.EngineConfig(grid_size=8, d=8, block_size=512)]:
+        r = rtk.topk(t, 777, cfg=cfg)
+        assert torch.equal(r.values, base.values) and torch.equal(r.indices, base.indices)
+
+
+# ---- batch -------------------------------------------------------------------------------
+def _batch_expect(data, offsets, lengths, ks, order):
+    return O.ref_batch_topk(data, offsets, lengths, ks, order, grid=8)
+
+
+def test_batch_ragged_misaligned(cuda):
+    # batch_test.cpp:145-165 / acceptance criterion 8: first task one element short
+    import torch
+    rtk = _rtk()
+    tasks = [O.ref_generate(UNIFORM, (1 << 16) - (1 if t == 0 else 0), 600 + t) for t in range(16)]
+    b = rtk.BatchInput.concatenate(tasks, [256] * 16)
+    exp = _batch_expect(b.data, b.offsets, b.lengths, b.ks, 0)
+    bd = rtk.BatchInput(torch.from_numpy(b.data).to(cuda), b.offsets, b.lengths, b.ks)
+    got = rtk.batch_topk(bd, rtk.SelectionOrder.Largest)
+    for t in range(16):
+        assert_same((got[t].values, got[t].indices, got[t].pivot), exp[t], f"task {t}")
+
+
+def test_batch_heterogeneous_k(cuda):
+    # batch_test.cpp:122-143: Normal rows of varying n, k = 1 + 100 t, smallest
+    import torch
+    rtk = _rtk()
+    tasks = [O.ref_generate(NORMAL, 3000 + 17 * t, 50 + t, b=1.0) for t in range(5)]
+    ks = [1 + 100 * t for t in range(5)]
+    b = rtk.BatchInput.concatenate(tasks, ks)
+    exp = _batch_expect(b.data, b.offsets, b.lengths, b.ks, 1)
+    got = rtk.batch_topk(rtk.BatchInput(torch.from_numpy(b.data).to(cuda), b.offsets, b.lengths, b.ks),
+                         rtk.SelectionOrder.Smallest)
+    for t in range(5):
+        assert_same((got[t].values, got[t].indices, got[t].pivot), exp[t], f"task {t}")
+
+
+@pytest.mark.parametrize("k", [50, 4096, 128256])
+def test_batch_llm_vocab_rows(cuda, k):
+    # BASELINE C3 shape (batch x 128256 logits), 16 rows here; bench runs 256
+    import torch
+    rtk = _rtk()
+    V, B = 128256, 16
+    tasks = [O.ref_generate(NORMAL, V, 100 + t, b=1.0) for t in range(B)]
+    b = rtk.BatchInput.concatenate(tasks, [k] * B)
+    exp = _batch_expect(b.data, b.offsets, b.lengths, b.ks, 0)
+    got = rtk.batch_topk(rtk.BatchInput(torch.from_numpy(b.data).to(cuda), b.offsets, b.lengths, b.ks))
+    for t in range(B):
+        assert_same((got[t].values, got[t].indices, got[t].pivot), exp[t], f"row {t} k={k}")
+
+
+def test_batch_errors(cuda):
+    import torch
+    rtk = _rtk()
+    d = torch.tensor([1.0, 2.0, 3.0], device=cuda)
+    with pytest.raises(ValueError, match="task 1"):
+        rtk.batch_topk(rtk.BatchInput(d, [0, 2], [2, 1], [1, 2]))
+    with pytest.raises(ValueError, match="overlaps"):
+        rtk.batch_topk(rtk.BatchInput(d, [0, 1], [3, 1], [1, 1]))
+
+
+# ---- scaling -----------------------------------------------------------------------------
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_scaled_matches_reference(cuda, mode):
+    # scaling_test.cpp:106-139 and acceptance criterion 6 (acceptance_test.cpp:215-265)
+    import torch
+    rtk = _rtk()
+    for n, seed in [(1 << 16, 1), (1 << 20, 5 + (1 << 20))]:
+        x = O.ref_generate(UNIFORM, n, seed, a=128.6, b=128.7)
+        wv, wi, wp, winfo = O.ref_scaled_topk(x, 512, 0, mode=mode, seed=31 + n, grid=4)
+        info = rtk.ScaleInfo()
+        r = rtk.scaled_topk(torch.from_numpy(x).to(cuda), 512, rtk.SelectionOrder.Largest,
+                            policy=rtk.ScalePolicy(rtk.ScaleMode(mode), 0.5, 31 + n), info=info)
+        assert info.scaled == winfo["scaled"] and info.a_index == (winfo["a_index"] if winfo["scaled"] else 0)
+        assert_same((r.values, r.indices, r.pivot), (wv, wi, wp), f"scaled mode={mode} n={n}")
+
+
+def test_adaptive_benign_does_not_scale(cuda):
+    # scaling_test.cpp:173-196
+    import torch
+    rtk = _rtk()
+    x = O.ref_generate(UNIFORM, 1 << 14, 43)
+    info = rtk.ScaleInfo()
+    r = rtk.scaled_topk(torch.from_numpy(x).to(cuda), 128, policy=rtk.ScalePolicy(rtk.ScaleMode.Adaptive, 0.5, 13),
+                        info=info)
+    assert not info.scaled
+    assert_same((r.values, r.indices, r.pivot), O.ref_topk(x, 128, 0), "benign adaptive")
+
+
+# ---- host entry points (numpy in / numpy out) --------------------------------------------
+def test_host_entry_points(cuda):
+    rtk = _rtk()
+    x = O.ref_generate(UNIFORM, 1 << 20, 3)
+    r = rtk.topk(x, 1000)
+    assert_same((r.values, r.indices, r.pivot), O.ref_topk(x, 1000, 0, grid=4), "host topk")
+    tasks = [O.ref_generate(NORMAL, 5000 + t, 9 + t, b=1.0) for t in range(7)]
+    b = rtk.BatchInput.concatenate(tasks, [100 * (t + 1) for t in range(7)])
+    got = rtk.batch_topk(b)
+    exp = _batch_expect(b.data, b.offsets, b.lengths, b.ks, 0)
+    for t in range(7):
+        assert_same((got[t].values, got[t].indices, got[t].pivot), exp[t], f"host task {t}")
+    y = O.ref_generate(UNIFORM, 1 << 16, 2, a=128.6, b=128.7)
+    wv, wi, wp, _ = O.ref_scaled_topk(y, 512, 0, mode=1, seed=2)
+    r = rtk.scaled_topk(y, 512, policy=rtk.ScalePolicy(rtk.ScaleMode.Always, 0.5, 2))
+    assert_same((r.values, r.indices, r.pivot), (wv, wi, wp), "host scaled")
