@@ -23,8 +23,8 @@ namespace rtk_b200 {
 
 namespace {
 
-constexpr uint64_t kSmallSort = 16384;  // largest group one CTA sorts in shared memory
-constexpr uint64_t kGroupPack = 8192;   // consecutive small buckets are packed up to this
+constexpr uint64_t kSmallSort = 4096;   // largest group one CTA sorts in shared memory
+constexpr uint64_t kGroupPack = 2048;   // consecutive small buckets are packed up to this
 
 void check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)
@@ -144,7 +144,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         bool samp = q.k < q.n && q.n >= 2 * kSmallSort;
         uint64_t ns = 0, rp = 0;
         if (samp) {
-            ns = std::min<uint64_t>(uint64_t(1) << 20, std::max<uint64_t>(2048, q.n / 64)) & ~uint64_t(31);
+            ns = std::min<uint64_t>(uint64_t(1) << 18, std::max<uint64_t>(2048, q.n / 64)) & ~uint64_t(31);
             const double rr = static_cast<double>(q.k) * static_cast<double>(ns) / static_cast<double>(q.n);
             rp = static_cast<uint64_t>(std::ceil(rr + 4.0 * std::sqrt(rr) + 3.0));
             if (rp >= ns / 2) samp = false;
@@ -391,7 +391,7 @@ void Engine::finish(const InputSrc& src, bool gather, const std::vector<RowReq>&
         uint8_t* D = upload(P, s);
         const SortGroup* dg = at<SortGroup>(D, o);
         size_t i = 0;
-        for (uint64_t cls : {uint64_t(1024), uint64_t(4096), uint64_t(8192), kSmallSort}) {
+        for (uint64_t cls : {uint64_t(1024), uint64_t(2048), kSmallSort}) {
             size_t j = i;
             while (j < groups.size() && groups[j].len <= cls) ++j;
             if (j > i) {

@@ -127,8 +127,14 @@ __device__ __forceinline__ void hist_add(uint32_t* h, uint32_t digit, bool valid
     const bool v0 = __shfl_sync(full, valid ? 1 : 0, 0);
     if (__all_sync(full, valid && digit == d0) && v0) {
         if ((threadIdx.x & 31) == 0) atomicAdd(&h[d0], 32u);
-    } else if (valid) {
-        atomicAdd(&h[digit], 1u);
+    } else {
+        // clustered digits (e.g. the top digit of Uniform[0,1) keys lands in ~8 bins): one
+        // shared atomic per distinct digit of the warp instead of one per lane
+        const unsigned act = __ballot_sync(full, valid);
+        if (valid) {
+            const unsigned peers = __match_any_sync(act, digit);
+            if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[digit], __popc(peers));
+        }
     }
 }
 
@@ -361,80 +367,68 @@ __global__ void k_set_threshold(int R, const uint32_t* rid, const uint32_t* samp
 // k_compact<KM>: the single streaming pass over the input. Keeps K >= T[rid] (fused key
 // transform, compile-time per dtype/order/scale) into the row's candidate region.
 //
-// Matches are staged in shared memory: each warp reserves a contiguous slot range with ONE
-// shared atomic (warp-aggregated), and the CTA flushes the staging buffer to global memory
-// with ONE global cursor atomic per flush — the flush-efficient buffer (PAPER.md:454-485,
-// engine.hpp:138-169, flush when occupancy > half the buffer). There is no block barrier per
-// tile: occupancy is checked every kFlushEvery tiles; a warp whose reservation would overflow
-// the buffer writes its matches straight to global memory with its own cursor atomic.
+// Flush-efficient buffering (engine.hpp:138-169), made warp-private: each
+// warp owns a kWarpStage-entry slice of shared memory and a warp-uniform cursor. A hit slot is
+// appended with one ballot + popc (no atomics); when the slice is nearly full the warp claims
+// a contiguous range of the row's candidate region with ONE global cursor atomic and copies
+// the slice out. No block-wide barrier in the streaming loop — only at row boundaries.
+// Per element on the common (no-hit) path: key transform (2 ops) + compare + mask bit.
 // Counts are exact even past `cap` (writes beyond cap are dropped -> host falls back).
 // ----------------------------------------------------------------------------------------
-constexpr int kFlushEvery = 8;
+constexpr int kWarpStage = 512;
 
 template <int KM>
-__global__ void __launch_bounds__(kThreads, 3) k_compact(Rows rows, InputSrc in, const uint64_t* T,
-                                                      uint64_t* cand, const uint64_t* cand_off,
-                                                      const uint64_t* cap,
-                                                      unsigned long long* count,
-                                                      unsigned long long* kmin,
-                                                      unsigned long long* kmax) {
-    __shared__ unsigned long long stage[kStageCap];
-    __shared__ unsigned int s_resv, s_valid;
-    __shared__ unsigned long long s_base, s_min, s_max;
-
+__global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in, const uint64_t* T,
+                                                         uint64_t* cand, const uint64_t* cand_off,
+                                                         const uint64_t* cap,
+                                                         unsigned long long* count,
+                                                         unsigned long long* kmin,
+                                                         unsigned long long* kmax) {
+    __shared__ unsigned long long stage_all[kThreads / 32][kWarpStage];
     const uint64_t ntiles = rows.tile_start[rows.R];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned full = 0xffffffffu;
-    if (threadIdx.x == 0) { s_resv = 0; s_valid = 0; s_min = ~0ull; s_max = 0; }
-    __syncthreads();
+    const unsigned lt_mask = (1u << lane) - 1u;
+    unsigned long long* stage = stage_all[warp];
 
     int cur = -1;
-    unsigned long long thr = 0;
-    uint32_t thi = 0, tlo = 0;
+    unsigned long long thr = 0, mn = ~0ull, mx = 0;
+    uint32_t thi = 0, tlo = 0, wcur = 0;
     uint64_t off = 0, len = 0, coff = 0, ccap = 0, tile0 = 0, tile1 = 0;
     uint32_t lead = 0, r = 0;
-    int since_flush = 0;
 
-    auto flush = [&]() {  // block-uniform
-        __syncthreads();
-        const unsigned int staged = s_valid;
-        if (staged) {
-            if (threadIdx.x == 0) s_base = atomicAdd(count + r, static_cast<unsigned long long>(staged));
-            __syncthreads();
-            const unsigned long long base = s_base;
-            unsigned long long a = ~0ull, b = 0;
-            for (unsigned int i = threadIdx.x; i < staged; i += kThreads) {
-                const unsigned long long K = stage[i];
-                a = min(a, K);
-                b = max(b, K);
-                if (base + i < ccap) cand[coff + base + i] = K;
-            }
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) {
-                a = min(a, __shfl_xor_sync(full, a, d));
-                b = max(b, __shfl_xor_sync(full, b, d));
-            }
-            if (lane == 0 && a <= b) { atomicMin(&s_min, a); atomicMax(&s_max, b); }
+    auto warp_flush = [&]() {  // warp-uniform
+        if (wcur == 0) return;
+        __syncwarp();
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(count + r, static_cast<unsigned long long>(wcur));
+        base = __shfl_sync(full, base, 0);
+        for (uint32_t i = lane; i < wcur; i += 32) {
+            const unsigned long long K = stage[i];
+            mn = min(mn, K);
+            mx = max(mx, K);
+            if (base + i < ccap) cand[coff + base + i] = K;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) { s_resv = 0; s_valid = 0; }
-        __syncthreads();
-        since_flush = 0;
+        __syncwarp();
+        wcur = 0;
     };
     auto finish_row = [&]() {
-        flush();
-        if (threadIdx.x == 0) {
-            if (s_min <= s_max) { atomicMin(kmin + r, s_min); atomicMax(kmax + r, s_max); }
-            s_min = ~0ull;
-            s_max = 0;
+        warp_flush();
+        unsigned long long a = mn, b = mx;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            a = min(a, __shfl_xor_sync(full, a, d));
+            b = max(b, __shfl_xor_sync(full, b, d));
         }
-        __syncthreads();
+        if (lane == 0 && a <= b) { atomicMin(kmin + r, a); atomicMax(kmax + r, b); }
+        mn = ~0ull;
+        mx = 0;
     };
 
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         if (t >= tile1 || cur < 0) {
-            const int j = row_of_tile(rows, t);
             if (cur >= 0) finish_row();
+            const int j = row_of_tile(rows, t);
             cur = j;
             r = rows.rid[j];
             thr = T[r];
@@ -453,87 +447,84 @@ __global__ void __launch_bounds__(kThreads, 3) k_compact(Rows rows, InputSrc in,
         // validity window of this tile in tile-local positions (32-bit math from here on)
         const uint32_t vlo = span0 >= lead ? 0u : static_cast<uint32_t>(lead - span0);
         const uint32_t vhi = static_cast<uint32_t>(span_len - span0 < kTile ? span_len - span0 : kTile);
-        const bool full_tile = vlo == 0 && vhi == kTile;
         const uint32_t idx0 = static_cast<uint32_t>(span0 - lead);  // low 32 bits of the row index
         uint32_t v[kUnroll][kVec];
         load_tile_local(in.base + off - lead + span0, vlo, vhi, v);
 
-        // pass 1: keys + match count (the only per-element work for non-matching data)
-        uint32_t mine = 0;
+        // pass 1: key transform + per-thread hit mask (bit u*8+i)
+        uint32_t mask = 0;
+        if (vlo == 0 && vhi == kTile) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
+            for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
-            for (int i = 0; i < kVec; ++i) {
-                const uint32_t key = key_of<KM>(v[u][i], in.a_s);
-                v[u][i] = key;
-                bool hit = key >= thi;
-                if (!full_tile) {
-                    const uint32_t l = (u * kThreads + threadIdx.x) * kVec + i;
-                    hit = hit && l >= vlo && l < vhi;
+                for (int i = 0; i < kVec; ++i) {
+                    const uint32_t key = key_of<KM>(v[u][i], in.a_s);
+                    v[u][i] = key;
+                    mask |= static_cast<uint32_t>(key >= thi) << (u * kVec + i);
                 }
-                mine += hit;
-            }
-        // exact composite compare only matters for keys equal to T.hi with T.lo != 0 (exact path)
-        if (tlo != 0 && __any_sync(full, mine != 0)) {
-            mine = 0;
+        } else {
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                for (int i = 0; i < kVec; ++i) {
+                    const uint32_t key = key_of<KM>(v[u][i], in.a_s);
+                    v[u][i] = key;
+                    const uint32_t l = (u * kThreads + threadIdx.x) * kVec + i;
+                    mask |= static_cast<uint32_t>(key >= thi && l >= vlo && l < vhi) << (u * kVec + i);
+                }
+        }
+        // exact composite compare: only differs from key >= T.hi when T.lo != 0 (exact path)
+        if (tlo != 0) {
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
                 for (int i = 0; i < kVec; ++i) {
                     const uint32_t l = (u * kThreads + threadIdx.x) * kVec + i;
-                    const uint32_t key = v[u][i];
-                    mine += l >= vlo && l < vhi && (key > thi || (key == thi && ~(idx0 + l) >= tlo));
+                    if (v[u][i] == thi && ~(idx0 + l) < tlo) mask &= ~(1u << (u * kVec + i));
                 }
         }
+        if (!__any_sync(full, mask)) continue;
 
-        if (__any_sync(full, mine != 0)) {
-            uint32_t incl = mine;
+        // pass 2 (tiles with hits only): each thread appends its hits as one contiguous run
+        const uint32_t c = __popc(mask);
+        uint32_t incl = c;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(full, incl, d);
-                if (lane >= d) incl += o;
-            }
-            const uint32_t wtot = __shfl_sync(full, incl, 31);
-            uint32_t wbase = 0;
-            if (lane == 31) wbase = atomicAdd(&s_resv, wtot);
-            wbase = __shfl_sync(full, wbase, 31);
-            const bool to_smem = wbase + wtot <= kStageCap;
-            unsigned long long gbase = 0;
-            if (to_smem) {
-                if (lane == 31) atomicMax(&s_valid, wbase + wtot);
-            } else {
-                if (lane == 31) gbase = atomicAdd(count + r, static_cast<unsigned long long>(wtot));
-                gbase = __shfl_sync(full, gbase, 31);
-            }
-            if (mine) {
-                uint32_t w = incl - mine;
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u)
-#pragma unroll
-                    for (int i = 0; i < kVec; ++i) {
-                        const uint32_t l = (u * kThreads + threadIdx.x) * kVec + i;
-                        const uint32_t key = v[u][i];
-                        const uint32_t nidx = ~(idx0 + l);
-                        if (l >= vlo && l < vhi && (key > thi || (key == thi && nidx >= tlo))) {
-                            const unsigned long long K = (static_cast<unsigned long long>(key) << 32) | nidx;
-                            if (to_smem) {
-                                stage[wbase + w] = K;
-                            } else {
-                                atomicMin(&s_min, K);
-                                atomicMax(&s_max, K);
-                                if (gbase + w < ccap) cand[coff + gbase + w] = K;
-                            }
-                            ++w;
-                        }
-                    }
-            }
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(full, incl, d);
+            if (lane >= d) incl += o;
         }
-        if (++since_flush >= kFlushEvery) {
-            __syncthreads();
-            const bool need = s_valid > kStageCap / 2 || s_resv > kStageCap;
-            __syncthreads();
-            if (need) flush();
-            else since_flush = 0;
+        const uint32_t wtot = __shfl_sync(full, incl, 31);
+        if (wcur + wtot > kWarpStage) warp_flush();
+        const uint32_t nidx0 = ~idx0;  // ~(idx0 + l) == nidx0 - l
+        if (wtot <= kWarpStage) {
+            uint32_t o = wcur + incl - c;
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                for (int i = 0; i < kVec; ++i) {
+                    if ((mask >> (u * kVec + i)) & 1u) {
+                        const uint32_t l = (u * kThreads + threadIdx.x) * kVec + i;
+                        stage[o++] = (static_cast<unsigned long long>(v[u][i]) << 32) | (nidx0 - l);
+                    }
+                }
+            wcur += wtot;
+        } else {  // dense hits (k close to n): straight to global with one cursor atomic
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(count + r, static_cast<unsigned long long>(wtot));
+            base = __shfl_sync(full, base, 0) + (incl - c);
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                for (int i = 0; i < kVec; ++i) {
+                    if ((mask >> (u * kVec + i)) & 1u) {
+                        const uint32_t l = (u * kThreads + threadIdx.x) * kVec + i;
+                        const unsigned long long K = (static_cast<unsigned long long>(v[u][i]) << 32) | (nidx0 - l);
+                        mn = min(mn, K);
+                        mx = max(mx, K);
+                        if (base < ccap) cand[coff + base] = K;
+                        ++base;
+                    }
+                }
         }
     }
     if (cur >= 0) finish_row();
@@ -846,6 +837,7 @@ static void sort_groups_cap(int ngroups, const SortGroups& g, cudaStream_t s) {
 void launch_sort_groups(int cap, int ngroups, const SortGroups& g, cudaStream_t s) {
     if (ngroups <= 0) return;
     if (cap <= 1024) sort_groups_cap<1024, 256>(ngroups, g, s);
+    else if (cap <= 2048) sort_groups_cap<2048, 256>(ngroups, g, s);
     else if (cap <= 4096) sort_groups_cap<4096, 512>(ngroups, g, s);
     else if (cap <= 8192) sort_groups_cap<8192, 1024>(ngroups, g, s);
     else sort_groups_cap<16384, 1024>(ngroups, g, s);
