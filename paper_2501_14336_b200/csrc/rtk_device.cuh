@@ -129,4 +129,115 @@ __device__ __forceinline__ int row_of_tile(const Rows& rows, uint64_t t) {
     return lo;
 }
 
+// ----------------------------------------------------------------------------------------
+// Block-wide helpers (kThreads = 256 = 8 warps)
+// ----------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        unsigned long long o = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += o;
+    }
+    return v;
+}
+
+// Exclusive scan across the block; returns this thread's exclusive prefix, *total = sum.
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v,
+                                                              unsigned long long* s_warp,
+                                                              unsigned long long* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned long long inc = warp_incl_scan(v);
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    unsigned long long wbase = 0, tot = 0;
+    for (int w = 0; w < nw; ++w) {
+        unsigned long long x = s_warp[w];
+        if (w < warp) wbase += x;
+        tot += x;
+    }
+    __syncthreads();
+    *total = tot;
+    return wbase + inc - v;
+}
+
+// ----------------------------------------------------------------------------------------
+// Input tile loading: 4 x 32-byte loads per thread, scalar head/tail. Element (u, i) of a
+// thread sits at span position p_u + i, p_u = span0 + (u * kThreads + tid) * 8; the row's
+// element index is span position - lead.
+// ----------------------------------------------------------------------------------------
+__device__ __forceinline__ void load_input_tile(const uint32_t* row_ptr, uint64_t span_len,
+                                                uint32_t lead, uint64_t span0,
+                                                uint32_t (&v)[kUnroll][kVec]) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+        const uint64_t p = span0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec;
+        if (p >= lead && p + kVec <= span_len) {
+            ldg256(row_ptr + p, v[u]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < kVec; ++i) {
+                const uint64_t q = p + i;
+                v[u][i] = (q >= lead && q < span_len) ? __ldg(row_ptr + q) : 0u;
+            }
+        }
+    }
+}
+
+// u64 tiles use the same span convention: ptr is 32-byte aligned, element e of the row sits
+// at span position e + lead (lead = row start's offset inside its 32-byte sector).
+// Same as load_input_tile, but addressed from the tile's own (32-byte aligned) start with the
+// tile-local validity window [vlo, vhi): 32-bit index math only.
+__device__ __forceinline__ void load_tile_local(const uint32_t* tile_ptr, uint32_t vlo, uint32_t vhi,
+                                                uint32_t (&v)[kUnroll][kVec]) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t l = (u * kThreads + threadIdx.x) * kVec;
+        if (l >= vlo && l + kVec <= vhi) {
+            ldg256(tile_ptr + l, v[u]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < kVec; ++i)
+                v[u][i] = (l + i >= vlo && l + i < vhi) ? __ldg(tile_ptr + l + i) : 0u;
+        }
+    }
+}
+
+__device__ __forceinline__ void load_u64_tile(const uint64_t* ptr, uint64_t span_len, uint32_t lead,
+                                              uint64_t e0, uint64_t (&v)[4][kVec64]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint64_t p = e0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec64;
+        if (p >= lead && p + kVec64 <= span_len) {
+            ldg256_u64(ptr + p, v[u]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < kVec64; ++i) {
+                const uint64_t q = p + i;
+                v[u][i] = (q >= lead && q < span_len) ? __ldg(ptr + q) : 0ull;
+            }
+        }
+    }
+}
+
+// smem histogram increment with a whole-warp fast path: adversarial inputs put every
+// element of a warp into one bin (engine_test.cpp:45-56, C4), which would otherwise
+// serialise 32 same-address shared atomics.
+__device__ __forceinline__ void hist_add(uint32_t* h, uint32_t digit, bool valid) {
+    const unsigned full = 0xffffffffu;
+    const uint32_t d0 = __shfl_sync(full, digit, 0);
+    const bool v0 = __shfl_sync(full, valid ? 1 : 0, 0);
+    if (__all_sync(full, valid && digit == d0) && v0) {
+        if ((threadIdx.x & 31) == 0) atomicAdd(&h[d0], 32u);
+    } else {
+        // clustered digits (e.g. the top digit of Uniform[0,1) keys lands in ~8 bins): one
+        // shared atomic per distinct digit of the warp instead of one per lane
+        const unsigned act = __ballot_sync(full, valid);
+        if (valid) {
+            const unsigned peers = __match_any_sync(act, digit);
+            if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[digit], __popc(peers));
+        }
+    }
+}
+
 }  // namespace rtk_b200

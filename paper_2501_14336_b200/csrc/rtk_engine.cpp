@@ -15,6 +15,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "rtk_kernels.h"
@@ -23,8 +26,6 @@ namespace rtk_b200 {
 
 namespace {
 
-constexpr uint64_t kSmallSort = 4096;   // largest group one CTA sorts in shared memory
-constexpr uint64_t kGroupPack = 2048;   // consecutive small buckets are packed up to this
 
 void check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)
@@ -62,13 +63,19 @@ void DevBuf::release() {
     cap = 0;
 }
 
-Engine::Engine(int device) : device_(device) {}
+Engine::Engine(int device) : device_(device) {
+    const char* p = std::getenv("RTK_PROFILE");
+    profile_ = p && *p && *p != '0';
+}
 
 Engine::~Engine() {
+    if (pin_) cudaFreeHost(pin_);
+    if (hctl_) cudaFreeHost(hctl_);
+    if (hcount_) cudaFreeHost(hcount_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     for (DevBuf* b : {&arena_, &sel_, &T_, &count_, &kmin_, &kmax_, &ghist_, &samples_, &cand_a_,
-                      &cand_b_, &seg_hist_, &gcursor_, &io_in, &io_vals, &io_idx,
+                      &cand_b_, &seg_hist_, &gcursor_, &bstart_, &dcap_, &dcoff_, &ctl_, &row_fail_, &groups_, &slots0_, &slotsA_, &slotsB_, &io_in, &io_vals, &io_idx,
                       &io_piv, &io_aux})
         b->release();
 }
@@ -85,14 +92,50 @@ uint8_t* Engine::upload(const Plan& p, cudaStream_t s) {
     }
     uint8_t* d = arena_.as<uint8_t>() + arena_used_;
     arena_used_ += need;
-    if (!p.bytes.empty())
-        check(cudaMemcpyAsync(d, p.bytes.data(), p.bytes.size(), cudaMemcpyHostToDevice, s), "plan upload");
+    if (!p.bytes.empty()) {
+        // stage through pinned memory so the copy is truly asynchronous
+        if (pin_used_ + need > pin_cap_) {
+            if (pin_) retired_pinned_.push_back(pin_);
+            pin_cap_ = std::max<size_t>(need * 2, size_t(4) << 20);
+            check(cudaHostAlloc(reinterpret_cast<void**>(&pin_), pin_cap_, cudaHostAllocDefault), "cudaHostAlloc");
+            pin_used_ = 0;
+        }
+        uint8_t* h = pin_ + pin_used_;
+        pin_used_ += need;
+        std::memcpy(h, p.bytes.data(), p.bytes.size());
+        check(cudaMemcpyAsync(d, h, p.bytes.size(), cudaMemcpyHostToDevice, s), "plan upload");
+    }
     return d;
+}
+
+void Engine::mark(const char* name, cudaStream_t s) {
+    if (!profile_) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    marks_.push_back({name, e, std::chrono::steady_clock::now()});
+}
+
+void Engine::report_marks() {
+    if (!profile_ || marks_.empty()) return;
+    cudaEventSynchronize(marks_.back().ev);
+    std::fprintf(stderr, "[rtk profile]");
+    for (size_t i = 1; i < marks_.size(); ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, marks_[i - 1].ev, marks_[i].ev);
+        const double host_us = std::chrono::duration<double, std::micro>(marks_[i].host - marks_[i - 1].host).count();
+        std::fprintf(stderr, " %s=%.1fus(h%.1f)", marks_[i].name, ms * 1000.0f, host_us);
+    }
+    std::fprintf(stderr, "\n");
+    for (auto& m : marks_) cudaEventDestroy(m.ev);
+    marks_.clear();
 }
 
 void Engine::release_retired() {
     for (DevBuf& b : retired_) b.release();
     retired_.clear();
+    for (uint8_t* p : retired_pinned_) cudaFreeHost(p);
+    retired_pinned_.clear();
 }
 
 void Engine::sync(cudaStream_t s, const char* what) {
@@ -113,6 +156,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
                  uint32_t* d_pivots, cudaStream_t s) {
     check(cudaSetDevice(device_), "cudaSetDevice");
     arena_used_ = 0;
+    pin_used_ = 0;
     stats = rtk_stats{};
     const int R = static_cast<int>(rows.size());
     if (R == 0) return;
@@ -120,6 +164,8 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         for (auto& e : ev_) check(cudaEventCreate(&e), "cudaEventCreate");
     }
     check(cudaEventRecord(ev_[0], s), "event");
+    mark("start", s);
+    group_base_ = 0;
     InputSrc src{d_base, dtype, smallest, scaled ? 1 : 0, a_s};
     const uint64_t base_words = reinterpret_cast<uintptr_t>(d_base) / 4;
 
@@ -127,10 +173,12 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
     std::vector<uint32_t> rid(R), lead(R), sampled(R);
     std::vector<uint64_t> off(R), len(R), tile_start(R + 1, 0), cand_off(R), cap(R), row_k(R),
         row_out(R), row_in(R);
-    std::vector<uint32_t> s_rid;
-    std::vector<uint64_t> s_inoff, s_n, s_soff, s_len, s_tile{0}, s_nseg{0}, s_k, s_target;
-    std::vector<uint32_t> s_lead;
-    uint64_t cand_total = 0, sample_total = 0;
+    struct SampleGroup {
+        std::vector<uint32_t> rid;
+        std::vector<uint64_t> off, len, nseg, k, target;
+        uint32_t per_cta = 0;
+    } sg[2];  // [0]: one CTA per row, [1]: an 8-CTA cluster per row
+    uint64_t cand_total = 0;
     for (int r = 0; r < R; ++r) {
         const RowReq& q = rows[r];
         rid[r] = r;
@@ -141,10 +189,13 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         row_k[r] = q.k;
         row_out[r] = q.out_off;
         row_in[r] = q.in_off;
-        bool samp = q.k < q.n && q.n >= 2 * kSmallSort;
+        bool samp = q.k < q.n && q.n >= 4 * kSortCap;
         uint64_t ns = 0, rp = 0;
         if (samp) {
-            ns = std::min<uint64_t>(uint64_t(1) << 18, std::max<uint64_t>(2048, q.n / 64)) & ~uint64_t(31);
+            // stratified sample: 2^-7 of huge rows (cluster of 8 CTAs), 2^-6 of the others
+            ns = q.n >= (uint64_t(1) << 22) ? std::min<uint64_t>(uint64_t(1) << 17, q.n / 128)
+                                             : std::min<uint64_t>(16384, std::max<uint64_t>(2048, q.n / 64));
+            ns &= ~uint64_t(31);
             const double rr = static_cast<double>(q.k) * static_cast<double>(ns) / static_cast<double>(q.n);
             rp = static_cast<uint64_t>(std::ceil(rr + 4.0 * std::sqrt(rr) + 3.0));
             if (rp >= ns / 2) samp = false;
@@ -153,103 +204,262 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         if (samp) {
             const double ratio = static_cast<double>(q.n) / static_cast<double>(ns);
             cap[r] = std::min<uint64_t>(q.n, static_cast<uint64_t>(ratio * (2.0 * rp + 16.0)) + 1024);
-            s_rid.push_back(r);
-            s_inoff.push_back(q.in_off);
-            s_n.push_back(q.n);
-            s_soff.push_back(sample_total);
-            s_len.push_back(ns);
-            s_lead.push_back(0);  // sample regions are 32-element aligned
-            s_tile.push_back(s_tile.back() + ceil_div(ns, kTile64));
-            s_nseg.push_back(s_nseg.back() + ns / 32);
-            s_k.push_back(rp);
-            s_target.push_back(rp + rp / 10 + 8);
-            sample_total += ns;
+            const int grp = ns > 16384 ? 1 : 0;
+            SampleGroup& g = sg[grp];
+            g.rid.push_back(r);
+            g.off.push_back(q.in_off);
+            g.len.push_back(q.n);
+            g.nseg.push_back(ns / 32);
+            g.k.push_back(rp);
+            g.target.push_back(rp + rp / 10 + 8);
+            g.per_cta = std::max<uint32_t>(g.per_cta, static_cast<uint32_t>(ns / (grp ? 8 : 1) + 32));
         } else {
             cap[r] = q.n;
         }
-        cand_off[r] = cand_total;
-        cand_total += cap[r];
+        cand_off[r] = (cand_total + 3) & ~uint64_t(3);
+        cand_total = cand_off[r] + cap[r];
         stats.elements_scanned += q.n + ns;
     }
-    const int RS = static_cast<int>(s_rid.size());
 
     sel_.ensure(sizeof(RowSel) * R);
     T_.ensure(8 * R);
     count_.ensure(8 * R);
     kmin_.ensure(8 * R);
     kmax_.ensure(8 * R);
-    ghist_.ensure(8ull * kBins * std::max(RS, R));
-    samples_.ensure(8 * std::max<uint64_t>(sample_total, 1));
+    ghist_.ensure(8ull * kBins * R);
     cand_a_.ensure(8 * std::max<uint64_t>(cand_total, 1));
 
     Plan P;
     const size_t o_rid = P.add(rid), o_off = P.add(off), o_len = P.add(len), o_lead = P.add(lead),
                  o_tile = P.add(tile_start), o_coff = P.add(cand_off), o_cap = P.add(cap),
-                 o_k = P.add(row_k), o_out = P.add(row_out), o_in = P.add(row_in),
-                 o_sampled = P.add(sampled), o_srid = P.add(s_rid), o_sin = P.add(s_inoff),
-                 o_sn = P.add(s_n), o_soff = P.add(s_soff), o_slen = P.add(s_len),
-                 o_stile = P.add(s_tile), o_snseg = P.add(s_nseg), o_sk = P.add(s_k),
-                 o_starget = P.add(s_target), o_slead = P.add(s_lead);
-    uint8_t* D = upload(P, s);
-
-    check(cudaMemsetAsync(count_.p, 0, 8 * R, s), "memset");
-    check(cudaMemsetAsync(kmin_.p, 0xFF, 8 * R, s), "memset");
-    check(cudaMemsetAsync(kmax_.p, 0, 8 * R, s), "memset");
-    check(cudaMemsetAsync(ghist_.p, 0, 8ull * kBins * std::max(RS, R), s), "memset");
-
-    if (RS > 0) {
-        launch_init_sel(RS, at<uint32_t>(D, o_srid), at<uint64_t>(D, o_sk), at<uint64_t>(D, o_starget),
-                        sel_.as<RowSel>(), s);
-        Rows gather_rows{RS, at<uint32_t>(D, o_srid), at<uint64_t>(D, o_sin), at<uint64_t>(D, o_sn),
-                         nullptr, nullptr};
-        launch_sample_gather(s_nseg.back(), gather_rows, src, at<uint64_t>(D, o_soff),
-                             at<uint64_t>(D, o_snseg), samples_.as<uint64_t>(), s);
-        Rows srows{RS, at<uint32_t>(D, o_srid), at<uint64_t>(D, o_soff), at<uint64_t>(D, o_slen),
-                   at<uint32_t>(D, o_slead), at<uint64_t>(D, o_stile)};
-        for (int pass = 0; pass < 3; ++pass)
-            launch_radix_pass(1, s_tile.back(), srows, src, samples_.as<uint64_t>(), sel_.as<RowSel>(),
-                              ghist_.as<unsigned long long>(), s);
-        stats.kernel_launches += 5;
+                 o_k = P.add(row_k), o_out = P.add(row_out), o_in = P.add(row_in);
+    size_t o_sg[2][6];
+    for (int g = 0; g < 2; ++g) {
+        o_sg[g][0] = P.add(sg[g].rid);
+        o_sg[g][1] = P.add(sg[g].off);
+        o_sg[g][2] = P.add(sg[g].len);
+        o_sg[g][3] = P.add(sg[g].nseg);
+        o_sg[g][4] = P.add(sg[g].k);
+        o_sg[g][5] = P.add(sg[g].target);
     }
-    launch_set_threshold(R, at<uint32_t>(D, o_rid), at<uint32_t>(D, o_sampled), sel_.as<RowSel>(),
-                         T_.as<uint64_t>(), s);
+    uint8_t* D = upload(P, s);
+    mark("plan", s);
+
+    ctl_.ensure(64);
+    row_fail_.ensure(4 * R);
+    seg_hist_.ensure(4ull * kBins * R);
+    // one kernel resets every per-call counter (unsampled rows keep T = 0)
+    launch_init_call(R, count_.as<unsigned long long>(), kmin_.as<unsigned long long>(),
+                     kmax_.as<unsigned long long>(), T_.as<uint64_t>(), row_fail_.as<uint32_t>(),
+                     ctl_.as<uint32_t>(), seg_hist_.as<uint32_t>(), s);
+    ++stats.kernel_launches;
+    mark("init", s);
+
+    for (int g = 0; g < 2; ++g) {
+        if (sg[g].rid.empty()) continue;
+        SampleRows sr{at<uint32_t>(D, o_sg[g][0]), at<uint64_t>(D, o_sg[g][1]), at<uint64_t>(D, o_sg[g][2]),
+                      at<uint64_t>(D, o_sg[g][3]), at<uint64_t>(D, o_sg[g][4]), at<uint64_t>(D, o_sg[g][5])};
+        launch_sample_select(static_cast<int>(sg[g].rid.size()), g ? 8 : 1, sg[g].per_cta, sr, src,
+                             T_.as<uint64_t>(), s);
+        ++stats.kernel_launches;
+    }
     Rows all{R, at<uint32_t>(D, o_rid), at<uint64_t>(D, o_off), at<uint64_t>(D, o_len),
              at<uint32_t>(D, o_lead), at<uint64_t>(D, o_tile)};
+    mark("sample", s);
     check(cudaEventRecord(ev_[1], s), "event");
     launch_compact(tile_start.back(), all, src, T_.as<uint64_t>(), cand_a_.as<uint64_t>(),
                    at<uint64_t>(D, o_coff), at<uint64_t>(D, o_cap), count_.as<unsigned long long>(),
                    kmin_.as<unsigned long long>(), kmax_.as<unsigned long long>(), s);
     check(cudaEventRecord(ev_[2], s), "event");
-    stats.kernel_launches += 2;
+    mark("compact", s);
+    stats.kernel_launches += 1;
 
-    std::vector<uint64_t> count(R), kmin(R), kmax(R);
-    check(cudaMemcpyAsync(count.data(), count_.p, 8 * R, cudaMemcpyDeviceToHost, s), "d2h");
-    check(cudaMemcpyAsync(kmin.data(), kmin_.p, 8 * R, cudaMemcpyDeviceToHost, s), "d2h");
-    check(cudaMemcpyAsync(kmax.data(), kmax_.p, 8 * R, cudaMemcpyDeviceToHost, s), "d2h");
-    sync(s, "compact");
-
-    // ---- 3. verify the sampled thresholds; exact path for the rows that missed -----------
-    std::vector<uint32_t> fb;
-    for (int r = 0; r < R; ++r)
-        if (count[r] < row_k[r] || count[r] > cap[r]) fb.push_back(r);
-    if (!fb.empty()) {
-        stats.fallback_rows = fb.size();
-        fallback(d_base, src, rows, fb, cand_off, count, kmin, kmax, cand_total, s);
-    }
-    for (int r = 0; r < R; ++r) stats.candidates += count[r];
-
-    // ---- 4. order candidates and gather the first k ------------------------------------
-    finish(src, gather, rows, cand_off, count, kmin, kmax, cand_total, at<uint64_t>(D, o_k),
-           at<uint64_t>(D, o_out), at<uint64_t>(D, o_in), d_vals, d_idx, s);
-    if (d_pivots) {
-        launch_pivots(R, at<uint64_t>(D, o_out), at<uint64_t>(D, o_k), d_vals, d_pivots, s);
-        ++stats.kernel_launches;
-    }
+    // ---- 3+4. device-planned ordering of every row's candidates; pivots optimistically ----
+    Call c{src, gather, at<uint64_t>(D, o_k), at<uint64_t>(D, o_out), at<uint64_t>(D, o_in), d_vals,
+           d_idx, s, cap, cand_off, cand_total, std::vector<uint64_t>(R), R,
+           at<uint64_t>(D, o_cap), at<uint64_t>(D, o_coff)};
+    finish_device(c, rid, /*hist_zeroed=*/true);
+    if (d_pivots) launch_pivots(R, c.d_row_out, c.d_row_k, d_vals, d_pivots, s);
+    mark("pivots", s);
     check(cudaEventRecord(ev_[3], s), "event");
-    sync(s, "finish");
+    uint32_t ctl[8];
+    drain(c, ctl);
+    bool redo_pivots = (ctl[0] & (kFlagFail | kFlagMore)) != 0;
+
+    // ---- exact path for rows whose sampled threshold missed (rare) ------------------------
+    if (ctl[0] & kFlagFail) {
+        std::vector<uint32_t> fail(R), fb;
+        check(cudaMemcpyAsync(fail.data(), row_fail_.p, 4 * R, cudaMemcpyDeviceToHost, s), "d2h");
+        sync(s, "row_fail");
+        for (int r = 0; r < R; ++r)
+            if (fail[r]) fb.push_back(r);
+        stats.fallback_rows = fb.size();
+        fallback(d_base, src, rows, fb, c, s);
+        check(cudaMemsetAsync(ctl_.p, 0, 4, s), "memset");          // flags
+        check(cudaMemsetAsync(ctl_.as<uint32_t>() + 3, 0, 8, s), "memset");  // slot lists
+        check(cudaMemcpyAsync(ctl_.as<uint32_t>() + 2, ctl_.as<uint32_t>() + 1, 4,
+                              cudaMemcpyDeviceToDevice, s), "work");  // work = groups so far
+        finish_device(c, fb, false);
+        drain(c, ctl);
+        if (ctl[0] & kFlagFail) throw Error{RTK_INVARIANT_VIOLATION, "filter: pivot inconsistent after exact path"};
+    }
+    if (redo_pivots) {
+        if (d_pivots) launch_pivots(R, c.d_row_out, c.d_row_k, d_vals, d_pivots, s);
+        check(cudaEventRecord(ev_[3], s), "event");
+        sync(s, "finish");
+    }
+    for (int r = 0; r < R; ++r) stats.candidates += hcount_[r];
+    mark("drain", s);
+    report_marks();
     release_retired();
     cudaEventElapsedTime(&stats.compact_ms, ev_[1], ev_[2]);
     cudaEventElapsedTime(&stats.total_ms, ev_[0], ev_[3]);
+}
+
+// ---------------------------------------------------------------------------------------
+// Device-planned ordering of the candidates of rows `rids` (no host round trip):
+// k_plan_rows -> [MSD level 0: k_seg_hist -> k_seg_plan -> k_seg_scatter] -> k_sort_groups.
+// Tiles of level 0 are laid out over the rows' candidate CAPACITIES; each tile reads the
+// actual count on the device.
+// ---------------------------------------------------------------------------------------
+void Engine::finish_device(Call& c, const std::vector<uint32_t>& rids, bool hist_zeroed) {
+    const int NR = static_cast<int>(rids.size());
+    if (NR == 0) return;
+    std::vector<uint64_t> tiles(NR + 1, 0);
+    uint64_t big_rows = 0;
+    for (int j = 0; j < NR; ++j) {
+        const uint64_t cp = c.cap[rids[j]];
+        const bool big = cp > kSortCap;
+        big_rows += big;
+        tiles[j + 1] = tiles[j] + (big ? ceil_div(cp + 3, kTile64) : 0);
+    }
+    const uint64_t max_groups = NR + big_rows * kBins;
+    groups_.ensure(sizeof(SortGroup) * (group_base_ + max_groups), /*keep=*/true, c.s);
+    slots0_.ensure(sizeof(SegSlot) * NR);
+    const uint64_t max_next = c.cand_total / kSortCap + NR + 1;
+    slotsA_.ensure(sizeof(SegSlot) * max_next);
+    slotsB_.ensure(sizeof(SegSlot) * max_next);
+    seg_hist_.ensure(4ull * kBins * std::max<int>(NR, 1));
+    gcursor_.ensure(4ull * kBins * std::max<int>(NR, 1));
+    bstart_.ensure(4ull * kBins * std::max<int>(NR, 1));
+    cand_b_.ensure(8 * std::max<uint64_t>(c.cand_total, 1));
+    next_cap_ = static_cast<uint32_t>(max_next);
+
+    Plan P;
+    const size_t o_rid = P.add(rids), o_tiles = P.add(tiles);
+    uint8_t* D = upload(P, c.s);
+    uint32_t* ctl = ctl_.as<uint32_t>();
+    GroupList gl{groups_.as<SortGroup>(), ctl + 1, static_cast<uint32_t>(group_base_ + max_groups)};
+    SlotList nextA{slotsA_.as<SegSlot>(), ctl + 3, next_cap_};
+    if (!hist_zeroed) check(cudaMemsetAsync(seg_hist_.p, 0, 4ull * kBins * NR, c.s), "memset");
+    launch_plan_rows(NR, at<uint32_t>(D, o_rid), count_.as<unsigned long long>(), c.d_cap,
+                     c.d_row_k, c.d_coff, kmin_.as<unsigned long long>(),
+                     kmax_.as<unsigned long long>(), slots0_.as<SegSlot>(), gl, ctl, row_fail_.as<uint32_t>(),
+                     c.s);
+    stats.kernel_launches += 1;
+    mark("plan_rows", c.s);
+    if (big_rows) {
+        launch_seg_hist(tiles.back(), slots0_.as<SegSlot>(), NR, at<uint64_t>(D, o_tiles),
+                        cand_a_.as<uint64_t>(), seg_hist_.as<uint32_t>(), c.s);
+        mark("seg_hist", c.s);
+        launch_seg_plan(NR, slots0_.as<SegSlot>(), seg_hist_.as<uint32_t>(), gcursor_.as<uint32_t>(),
+                        c.d_row_k, bstart_.as<uint32_t>(), gl, 1, nextA, ctl, c.s);
+        mark("seg_plan", c.s);
+        launch_seg_scatter(tiles.back(), slots0_.as<SegSlot>(), NR, at<uint64_t>(D, o_tiles),
+                           cand_a_.as<uint64_t>(), cand_b_.as<uint64_t>(), bstart_.as<uint32_t>(),
+                           gcursor_.as<uint32_t>(), c.s);
+        stats.kernel_launches += 3;
+        mark("seg_scatter", c.s);
+    }
+    launch_sort_groups(static_cast<uint32_t>(max_groups), sort_args(c, gl), c.s);
+    mark("sort", c.s);
+    stats.kernel_launches += 1;
+    group_base_ += max_groups;
+}
+
+SortArgs Engine::sort_args(const Call& c, const GroupList& gl) {
+    SortArgs a{};
+    a.groups = gl;
+    a.work = ctl_.as<uint32_t>() + 2;
+    a.buf0 = cand_a_.as<unsigned long long>();
+    a.buf1 = cand_b_.as<unsigned long long>();
+    a.row_k = c.d_row_k;
+    a.row_out_off = c.d_row_out;
+    a.row_in_off = c.d_row_in;
+    a.in_base = c.src.base;
+    a.out_vals = c.d_vals;
+    a.out_idx = c.d_idx;
+    a.gather = c.gather ? 1 : 0;
+    a.dtype = c.src.dtype;
+    a.smallest = c.src.smallest;
+    return a;
+}
+
+// Synchronise, then run host-driven deeper MSD levels while some bucket is still larger than
+// one CTA's sort (adversarial/clustered candidate sets only). ctl: [flags, groups, work, nA, nB].
+void Engine::drain(Call& c, uint32_t (&ctl)[8]) {
+    if (!hctl_) check(cudaHostAlloc(reinterpret_cast<void**>(&hctl_), 64, cudaHostAllocDefault), "cudaHostAlloc");
+    if (hcount_cap_ < static_cast<size_t>(c.R)) {
+        if (hcount_) cudaFreeHost(hcount_);
+        hcount_cap_ = std::max<size_t>(c.R, 1024);
+        check(cudaHostAlloc(reinterpret_cast<void**>(&hcount_), 8 * hcount_cap_, cudaHostAllocDefault), "cudaHostAlloc");
+    }
+    check(cudaMemcpyAsync(hctl_, ctl_.p, 32, cudaMemcpyDeviceToHost, c.s), "d2h");
+    check(cudaMemcpyAsync(hcount_, count_.p, 8 * c.R, cudaMemcpyDeviceToHost, c.s), "d2h");
+    sync(c.s, "finish");
+    std::memcpy(ctl, hctl_, 32);
+    if (ctl[0] & kFlagOverflow) throw Error{RTK_INTERNAL, "device work list overflow"};
+    const uint32_t sticky = ctl[0] & kFlagFail;  // rows for the exact path (kept across levels)
+    bool ran_levels = false;
+    int src_buf = 1;  // level-0 buckets live in buffer B
+    int list = 0;     // next-level slots are in list A (count ctl[3])
+    uint32_t nslots = ctl[3];
+    while (ctl[0] & kFlagMore) {
+        ran_levels = true;
+        if (nslots > next_cap_) throw Error{RTK_INTERNAL, "MSD slot list overflow"};
+        std::vector<SegSlot> sl(nslots);
+        DevBuf& cur = list == 0 ? slotsA_ : slotsB_;
+        DevBuf& nxt = list == 0 ? slotsB_ : slotsA_;
+        check(cudaMemcpyAsync(sl.data(), cur.p, sizeof(SegSlot) * nslots, cudaMemcpyDeviceToHost, c.s), "d2h");
+        sync(c.s, "slots");
+        std::vector<uint64_t> tiles(nslots + 1, 0);
+        for (uint32_t j = 0; j < nslots; ++j) tiles[j + 1] = tiles[j] + ceil_div(sl[j].len + (sl[j].off & 3), kTile64);
+        const uint64_t max_groups = uint64_t(nslots) * kBins;
+        groups_.ensure(sizeof(SortGroup) * (group_base_ + max_groups), true, c.s);
+        seg_hist_.ensure(4ull * kBins * nslots);
+        gcursor_.ensure(4ull * kBins * nslots);
+        bstart_.ensure(4ull * kBins * nslots);
+        Plan P;
+        const size_t o_tiles = P.add(tiles);
+        uint8_t* D = upload(P, c.s);
+        uint32_t* dctl = ctl_.as<uint32_t>();
+        // flags = 0, work = groups so far, next list count = 0
+        uint32_t reset[1] = {0};
+        check(cudaMemcpyAsync(dctl, reset, 4, cudaMemcpyHostToDevice, c.s), "h2d");
+        check(cudaMemcpyAsync(dctl + 2, dctl + 1, 4, cudaMemcpyDeviceToDevice, c.s), "work");
+        check(cudaMemsetAsync(dctl + (list == 0 ? 4 : 3), 0, 4, c.s), "memset");
+        check(cudaMemsetAsync(seg_hist_.p, 0, 4ull * kBins * nslots, c.s), "memset");
+        GroupList gl{groups_.as<SortGroup>(), dctl + 1, static_cast<uint32_t>(group_base_ + max_groups)};
+        SlotList nl{nxt.as<SegSlot>(), dctl + (list == 0 ? 4 : 3), next_cap_};
+        uint64_t* bsrc = src_buf ? cand_b_.as<uint64_t>() : cand_a_.as<uint64_t>();
+        uint64_t* bdst = src_buf ? cand_a_.as<uint64_t>() : cand_b_.as<uint64_t>();
+        launch_seg_hist(tiles.back(), cur.as<SegSlot>(), nslots, at<uint64_t>(D, o_tiles), bsrc,
+                        seg_hist_.as<uint32_t>(), c.s);
+        launch_seg_plan(nslots, cur.as<SegSlot>(), seg_hist_.as<uint32_t>(), gcursor_.as<uint32_t>(), c.d_row_k,
+                        bstart_.as<uint32_t>(), gl, src_buf ? 0 : 1, nl, dctl, c.s);
+        launch_seg_scatter(tiles.back(), cur.as<SegSlot>(), nslots, at<uint64_t>(D, o_tiles), bsrc, bdst,
+                           bstart_.as<uint32_t>(), gcursor_.as<uint32_t>(), c.s);
+        launch_sort_groups(static_cast<uint32_t>(max_groups), sort_args(c, gl), c.s);
+        stats.kernel_launches += 4;
+        group_base_ += max_groups;
+        check(cudaMemcpyAsync(ctl, ctl_.p, 32, cudaMemcpyDeviceToHost, c.s), "d2h");
+        sync(c.s, "msd level");
+        if (ctl[0] & kFlagOverflow) throw Error{RTK_INTERNAL, "device work list overflow"};
+        nslots = list == 0 ? ctl[4] : ctl[3];
+        list ^= 1;
+        src_buf ^= 1;
+    }
+    ctl[0] |= sticky | (ran_levels ? kFlagMore : 0u);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -258,9 +468,9 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
 // on the composite key, so ties at the pivot are resolved by index inside the same loop.
 // ---------------------------------------------------------------------------------------
 void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::vector<RowReq>& rows,
-                      const std::vector<uint32_t>& fb, std::vector<uint64_t>& cand_off,
-                      std::vector<uint64_t>& count, std::vector<uint64_t>& kmin,
-                      std::vector<uint64_t>& kmax, uint64_t& cand_total, cudaStream_t s) {
+                      const std::vector<uint32_t>& fb, Call& c, cudaStream_t s) {
+    std::vector<uint64_t>& cand_off = c.cand_off;
+    uint64_t& cand_total = c.cand_total;
     const uint64_t base_words = reinterpret_cast<uintptr_t>(d_base) / 4;
     const int R = static_cast<int>(rows.size());
     std::vector<uint32_t> active = fb;
@@ -277,6 +487,7 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
                         at<uint64_t>(D, o_t), sel_.as<RowSel>(), s);
         ++stats.kernel_launches;
     }
+    check(cudaMemsetAsync(ghist_.p, 0, 8ull * kBins * R, s), "memset");
     std::vector<RowSel> st(R);
     for (int pass = 0; pass < 6 && !active.empty(); ++pass) {
         const int RA = static_cast<int>(active.size());
@@ -314,15 +525,15 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
     std::vector<uint64_t> T(R);
     check(cudaMemcpyAsync(T.data(), T_.p, 8 * R, cudaMemcpyDeviceToHost, s), "d2h");
     sync(s, "T");
-    std::vector<uint64_t> cap(R, 0), expect(R, 0);
+    std::vector<uint64_t> expect(R, 0);
     std::vector<uint64_t> off, len, tiles{0};
     std::vector<uint32_t> lead;
     for (uint32_t r : fb) {
         T[r] = st[r].T;
         expect[r] = st[r].count_ge;
-        cand_off[r] = cand_total;
-        cap[r] = expect[r];
-        cand_total += expect[r];
+        cand_off[r] = (cand_total + 3) & ~uint64_t(3);
+        c.cap[r] = expect[r];
+        cand_total = cand_off[r] + expect[r];
         off.push_back(rows[r].in_off);
         len.push_back(rows[r].n);
         lead.push_back(static_cast<uint32_t>((base_words + rows[r].in_off) & 7));
@@ -330,173 +541,32 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
         stats.elements_scanned += rows[r].n;
     }
     cand_a_.ensure(8 * cand_total, /*keep=*/true, s);
+    cand_b_.ensure(8 * cand_total, /*keep=*/false, s);
     check(cudaMemcpyAsync(T_.p, T.data(), 8 * R, cudaMemcpyHostToDevice, s), "h2d");
     Plan P;
     const size_t o_rid = P.add(fb), o_off = P.add(off), o_len = P.add(len), o_lead = P.add(lead),
-                 o_tile = P.add(tiles), o_coff = P.add(cand_off), o_cap = P.add(cap);
+                 o_tile = P.add(tiles), o_coff = P.add(cand_off), o_cap = P.add(c.cap);
     uint8_t* D = upload(P, s);
+    c.d_cap = at<uint64_t>(D, o_cap);
+    c.d_coff = at<uint64_t>(D, o_coff);
     for (uint32_t r : fb) {
         check(cudaMemsetAsync(count_.as<uint64_t>() + r, 0, 8, s), "memset");
         check(cudaMemsetAsync(kmin_.as<uint64_t>() + r, 0xFF, 8, s), "memset");
         check(cudaMemsetAsync(kmax_.as<uint64_t>() + r, 0, 8, s), "memset");
+        check(cudaMemsetAsync(row_fail_.as<uint32_t>() + r, 0, 4, s), "memset");
     }
     Rows rr{static_cast<int>(fb.size()), at<uint32_t>(D, o_rid), at<uint64_t>(D, o_off),
             at<uint64_t>(D, o_len), at<uint32_t>(D, o_lead), at<uint64_t>(D, o_tile)};
     launch_compact(tiles.back(), rr, src, T_.as<uint64_t>(), cand_a_.as<uint64_t>(),
-                   at<uint64_t>(D, o_coff), at<uint64_t>(D, o_cap), count_.as<unsigned long long>(),
+                   c.d_coff, c.d_cap, count_.as<unsigned long long>(),
                    kmin_.as<unsigned long long>(), kmax_.as<unsigned long long>(), s);
     ++stats.kernel_launches;
+    std::vector<uint64_t> count(R);
     check(cudaMemcpyAsync(count.data(), count_.p, 8 * R, cudaMemcpyDeviceToHost, s), "d2h");
-    check(cudaMemcpyAsync(kmin.data(), kmin_.p, 8 * R, cudaMemcpyDeviceToHost, s), "d2h");
-    check(cudaMemcpyAsync(kmax.data(), kmax_.p, 8 * R, cudaMemcpyDeviceToHost, s), "d2h");
     sync(s, "fallback compact");
     for (uint32_t r : fb)
         if (count[r] != expect[r] || count[r] < rows[r].k)
             throw Error{RTK_INVARIANT_VIOLATION, "filter: candidate count disagrees with the selected pivot"};
-}
-
-// ---------------------------------------------------------------------------------------
-// Ordering + gather (normalize_result engine.hpp:402-420 fused with filter's output).
-// ---------------------------------------------------------------------------------------
-void Engine::finish(const InputSrc& src, bool gather, const std::vector<RowReq>& rows,
-                    const std::vector<uint64_t>& cand_off, const std::vector<uint64_t>& count,
-                    const std::vector<uint64_t>& kmin, const std::vector<uint64_t>& kmax,
-                    uint64_t cand_total, const uint64_t* d_row_k, const uint64_t* d_row_out_off,
-                    const uint64_t* d_row_in_off, uint32_t* d_vals, uint64_t* d_idx,
-                    cudaStream_t s) {
-    struct Seg {
-        uint64_t off;
-        uint64_t len;
-        uint32_t rid;
-        uint64_t rank_base;
-        uint32_t pos;
-    };
-    SortGroups g{};
-    g.row_k = d_row_k;
-    g.row_out_off = d_row_out_off;
-    g.row_in_off = d_row_in_off;
-    g.in_base = src.base;
-    g.out_vals = d_vals;
-    g.out_idx = d_idx;
-    g.gather = gather ? 1 : 0;
-    g.dtype = src.dtype;
-    g.smallest = src.smallest;
-
-    auto launch_groups = [&](std::vector<SortGroup>& groups, const uint64_t* buf) {
-        if (groups.empty()) return;
-        std::sort(groups.begin(), groups.end(),
-                  [](const SortGroup& a, const SortGroup& b) { return a.len < b.len; });
-        Plan P;
-        const size_t o = P.add(groups);
-        uint8_t* D = upload(P, s);
-        const SortGroup* dg = at<SortGroup>(D, o);
-        size_t i = 0;
-        for (uint64_t cls : {uint64_t(1024), uint64_t(2048), kSmallSort}) {
-            size_t j = i;
-            while (j < groups.size() && groups[j].len <= cls) ++j;
-            if (j > i) {
-                SortGroups gg = g;
-                gg.groups = dg + i;
-                gg.buf = reinterpret_cast<const unsigned long long*>(buf);
-                launch_sort_groups(static_cast<int>(cls), static_cast<int>(j - i), gg, s);
-                ++stats.kernel_launches;
-            }
-            i = j;
-        }
-    };
-
-    std::vector<SortGroup> groups;
-    std::vector<Seg> segs;
-    for (size_t r = 0; r < rows.size(); ++r) {
-        const uint64_t m = count[r];
-        if (m <= kSmallSort) {
-            groups.push_back(SortGroup{cand_off[r], static_cast<uint32_t>(m), static_cast<uint32_t>(r), 0});
-        } else {
-            const uint64_t x = kmin[r] ^ kmax[r];
-            const int hb = 63 - __builtin_clzll(x ? x : 1);
-            segs.push_back(Seg{cand_off[r], m, static_cast<uint32_t>(r), 0,
-                               static_cast<uint32_t>(hb >= 10 ? hb - 10 : 0)});
-        }
-    }
-    launch_groups(groups, cand_a_.as<uint64_t>());
-    if (segs.empty()) return;
-
-    cand_b_.ensure(8 * std::max<uint64_t>(cand_total, 1));
-    uint64_t* cur = cand_a_.as<uint64_t>();
-    uint64_t* nxt = cand_b_.as<uint64_t>();
-    while (!segs.empty()) {
-        const int NS = static_cast<int>(segs.size());
-        std::vector<uint32_t> sid(NS), pos(NS), lead(NS);
-        std::vector<uint64_t> off(NS), len(NS), tiles(NS + 1, 0);
-        for (int j = 0; j < NS; ++j) {
-            sid[j] = j;
-            pos[j] = segs[j].pos;
-            off[j] = segs[j].off;
-            len[j] = segs[j].len;
-            lead[j] = static_cast<uint32_t>(segs[j].off & 3);  // both buffers are 256-B aligned
-            tiles[j + 1] = tiles[j] + ceil_div(segs[j].len + lead[j], kTile64);
-        }
-        seg_hist_.ensure(4ull * kBins * NS);
-        gcursor_.ensure(4ull * kBins * NS);
-        Plan P;
-        const size_t o_sid = P.add(sid), o_pos = P.add(pos), o_off = P.add(off), o_len = P.add(len),
-                     o_tile = P.add(tiles), o_lead = P.add(lead);
-        uint8_t* D = upload(P, s);
-        Rows sr{NS, at<uint32_t>(D, o_sid), at<uint64_t>(D, o_off), at<uint64_t>(D, o_len),
-                at<uint32_t>(D, o_lead), at<uint64_t>(D, o_tile)};
-        check(cudaMemsetAsync(seg_hist_.p, 0, 4ull * kBins * NS, s), "memset");
-        check(cudaMemsetAsync(gcursor_.p, 0, 4ull * kBins * NS, s), "memset");
-        launch_seg_hist(tiles.back(), sr, at<uint32_t>(D, o_pos), cur, seg_hist_.as<uint32_t>(), s);
-        ++stats.kernel_launches;
-        std::vector<uint32_t> hist(static_cast<size_t>(kBins) * NS);
-        check(cudaMemcpyAsync(hist.data(), seg_hist_.p, 4ull * kBins * NS, cudaMemcpyDeviceToHost, s), "d2h");
-        sync(s, "seg hist");
-
-        std::vector<uint32_t> bstart(static_cast<size_t>(kBins) * NS, ~0u);
-        std::vector<Seg> next;
-        groups.clear();
-        for (int j = 0; j < NS; ++j) {
-            const Seg& sg = segs[j];
-            const uint64_t kr = rows[sg.rid].k;
-            const uint32_t* h = hist.data() + static_cast<size_t>(j) * kBins;
-            uint32_t* bs = bstart.data() + static_cast<size_t>(j) * kBins;
-            uint64_t cum = 0;
-            bool open = false;
-            SortGroup cg{};
-            for (int b = kBins - 1; b >= 0; --b) {
-                const uint64_t c = h[b];
-                if (!c) continue;
-                const uint64_t start_rank = sg.rank_base + cum;
-                if (start_rank >= kr) break;
-                bs[b] = static_cast<uint32_t>(cum);
-                if (c <= kSmallSort) {
-                    if (open && cg.len + c <= kGroupPack) {
-                        cg.len += static_cast<uint32_t>(c);
-                    } else {
-                        if (open) groups.push_back(cg);
-                        cg = SortGroup{sg.off + cum, static_cast<uint32_t>(c), sg.rid, start_rank};
-                        open = true;
-                    }
-                } else {
-                    if (open) groups.push_back(cg);
-                    open = false;
-                    next.push_back(Seg{sg.off + cum, c, sg.rid, start_rank, sg.pos >= 11 ? sg.pos - 11 : 0});
-                }
-                cum += c;
-            }
-            if (open) groups.push_back(cg);
-        }
-        Plan P2;
-        const size_t o_bs = P2.add(bstart);
-        uint8_t* D2 = upload(P2, s);
-        launch_seg_scatter(tiles.back(), sr, at<uint32_t>(D, o_pos), cur, nxt, at<uint32_t>(D2, o_bs),
-                           gcursor_.as<uint32_t>(), s);
-        ++stats.kernel_launches;
-        launch_groups(groups, nxt);
-        segs.swap(next);
-        std::swap(cur, nxt);
-        if (!segs.empty()) sync(s, "msd level");
-    }
 }
 
 // ---------------------------------------------------------------------------------------

@@ -6,6 +6,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -13,6 +14,7 @@
 
 #include "../../include/rtk_c.h"
 #include "rtk_device.cuh"
+#include "rtk_kernels.h"
 
 namespace rtk_b200 {
 
@@ -80,23 +82,54 @@ private:
     uint8_t* upload(const Plan& p, cudaStream_t s);
     void sync(cudaStream_t s, const char* what);
     void release_retired();
+    void mark(const char* name, cudaStream_t s);
+    void report_marks();
+    struct Mark {
+        const char* name;
+        cudaEvent_t ev;
+        std::chrono::steady_clock::time_point host;
+    };
+    bool profile_ = false;
+    std::vector<Mark> marks_;
+    // State of one run() call shared by the finish / fallback stages.
+    struct Call {
+        InputSrc src;
+        bool gather;
+        const uint64_t* d_row_k;
+        const uint64_t* d_row_out;
+        const uint64_t* d_row_in;
+        uint32_t* d_vals;
+        uint64_t* d_idx;
+        cudaStream_t s;
+        std::vector<uint64_t> cap;       // candidate capacity per row
+        std::vector<uint64_t> cand_off;  // candidate region per row (buffer A/B)
+        uint64_t cand_total;
+        std::vector<uint64_t> scratch;
+        int R;
+        const uint64_t* d_cap;   // device copies of cap / cand_off (plan arena)
+        const uint64_t* d_coff;
+    };
     void fallback(const uint32_t* d_base, const InputSrc& src, const std::vector<RowReq>& rows,
-                  const std::vector<uint32_t>& fb, std::vector<uint64_t>& cand_off,
-                  std::vector<uint64_t>& count, std::vector<uint64_t>& kmin,
-                  std::vector<uint64_t>& kmax, uint64_t& cand_total, cudaStream_t s);
-    void finish(const InputSrc& src, bool gather, const std::vector<RowReq>& rows,
-                const std::vector<uint64_t>& cand_off, const std::vector<uint64_t>& count,
-                const std::vector<uint64_t>& kmin, const std::vector<uint64_t>& kmax,
-                uint64_t cand_total, const uint64_t* d_row_k, const uint64_t* d_row_out_off,
-                const uint64_t* d_row_in_off, uint32_t* d_vals, uint64_t* d_idx, cudaStream_t s);
+                  const std::vector<uint32_t>& fb, Call& c, cudaStream_t s);
+    void finish_device(Call& c, const std::vector<uint32_t>& rids, bool hist_zeroed);
+    void drain(Call& c, uint32_t (&ctl)[8]);
+    SortArgs sort_args(const Call& c, const GroupList& gl);
 
     int device_;
     DevBuf arena_;
     size_t arena_used_ = 0;
     std::vector<DevBuf> retired_;
+    uint8_t* pin_ = nullptr;       // pinned staging for plan uploads
+    size_t pin_cap_ = 0, pin_used_ = 0;
+    std::vector<uint8_t*> retired_pinned_;
+    uint32_t* hctl_ = nullptr;     // pinned readback of the control words
+    uint64_t* hcount_ = nullptr;   // pinned readback of candidate counts
+    size_t hcount_cap_ = 0;
     cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
     DevBuf sel_, T_, count_, kmin_, kmax_, ghist_, samples_, cand_a_, cand_b_, seg_hist_,
-        gcursor_;
+        gcursor_, bstart_, dcap_, dcoff_, ctl_, row_fail_, groups_, slots0_, slotsA_, slotsB_;
+    uint64_t group_base_ = 0;
+    uint32_t next_cap_ = 0;
 };
 
 }  // namespace rtk_b200

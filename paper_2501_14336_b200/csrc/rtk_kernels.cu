@@ -13,7 +13,10 @@
 // Reference mapping: count_bins engine.hpp:177-222, select_bin :231-241, select_candidates
 // :245-284 (+ WriteBuffer :138-169), radix_select :293-312, filter :318-398,
 // normalize_result :402-420, scaled_topk scaling.hpp:42-78.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "rtk_device.cuh"
 #include "rtk_kernels.h"
@@ -25,117 +28,6 @@ __host__ __device__ __forceinline__ unsigned int digit_hi(unsigned int pos) {
 }
 __host__ __device__ __forceinline__ unsigned int next_pos(unsigned int pos) {
     return pos == 9 ? 0u : pos - 11u;
-}
-
-// ----------------------------------------------------------------------------------------
-// Block-wide helpers (kThreads = 256 = 8 warps)
-// ----------------------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long v) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        unsigned long long o = __shfl_up_sync(0xffffffffu, v, d);
-        if (lane >= d) v += o;
-    }
-    return v;
-}
-
-// Exclusive scan across the block; returns this thread's exclusive prefix, *total = sum.
-__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v,
-                                                              unsigned long long* s_warp,
-                                                              unsigned long long* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    unsigned long long inc = warp_incl_scan(v);
-    if (lane == 31) s_warp[warp] = inc;
-    __syncthreads();
-    unsigned long long wbase = 0, tot = 0;
-    for (int w = 0; w < nw; ++w) {
-        unsigned long long x = s_warp[w];
-        if (w < warp) wbase += x;
-        tot += x;
-    }
-    __syncthreads();
-    *total = tot;
-    return wbase + inc - v;
-}
-
-// ----------------------------------------------------------------------------------------
-// Input tile loading: 4 x 32-byte loads per thread, scalar head/tail. Element (u, i) of a
-// thread sits at span position p_u + i, p_u = span0 + (u * kThreads + tid) * 8; the row's
-// element index is span position - lead.
-// ----------------------------------------------------------------------------------------
-__device__ __forceinline__ void load_input_tile(const uint32_t* row_ptr, uint64_t span_len,
-                                                uint32_t lead, uint64_t span0,
-                                                uint32_t (&v)[kUnroll][kVec]) {
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-        const uint64_t p = span0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec;
-        if (p >= lead && p + kVec <= span_len) {
-            ldg256(row_ptr + p, v[u]);
-        } else {
-#pragma unroll
-            for (int i = 0; i < kVec; ++i) {
-                const uint64_t q = p + i;
-                v[u][i] = (q >= lead && q < span_len) ? __ldg(row_ptr + q) : 0u;
-            }
-        }
-    }
-}
-
-// u64 tiles use the same span convention: ptr is 32-byte aligned, element e of the row sits
-// at span position e + lead (lead = row start's offset inside its 32-byte sector).
-// Same as load_input_tile, but addressed from the tile's own (32-byte aligned) start with the
-// tile-local validity window [vlo, vhi): 32-bit index math only.
-__device__ __forceinline__ void load_tile_local(const uint32_t* tile_ptr, uint32_t vlo, uint32_t vhi,
-                                                uint32_t (&v)[kUnroll][kVec]) {
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-        const uint32_t l = (u * kThreads + threadIdx.x) * kVec;
-        if (l >= vlo && l + kVec <= vhi) {
-            ldg256(tile_ptr + l, v[u]);
-        } else {
-#pragma unroll
-            for (int i = 0; i < kVec; ++i)
-                v[u][i] = (l + i >= vlo && l + i < vhi) ? __ldg(tile_ptr + l + i) : 0u;
-        }
-    }
-}
-
-__device__ __forceinline__ void load_u64_tile(const uint64_t* ptr, uint64_t span_len, uint32_t lead,
-                                              uint64_t e0, uint64_t (&v)[4][kVec64]) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const uint64_t p = e0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec64;
-        if (p >= lead && p + kVec64 <= span_len) {
-            ldg256_u64(ptr + p, v[u]);
-        } else {
-#pragma unroll
-            for (int i = 0; i < kVec64; ++i) {
-                const uint64_t q = p + i;
-                v[u][i] = (q >= lead && q < span_len) ? __ldg(ptr + q) : 0ull;
-            }
-        }
-    }
-}
-
-// smem histogram increment with a whole-warp fast path: adversarial inputs put every
-// element of a warp into one bin (engine_test.cpp:45-56, C4), which would otherwise
-// serialise 32 same-address shared atomics.
-__device__ __forceinline__ void hist_add(uint32_t* h, uint32_t digit, bool valid) {
-    const unsigned full = 0xffffffffu;
-    const uint32_t d0 = __shfl_sync(full, digit, 0);
-    const bool v0 = __shfl_sync(full, valid ? 1 : 0, 0);
-    if (__all_sync(full, valid && digit == d0) && v0) {
-        if ((threadIdx.x & 31) == 0) atomicAdd(&h[d0], 32u);
-    } else {
-        // clustered digits (e.g. the top digit of Uniform[0,1) keys lands in ~8 bins): one
-        // shared atomic per distinct digit of the warp instead of one per lane
-        const unsigned act = __ballot_sync(full, valid);
-        if (valid) {
-            const unsigned peers = __match_any_sync(act, digit);
-            if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[digit], __popc(peers));
-        }
-    }
 }
 
 // ----------------------------------------------------------------------------------------
@@ -328,39 +220,127 @@ __global__ void __launch_bounds__(kThreads) k_radix_pass(Rows rows, InputSrc in,
     if (cur >= 0) finish_row(cur);
 }
 
-// ----------------------------------------------------------------------------------------
-// k_sample_gather: stratified sample. Row j contributes nseg[j] segments of 32 contiguous
-// elements spread evenly over the row; one warp per segment writes 32 composites.
-// ----------------------------------------------------------------------------------------
-__global__ void k_sample_gather(Rows rows, InputSrc in, const uint64_t* sample_off,
-                                const uint64_t* nseg_start, uint64_t* samples) {
-    const uint64_t total = nseg_start[rows.R];
-    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-    const int lane = threadIdx.x & 31;
-    for (uint64_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < total; g += warps) {
-        int lo = 0, hi = rows.R - 1;
-        while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (nseg_start[mid] <= g) lo = mid; else hi = mid - 1;
-        }
-        const int j = lo;
-        const uint64_t s = g - nseg_start[j];
-        const uint64_t nseg = nseg_start[j + 1] - nseg_start[j];
-        const uint64_t n = rows.len[j];
-        const uint64_t start = (s * (n - 32)) / (nseg > 1 ? nseg - 1 : 1);
-        const uint64_t idx = start + lane;
-        const uint32_t raw = __ldg(in.base + rows.off[j] + idx);
-        samples[sample_off[j] + s * 32 + lane] = composite(make_key(in, raw), idx);
+// k_init_call: reset every per-call counter in one launch.
+__global__ void k_init_call(int R, unsigned long long* count, unsigned long long* kmin,
+                            unsigned long long* kmax, uint64_t* T, uint32_t* row_fail, uint32_t* ctl,
+                            uint32_t* seg_hist) {
+    const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = i0; i < static_cast<uint64_t>(R); i += stride) {
+        count[i] = 0;
+        kmin[i] = ~0ull;
+        kmax[i] = 0;
+        T[i] = 0;
+        row_fail[i] = 0;
     }
+    if (i0 < 16) ctl[i0] = 0;
+    for (uint64_t i = i0; i < static_cast<uint64_t>(R) * kBins; i += stride) seg_hist[i] = 0;
 }
 
-// T[rid] = key-level threshold from the resolved sample selection (or 0 = take all).
-__global__ void k_set_threshold(int R, const uint32_t* rid, const uint32_t* sampled,
-                                const RowSel* sel, uint64_t* T) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= R) return;
-    const uint32_t r = rid[j];
-    T[r] = sampled[j] ? (sel[r].T & 0xFFFFFFFF00000000ull) : 0ull;
+// ----------------------------------------------------------------------------------------
+// k_sample_select: the sampled threshold of each row in ONE kernel. A thread-block cluster of
+// CS CTAs owns one row: the CTAs gather a stratified sample (nseg segments of 32 contiguous
+// elements spread evenly over the row) into shared memory as composites, then run radix
+// select passes over it (2048-bin digits, MSD first). Per pass every CTA histograms its part,
+// the cluster barriers, and every CTA sums all CS histograms through distributed shared
+// memory (DSMEM) and takes the same bin decision — no global atomics, no extra launches.
+// The loop stops once #{sample K >= T} <= target (or the composite is exhausted), so heavy
+// key ties in the sample are split by index inside the same loop. T[rid] = that composite.
+// ----------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc in, uint64_t* T) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ unsigned long long smp[];
+    __shared__ uint32_t hist[kBins];
+    __shared__ uint32_t s_wsum[32];
+    __shared__ unsigned long long s_res[3];
+    const unsigned CS = cluster.num_blocks();
+    const unsigned crank = cluster.block_rank();
+    const int j = blockIdx.x / CS;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t n = sr.len[j], off = sr.off[j];
+    const uint64_t nseg = sr.nseg[j];
+    const uint64_t s0 = crank * nseg / CS, s1 = (crank + 1) * nseg / CS;
+    // segment start = floor(sg * (n - 32) / (nseg - 1)) in 16.16-style fixed point
+    const uint64_t stride_fp = ((n - 32) << 16) / (nseg > 1 ? nseg - 1 : 1);
+    // gather: element e of this CTA's share = lane (e % 32) of segment s0 + e / 32; each
+    // thread issues all of its loads before the first use (memory-level parallelism)
+    const uint32_t local = static_cast<uint32_t>((s1 - s0) * 32);
+    constexpr int kG = 16;  // per_cta <= 16384 = 16 x 1024
+    uint32_t raw[kG];
+#pragma unroll
+    for (int q = 0; q < kG; ++q) {
+        const uint32_t e = q * 1024u + tid;
+        if (e < local) {
+            const uint64_t sg = s0 + e / 32;
+            raw[q] = __ldg(in.base + off + ((sg * stride_fp) >> 16) + (e & 31));
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kG; ++q) {
+        const uint32_t e = q * 1024u + tid;
+        if (e < local) {
+            const uint64_t sg = s0 + e / 32;
+            smp[e] = composite(make_key(in, raw[q]), ((sg * stride_fp) >> 16) + (e & 31));
+        }
+    }
+    __syncthreads();
+
+    unsigned long long prefix = 0, k_rem = sr.k[j], above = 0;
+    const unsigned long long target = sr.target[j];
+    unsigned int pos = 53;
+    for (;;) {
+        for (int b = tid; b < kBins; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        const unsigned int hi = digit_hi(pos);
+        const unsigned long long pm = hi >= 64 ? 0ull : (prefix >> hi);
+        const uint32_t dmask = (1u << (hi - pos)) - 1u;
+        for (uint32_t i = tid; i < ((local + 31) & ~31u); i += blockDim.x) {
+            const bool in_range = i < local;
+            const unsigned long long K = in_range ? smp[i] : 0ull;
+            const bool match = in_range && (hi >= 64 || (K >> hi) == pm);
+            hist_add(hist, static_cast<uint32_t>(K >> pos) & dmask, match);
+        }
+        cluster.sync();
+        // every CTA reduces all CS histograms (DSMEM) for its two bins per thread, descending:
+        // thread t owns bins 2047-2t and 2046-2t
+        uint32_t c0 = 0, c1 = 0;
+        const int b0 = kBins - 1 - 2 * tid, b1 = b0 - 1;
+        for (unsigned rk = 0; rk < CS; ++rk) {
+            const uint32_t* hr = cluster.map_shared_rank(hist, rk);
+            c0 += hr[b0];
+            c1 += hr[b1];
+        }
+        // block exclusive scan of (c0 + c1) in descending-bin order
+        const uint32_t v = c0 + c1;
+        uint32_t inc = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        if (lane == 31) s_wsum[warp] = inc;
+        __syncthreads();
+        uint32_t wpre = 0;
+        for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+        const uint64_t before = wpre + inc - v;
+        if (tid == 0) s_res[0] = ~0ull;
+        __syncthreads();
+        if (before < k_rem && before + v >= k_rem) {
+            if (before + c0 >= k_rem) { s_res[0] = b0; s_res[1] = before; s_res[2] = c0; }
+            else { s_res[0] = b1; s_res[1] = before + c0; s_res[2] = c1; }
+        }
+        cluster.sync();  // all DSMEM reads done before anyone rewrites its histogram
+        if (s_res[0] == ~0ull) break;  // rank outside sample (cannot happen: k <= sample size)
+        prefix |= s_res[0] << pos;
+        above += s_res[1];
+        k_rem -= s_res[1];
+        const unsigned long long count_ge = above + s_res[2];
+        __syncthreads();
+        if (count_ge <= target || pos == 0) break;
+        pos = pos == 9 ? 0u : pos - 11u;
+    }
+    if (crank == 0 && tid == 0) T[sr.rid[j]] = prefix;
 }
 
 // ----------------------------------------------------------------------------------------
@@ -530,147 +510,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
     if (cur >= 0) finish_row();
 }
 
-// ----------------------------------------------------------------------------------------
-// MSD partition (for candidate sets larger than one CTA's smem sort):
-// k_seg_hist:    2048-bin histogram of digit (K >> pos[s]) & 2047 per segment.
-// k_seg_scatter: writes every element whose bucket is kept (bstart != ~0u) to
-//                dst[off + bstart[b] + slot]; slots are reserved per (tile, bucket) with one
-//                global atomic each, then handed out from smem (warp/CTA aggregated).
-// ----------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_seg_hist(Rows segs, const uint32_t* pos,
-                                                       const uint64_t* src, uint32_t* ghist) {
-    __shared__ uint32_t h[kBins];
-    for (int b = threadIdx.x; b < kBins; b += kThreads) h[b] = 0;
-    __syncthreads();
-    const uint64_t ntiles = segs.tile_start[segs.R];
-    int cur = -1;
-    uint64_t off = 0, len = 0;
-    uint32_t lead = 0;
-    unsigned int p = 0;
-    auto flush = [&](int j) {
-        __syncthreads();
-        for (int b = threadIdx.x; b < kBins; b += kThreads) {
-            if (h[b]) { atomicAdd(ghist + static_cast<uint64_t>(j) * kBins + b, h[b]); h[b] = 0; }
-        }
-        __syncthreads();
-    };
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int j = row_of_tile(segs, t);
-        if (j != cur) {
-            if (cur >= 0) flush(cur);
-            cur = j;
-            off = segs.off[j];
-            len = segs.len[j];
-            lead = segs.lead[j];
-            p = pos[j];
-        }
-        const uint64_t e0 = (t - segs.tile_start[j]) * kTile64;
-        const uint64_t span_len = len + lead;
-        uint64_t v[4][kVec64];
-        load_u64_tile(src + off - lead, span_len, lead, e0, v);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int i = 0; i < kVec64; ++i) {
-                const uint64_t q = e0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec64 + i;
-                hist_add(h, static_cast<uint32_t>(v[u][i] >> p) & (kBins - 1), q >= lead && q < span_len);
-            }
-    }
-    if (cur >= 0) flush(cur);
-}
-
-__global__ void __launch_bounds__(kThreads) k_seg_scatter(Rows segs, const uint32_t* pos,
-                                                          const uint64_t* src, uint64_t* dst,
-                                                          const uint32_t* bstart,
-                                                          uint32_t* gcursor) {
-    __shared__ uint32_t h[kBins];
-    __shared__ uint32_t base[kBins];
-    const uint64_t ntiles = segs.tile_start[segs.R];
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int j = row_of_tile(segs, t);
-        const uint64_t off = segs.off[j], len = segs.len[j];
-        const uint32_t lead = segs.lead[j];
-        const uint64_t span_len = len + lead;
-        const unsigned int p = pos[j];
-        const uint32_t* bs = bstart + static_cast<uint64_t>(j) * kBins;
-        uint32_t* gc = gcursor + static_cast<uint64_t>(j) * kBins;
-        for (int b = threadIdx.x; b < kBins; b += kThreads) h[b] = 0;
-        __syncthreads();
-        const uint64_t e0 = (t - segs.tile_start[j]) * kTile64;
-        uint64_t v[4][kVec64];
-        uint32_t slot[4][kVec64];
-        load_u64_tile(src + off - lead, span_len, lead, e0, v);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int i = 0; i < kVec64; ++i) {
-                const uint64_t q = e0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec64 + i;
-                const uint32_t d = static_cast<uint32_t>(v[u][i] >> p) & (kBins - 1);
-                slot[u][i] = (q >= lead && q < span_len && bs[d] != ~0u) ? atomicAdd(&h[d], 1u) : ~0u;
-            }
-        __syncthreads();
-        for (int b = threadIdx.x; b < kBins; b += kThreads)
-            if (h[b]) base[b] = bs[b] + atomicAdd(gc + b, h[b]);
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int i = 0; i < kVec64; ++i) {
-                if (slot[u][i] != ~0u) {
-                    const uint32_t d = static_cast<uint32_t>(v[u][i] >> p) & (kBins - 1);
-                    dst[off + base[d] + slot[u][i]] = v[u][i];
-                }
-            }
-        __syncthreads();
-    }
-}
-
-// ----------------------------------------------------------------------------------------
-// k_sort_groups<CAP>: one CTA per group of <= CAP composites. Bitonic sort (descending) in
-// shared memory, then the gather: rank = rank_base + position; ranks < k are written as
-// value bits (decoded from the key, or re-read from the original input for scaled runs,
-// scaling.hpp:74-75) and the u64 row-local index (engine.hpp:106).
-// ----------------------------------------------------------------------------------------
-template <int CAP, int NT>
-__global__ void __launch_bounds__(NT) k_sort_groups(SortGroups g) {
-    extern __shared__ unsigned long long sk[];
-    const SortGroup grp = g.groups[blockIdx.x];
-    const uint32_t len = grp.len;
-    const unsigned long long* src = g.buf + grp.off;
-    int n2 = 1;
-    while (n2 < static_cast<int>(len)) n2 <<= 1;
-    for (int i = threadIdx.x; i < n2; i += NT) sk[i] = i < static_cast<int>(len) ? src[i] : 0ull;
-    __syncthreads();
-    for (int k = 2; k <= n2; k <<= 1) {
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-            for (int i = threadIdx.x; i < (n2 >> 1); i += NT) {
-                const int lo = ((i & ~(jj - 1)) << 1) | (i & (jj - 1));
-                const int hi = lo + jj;
-                const unsigned long long a = sk[lo], b = sk[hi];
-                const bool desc = (lo & k) == 0;
-                if (desc ? (a < b) : (a > b)) { sk[lo] = b; sk[hi] = a; }
-            }
-            __syncthreads();
-        }
-    }
-    const uint32_t r = grp.rid;
-    const uint64_t kr = g.row_k[r];
-    const uint64_t oo = g.row_out_off[r];
-    for (int i = threadIdx.x; i < static_cast<int>(len); i += NT) {
-        const uint64_t rank = grp.rank_base + i;
-        if (rank >= kr) continue;
-        const unsigned long long K = sk[i];
-        const uint32_t key = static_cast<uint32_t>(K >> 32);
-        const uint32_t idx = ~static_cast<uint32_t>(K);
-        uint32_t val;
-        if (g.gather) val = __ldg(g.in_base + g.row_in_off[r] + idx);
-        else if (g.dtype == kF32) val = decode_f32_bits(key, g.smallest);
-        else val = g.smallest ? ~key : key;
-        g.out_vals[oo + rank] = val;
-        g.out_idx[oo + rank] = idx;
-    }
-}
-
 // pivot[r] = values[k-1] of each row (engine.hpp:333 / scaling.hpp:76).
 __global__ void k_pivots(int R, const uint64_t* row_out_off, const uint64_t* row_k,
                          const uint32_t* vals, uint32_t* pivots) {
@@ -738,26 +577,6 @@ __global__ void __launch_bounds__(kThreads) k_first_digit_hist(Rows rows, InputS
 // Launchers. Streaming kernels run as persistent grids: resident CTAs per SM (occupancy API)
 // x SM count, capped by the tile count.
 // ----------------------------------------------------------------------------------------
-static int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
-
-template <typename K>
-static int persistent_grid(K kernel, int threads, size_t smem, uint64_t tiles) {
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
-    if (occ <= 0) occ = 1;
-    const uint64_t g = static_cast<uint64_t>(occ) * num_sms();
-    return static_cast<int>(tiles < g ? (tiles ? tiles : 1) : g);
-}
-
 void launch_init_sel(int R, const uint32_t* rid, const uint64_t* k, const uint64_t* target,
                      RowSel* sel, cudaStream_t s) {
     if (R > 0) k_init_sel<<<(R + 255) / 256, 256, 0, s>>>(R, rid, k, target, sel);
@@ -774,17 +593,35 @@ void launch_radix_pass(int src, uint64_t tiles, const Rows& rows, const InputSrc
     }
 }
 
-void launch_sample_gather(uint64_t segments, const Rows& rows, const InputSrc& in,
-                          const uint64_t* sample_off, const uint64_t* nseg_start, uint64_t* samples,
-                          cudaStream_t s) {
-    const uint64_t blocks = (segments + 7) / 8;  // 8 warps per CTA, one segment per warp
-    const int grid = static_cast<int>(blocks < 4096 ? (blocks ? blocks : 1) : 4096);
-    k_sample_gather<<<grid, 256, 0, s>>>(rows, in, sample_off, nseg_start, samples);
+void launch_init_call(int R, unsigned long long* count, unsigned long long* kmin, unsigned long long* kmax,
+                      uint64_t* T, uint32_t* row_fail, uint32_t* ctl, uint32_t* seg_hist, cudaStream_t s) {
+    const uint64_t work = static_cast<uint64_t>(R) * kBins;
+    const int grid = static_cast<int>(std::min<uint64_t>((work + 255) / 256, 1024));
+    k_init_call<<<grid, 256, 0, s>>>(R, count, kmin, kmax, T, row_fail, ctl, seg_hist);
 }
 
-void launch_set_threshold(int R, const uint32_t* rid, const uint32_t* sampled, const RowSel* sel,
+void launch_sample_select(int rows, int cs, uint32_t per_cta, const SampleRows& sr, const InputSrc& in,
                           uint64_t* T, cudaStream_t s) {
-    if (R > 0) k_set_threshold<<<(R + 255) / 256, 256, 0, s>>>(R, rid, sampled, sel, T);
+    if (rows <= 0) return;
+    const size_t smem = static_cast<size_t>(per_cta) * sizeof(unsigned long long);
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaFuncSetAttribute(k_sample_select, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        configured = smem;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(rows * cs);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_sample_select, sr, in, T);
 }
 
 template <int KM>
@@ -808,39 +645,6 @@ void launch_compact(uint64_t tiles, const Rows& rows, const InputSrc& in, const 
         case kKmU32L: compact_km<kKmU32L>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, s); break;
         default: compact_km<kKmU32S>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, s); break;
     }
-}
-
-void launch_seg_hist(uint64_t tiles, const Rows& segs, const uint32_t* pos, const uint64_t* src,
-                     uint32_t* ghist, cudaStream_t s) {
-    const int grid = persistent_grid(k_seg_hist, kThreads, 0, tiles);
-    k_seg_hist<<<grid, kThreads, 0, s>>>(segs, pos, src, ghist);
-}
-
-void launch_seg_scatter(uint64_t tiles, const Rows& segs, const uint32_t* pos, const uint64_t* src,
-                        uint64_t* dst, const uint32_t* bstart, uint32_t* gcursor, cudaStream_t s) {
-    const int grid = persistent_grid(k_seg_scatter, kThreads, 0, tiles);
-    k_seg_scatter<<<grid, kThreads, 0, s>>>(segs, pos, src, dst, bstart, gcursor);
-}
-
-template <int CAP, int NT>
-static void sort_groups_cap(int ngroups, const SortGroups& g, cudaStream_t s) {
-    constexpr size_t smem = static_cast<size_t>(CAP) * sizeof(unsigned long long);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_sort_groups<CAP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        configured = true;
-    }
-    k_sort_groups<CAP, NT><<<ngroups, NT, smem, s>>>(g);
-}
-
-void launch_sort_groups(int cap, int ngroups, const SortGroups& g, cudaStream_t s) {
-    if (ngroups <= 0) return;
-    if (cap <= 1024) sort_groups_cap<1024, 256>(ngroups, g, s);
-    else if (cap <= 2048) sort_groups_cap<2048, 256>(ngroups, g, s);
-    else if (cap <= 4096) sort_groups_cap<4096, 512>(ngroups, g, s);
-    else if (cap <= 8192) sort_groups_cap<8192, 1024>(ngroups, g, s);
-    else sort_groups_cap<16384, 1024>(ngroups, g, s);
 }
 
 void launch_pivots(int R, const uint64_t* row_out_off, const uint64_t* row_k, const uint32_t* vals,

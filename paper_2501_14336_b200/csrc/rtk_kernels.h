@@ -8,16 +8,55 @@
 
 namespace rtk_b200 {
 
+constexpr uint32_t kSortCap = 4096;    // largest group one CTA sorts in shared memory
+constexpr uint32_t kGroupPack = 2048;  // small buckets are packed per quantum of this size
+constexpr uint32_t kFlagFail = 1;      // some row's sampled threshold missed (exact path)
+constexpr uint32_t kFlagMore = 2;      // some bucket needs a deeper MSD level
+constexpr uint32_t kFlagOverflow = 4;  // a device work list overflowed its capacity
+
+struct SampleRows {       // rows whose threshold comes from a stratified sample
+    const uint32_t* rid;
+    const uint64_t* off;     // input element offset
+    const uint64_t* len;     // n
+    const uint64_t* nseg;    // 32-element segments sampled
+    const uint64_t* k;       // sample rank r'
+    const uint64_t* target;  // stop once #{sample K >= T} <= target
+};
+
 struct SortGroup {
-    uint64_t off;        // element offset into SortGroups::buf
-    uint32_t len;        // <= CAP
+    uint64_t off;        // element offset into buffer `buf`
+    uint32_t len;        // <= kSortCap
     uint32_t rid;        // state row
+    uint32_t buf;        // 0: candidate buffer A, 1: buffer B
+    uint32_t pad;
     uint64_t rank_base;  // output rank of the group's first element
 };
 
-struct SortGroups {
-    const SortGroup* groups;
-    const unsigned long long* buf;
+struct SegSlot {        // one MSD segment; len == 0 means inactive
+    uint64_t off;
+    uint64_t len;
+    uint64_t rank_base;
+    uint32_t rid;
+    uint32_t pos;        // digit = (K >> pos) & 2047
+};
+
+struct GroupList {
+    SortGroup* groups;
+    uint32_t* count;
+    uint32_t cap;
+};
+
+struct SlotList {
+    SegSlot* slots;
+    uint32_t* count;
+    uint32_t cap;
+};
+
+struct SortArgs {
+    GroupList groups;
+    uint32_t* work;
+    const unsigned long long* buf0;
+    const unsigned long long* buf1;
     const uint64_t* row_k;
     const uint64_t* row_out_off;
     const uint64_t* row_in_off;   // gather mode only
@@ -29,24 +68,51 @@ struct SortGroups {
     int smallest;
 };
 
+inline int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+template <typename K>
+inline int persistent_grid(K kernel, int threads, size_t smem, uint64_t tiles) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
+    if (occ <= 0) occ = 1;
+    const uint64_t g = static_cast<uint64_t>(occ) * num_sms();
+    return static_cast<int>(tiles < g ? (tiles ? tiles : 1) : g);
+}
+
 void launch_init_sel(int R, const uint32_t* rid, const uint64_t* k, const uint64_t* target,
                      RowSel* sel, cudaStream_t s);
 void launch_radix_pass(int src, uint64_t tiles, const Rows& rows, const InputSrc& in,
                        const uint64_t* buf, RowSel* sel, unsigned long long* ghist, cudaStream_t s);
-void launch_sample_gather(uint64_t segments, const Rows& rows, const InputSrc& in,
-                          const uint64_t* sample_off, const uint64_t* nseg_start, uint64_t* samples,
-                          cudaStream_t s);
-void launch_set_threshold(int R, const uint32_t* rid, const uint32_t* sampled, const RowSel* sel,
+void launch_init_call(int R, unsigned long long* count, unsigned long long* kmin, unsigned long long* kmax,
+                      uint64_t* T, uint32_t* row_fail, uint32_t* ctl, uint32_t* seg_hist, cudaStream_t s);
+void launch_sample_select(int rows, int cs, uint32_t per_cta, const SampleRows& sr, const InputSrc& in,
                           uint64_t* T, cudaStream_t s);
 void launch_compact(uint64_t tiles, const Rows& rows, const InputSrc& in, const uint64_t* T,
                     uint64_t* cand, const uint64_t* cand_off, const uint64_t* cap,
                     unsigned long long* count, unsigned long long* kmin, unsigned long long* kmax,
                     cudaStream_t s);
-void launch_seg_hist(uint64_t tiles, const Rows& segs, const uint32_t* pos, const uint64_t* src,
-                     uint32_t* ghist, cudaStream_t s);
-void launch_seg_scatter(uint64_t tiles, const Rows& segs, const uint32_t* pos, const uint64_t* src,
-                        uint64_t* dst, const uint32_t* bstart, uint32_t* gcursor, cudaStream_t s);
-void launch_sort_groups(int cap, int ngroups, const SortGroups& g, cudaStream_t s);
+void launch_plan_rows(int R, const uint32_t* rid, const unsigned long long* count, const uint64_t* cap,
+                      const uint64_t* row_k, const uint64_t* cand_off, const unsigned long long* kmin,
+                      const unsigned long long* kmax, SegSlot* slots, const GroupList& groups,
+                      uint32_t* flags, uint32_t* row_fail, cudaStream_t s);
+void launch_seg_hist(uint64_t tiles, const SegSlot* slots, int nslots, const uint64_t* tile_start,
+                     const uint64_t* src, uint32_t* ghist, cudaStream_t s);
+void launch_seg_plan(int nslots, const SegSlot* slots, uint32_t* ghist, uint32_t* gcursor,
+                     const uint64_t* row_k, uint32_t* bstart, const GroupList& groups, uint32_t dst_buf,
+                     const SlotList& next, uint32_t* flags, cudaStream_t s);
+void launch_seg_scatter(uint64_t tiles, const SegSlot* slots, int nslots, const uint64_t* tile_start,
+                        const uint64_t* src, uint64_t* dst, const uint32_t* bstart, uint32_t* gcursor,
+                        cudaStream_t s);
+void launch_sort_groups(uint32_t max_groups, const SortArgs& g, cudaStream_t s);
 void launch_pivots(int R, const uint64_t* row_out_off, const uint64_t* row_k, const uint32_t* vals,
                    uint32_t* pivots, cudaStream_t s);
 void launch_first_digit_hist(uint64_t tiles, const Rows& rows, const InputSrc& in, unsigned int d,
