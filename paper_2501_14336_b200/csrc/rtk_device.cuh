@@ -223,6 +223,11 @@ __device__ __forceinline__ void load_u64_tile(const uint64_t* ptr, uint64_t span
 // smem histogram increment with a whole-warp fast path: adversarial inputs put every
 // element of a warp into one bin (engine_test.cpp:45-56, C4), which would otherwise
 // serialise 32 same-address shared atomics.
+// Spread digits (MSD levels over candidates): plain shared atomics, conflicts are rare.
+__device__ __forceinline__ void hist_add_spread(uint32_t* h, uint32_t digit, bool valid) {
+    if (valid) atomicAdd(&h[digit], 1u);
+}
+
 __device__ __forceinline__ void hist_add(uint32_t* h, uint32_t digit, bool valid) {
     const unsigned full = 0xffffffffu;
     const uint32_t d0 = __shfl_sync(full, digit, 0);

@@ -66,6 +66,8 @@ void DevBuf::release() {
 Engine::Engine(int device) : device_(device) {
     const char* p = std::getenv("RTK_PROFILE");
     profile_ = p && *p && *p != '0';
+    const char* cs = std::getenv("RTK_COUNT_STATS");
+    count_stats_ = profile_ || (cs && *cs && *cs != '0');
 }
 
 Engine::~Engine() {
@@ -75,7 +77,7 @@ Engine::~Engine() {
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     for (DevBuf* b : {&arena_, &sel_, &T_, &count_, &kmin_, &kmax_, &ghist_, &samples_, &cand_a_,
-                      &cand_b_, &seg_hist_, &gcursor_, &bstart_, &dcap_, &dcoff_, &ctl_, &row_fail_, &groups_, &slots0_, &slotsA_, &slotsB_, &io_in, &io_vals, &io_idx,
+                      &cand_b_, &seg_hist_, &gcursor_, &bstart_, &dcap_, &dcoff_, &ctl_, &row_fail_, &groups_, &slots0_, &slotsA_, &slotsB_, &done_, &seg_ticket_, &io_in, &io_vals, &io_idx,
                       &io_piv, &io_aux})
         b->release();
 }
@@ -119,6 +121,13 @@ void Engine::mark(const char* name, cudaStream_t s) {
 void Engine::report_marks() {
     if (!profile_ || marks_.empty()) return;
     cudaEventSynchronize(marks_.back().ev);
+    if (dbg_.p) {
+        unsigned long long d[32];
+        cudaMemcpy(d, dbg_.p, sizeof(d), cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "[rtk sample phases ns]");
+        for (unsigned long long i = 1; i < d[31] && i < 31; ++i) std::fprintf(stderr, " %llu", d[i] - d[i - 1]);
+        std::fprintf(stderr, "\n");
+    }
     std::fprintf(stderr, "[rtk profile]");
     for (size_t i = 1; i < marks_.size(); ++i) {
         float ms = 0;
@@ -177,7 +186,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         std::vector<uint32_t> rid;
         std::vector<uint64_t> off, len, nseg, k, target;
         uint32_t per_cta = 0;
-    } sg[2];  // [0]: one CTA per row, [1]: an 8-CTA cluster per row
+    } sg[2];  // [0]: one CTA per row, [1]: a 16-CTA cluster per row
     uint64_t cand_total = 0;
     for (int r = 0; r < R; ++r) {
         const RowReq& q = rows[r];
@@ -194,7 +203,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         if (samp) {
             // stratified sample: 2^-7 of huge rows (cluster of 8 CTAs), 2^-6 of the others
             ns = q.n >= (uint64_t(1) << 22) ? std::min<uint64_t>(uint64_t(1) << 17, q.n / 128)
-                                             : std::min<uint64_t>(16384, std::max<uint64_t>(2048, q.n / 64));
+                                             : std::min<uint64_t>(8192, std::max<uint64_t>(2048, q.n / 64));
             ns &= ~uint64_t(31);
             const double rr = static_cast<double>(q.k) * static_cast<double>(ns) / static_cast<double>(q.n);
             rp = static_cast<uint64_t>(std::ceil(rr + 4.0 * std::sqrt(rr) + 3.0));
@@ -204,7 +213,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         if (samp) {
             const double ratio = static_cast<double>(q.n) / static_cast<double>(ns);
             cap[r] = std::min<uint64_t>(q.n, static_cast<uint64_t>(ratio * (2.0 * rp + 16.0)) + 1024);
-            const int grp = ns > 16384 ? 1 : 0;
+            const int grp = ns > 8192 ? 1 : 0;
             SampleGroup& g = sg[grp];
             g.rid.push_back(r);
             g.off.push_back(q.in_off);
@@ -212,7 +221,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
             g.nseg.push_back(ns / 32);
             g.k.push_back(rp);
             g.target.push_back(rp + rp / 10 + 8);
-            g.per_cta = std::max<uint32_t>(g.per_cta, static_cast<uint32_t>(ns / (grp ? 8 : 1) + 32));
+            g.per_cta = std::max<uint32_t>(g.per_cta, static_cast<uint32_t>(ns / (grp ? 16 : 1)));
         } else {
             cap[r] = q.n;
         }
@@ -247,44 +256,48 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
 
     ctl_.ensure(64);
     row_fail_.ensure(4 * R);
+    done_.ensure(4 * R);
+    seg_ticket_.ensure(4 * R);
     seg_hist_.ensure(4ull * kBins * R);
     // one kernel resets every per-call counter (unsampled rows keep T = 0)
     launch_init_call(R, count_.as<unsigned long long>(), kmin_.as<unsigned long long>(),
                      kmax_.as<unsigned long long>(), T_.as<uint64_t>(), row_fail_.as<uint32_t>(),
-                     ctl_.as<uint32_t>(), seg_hist_.as<uint32_t>(), s);
+                     ctl_.as<uint32_t>(), seg_hist_.as<uint32_t>(), done_.as<uint32_t>(),
+                     seg_ticket_.as<uint32_t>(), s);
     ++stats.kernel_launches;
     mark("init", s);
 
     for (int g = 0; g < 2; ++g) {
         if (sg[g].rid.empty()) continue;
+        if (profile_) dbg_.ensure(256);
         SampleRows sr{at<uint32_t>(D, o_sg[g][0]), at<uint64_t>(D, o_sg[g][1]), at<uint64_t>(D, o_sg[g][2]),
-                      at<uint64_t>(D, o_sg[g][3]), at<uint64_t>(D, o_sg[g][4]), at<uint64_t>(D, o_sg[g][5])};
-        launch_sample_select(static_cast<int>(sg[g].rid.size()), g ? 8 : 1, sg[g].per_cta, sr, src,
+                      at<uint64_t>(D, o_sg[g][3]), at<uint64_t>(D, o_sg[g][4]), at<uint64_t>(D, o_sg[g][5]),
+                      profile_ ? dbg_.as<unsigned long long>() : nullptr};
+        launch_sample_select(static_cast<int>(sg[g].rid.size()), g ? 16 : 1, sg[g].per_cta, sr, src,
                              T_.as<uint64_t>(), s);
+        check(cudaGetLastError(), "sample_select launch");
         ++stats.kernel_launches;
     }
+    mark("sample", s);
+
+    // ---- 2-4. compaction (+ fused per-row plan) and the device-planned ordering ----------
+    Call c{src, gather, at<uint64_t>(D, o_k), at<uint64_t>(D, o_out), at<uint64_t>(D, o_in), d_vals,
+           d_idx, s, cap, cand_off, cand_total, std::vector<uint64_t>(R), R,
+           at<uint64_t>(D, o_cap), at<uint64_t>(D, o_coff), d_pivots};
+    FinishPrep fp = prepare_finish(c, rid);
     Rows all{R, at<uint32_t>(D, o_rid), at<uint64_t>(D, o_off), at<uint64_t>(D, o_len),
              at<uint32_t>(D, o_lead), at<uint64_t>(D, o_tile)};
-    mark("sample", s);
     check(cudaEventRecord(ev_[1], s), "event");
-    launch_compact(tile_start.back(), all, src, T_.as<uint64_t>(), cand_a_.as<uint64_t>(),
-                   at<uint64_t>(D, o_coff), at<uint64_t>(D, o_cap), count_.as<unsigned long long>(),
-                   kmin_.as<unsigned long long>(), kmax_.as<unsigned long long>(), s);
+    launch_compact(tile_start.back(), all, src, T_.as<uint64_t>(), cand_a_.as<uint64_t>(), c.d_coff, c.d_cap,
+                   count_.as<unsigned long long>(), kmin_.as<unsigned long long>(),
+                   kmax_.as<unsigned long long>(), plan_args(c, fp), s);
     check(cudaEventRecord(ev_[2], s), "event");
     mark("compact", s);
     stats.kernel_launches += 1;
-
-    // ---- 3+4. device-planned ordering of every row's candidates; pivots optimistically ----
-    Call c{src, gather, at<uint64_t>(D, o_k), at<uint64_t>(D, o_out), at<uint64_t>(D, o_in), d_vals,
-           d_idx, s, cap, cand_off, cand_total, std::vector<uint64_t>(R), R,
-           at<uint64_t>(D, o_cap), at<uint64_t>(D, o_coff)};
-    finish_device(c, rid, /*hist_zeroed=*/true);
-    if (d_pivots) launch_pivots(R, c.d_row_out, c.d_row_k, d_vals, d_pivots, s);
-    mark("pivots", s);
+    launch_finish(c, fp);
     check(cudaEventRecord(ev_[3], s), "event");
     uint32_t ctl[8];
     drain(c, ctl);
-    bool redo_pivots = (ctl[0] & (kFlagFail | kFlagMore)) != 0;
 
     // ---- exact path for rows whose sampled threshold missed (rare) ------------------------
     if (ctl[0] & kFlagFail) {
@@ -295,20 +308,13 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
             if (fail[r]) fb.push_back(r);
         stats.fallback_rows = fb.size();
         fallback(d_base, src, rows, fb, c, s);
-        check(cudaMemsetAsync(ctl_.p, 0, 4, s), "memset");          // flags
-        check(cudaMemsetAsync(ctl_.as<uint32_t>() + 3, 0, 8, s), "memset");  // slot lists
-        check(cudaMemcpyAsync(ctl_.as<uint32_t>() + 2, ctl_.as<uint32_t>() + 1, 4,
-                              cudaMemcpyDeviceToDevice, s), "work");  // work = groups so far
-        finish_device(c, fb, false);
         drain(c, ctl);
         if (ctl[0] & kFlagFail) throw Error{RTK_INVARIANT_VIOLATION, "filter: pivot inconsistent after exact path"};
-    }
-    if (redo_pivots) {
-        if (d_pivots) launch_pivots(R, c.d_row_out, c.d_row_k, d_vals, d_pivots, s);
         check(cudaEventRecord(ev_[3], s), "event");
         sync(s, "finish");
     }
-    for (int r = 0; r < R; ++r) stats.candidates += hcount_[r];
+    if (count_stats_)
+        for (int r = 0; r < R; ++r) stats.candidates += hcount_[r];
     mark("drain", s);
     report_marks();
     release_retired();
@@ -318,63 +324,76 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
 
 // ---------------------------------------------------------------------------------------
 // Device-planned ordering of the candidates of rows `rids` (no host round trip):
-// k_plan_rows -> [MSD level 0: k_seg_hist -> k_seg_plan -> k_seg_scatter] -> k_sort_groups.
-// Tiles of level 0 are laid out over the rows' candidate CAPACITIES; each tile reads the
-// actual count on the device.
+// [k_compact's last CTA per row plans it] -> MSD level 0: k_seg_hist (+ fused bucket plan)
+// -> k_seg_scatter -> k_sort_groups (+ pivots). Level-0 tiles are laid out over the rows'
+// candidate CAPACITIES; each tile reads the actual count on the device.
 // ---------------------------------------------------------------------------------------
-void Engine::finish_device(Call& c, const std::vector<uint32_t>& rids, bool hist_zeroed) {
-    const int NR = static_cast<int>(rids.size());
-    if (NR == 0) return;
-    std::vector<uint64_t> tiles(NR + 1, 0);
-    uint64_t big_rows = 0;
-    for (int j = 0; j < NR; ++j) {
+Engine::FinishPrep Engine::prepare_finish(Call& c, const std::vector<uint32_t>& rids) {
+    FinishPrep f{};
+    f.NR = static_cast<int>(rids.size());
+    std::vector<uint64_t> tiles(f.NR + 1, 0);
+    for (int j = 0; j < f.NR; ++j) {
         const uint64_t cp = c.cap[rids[j]];
         const bool big = cp > kSortCap;
-        big_rows += big;
+        f.big_rows += big;
         tiles[j + 1] = tiles[j] + (big ? ceil_div(cp + 3, kTile64) : 0);
     }
-    const uint64_t max_groups = NR + big_rows * kBins;
-    groups_.ensure(sizeof(SortGroup) * (group_base_ + max_groups), /*keep=*/true, c.s);
-    slots0_.ensure(sizeof(SegSlot) * NR);
-    const uint64_t max_next = c.cand_total / kSortCap + NR + 1;
+    f.ntiles = tiles.back();
+    f.max_groups = f.NR + f.big_rows * kBins;
+    groups_.ensure(sizeof(SortGroup) * (group_base_ + f.max_groups), /*keep=*/true, c.s);
+    slots0_.ensure(sizeof(SegSlot) * std::max(f.NR, 1));
+    const uint64_t max_next = c.cand_total / kSortCap + f.NR + 1;
     slotsA_.ensure(sizeof(SegSlot) * max_next);
     slotsB_.ensure(sizeof(SegSlot) * max_next);
-    seg_hist_.ensure(4ull * kBins * std::max<int>(NR, 1));
-    gcursor_.ensure(4ull * kBins * std::max<int>(NR, 1));
-    bstart_.ensure(4ull * kBins * std::max<int>(NR, 1));
+    seg_hist_.ensure(4ull * kBins * std::max<int>(f.NR, 1));
+    gcursor_.ensure(4ull * kBins * std::max<int>(f.NR, 1));
+    bstart_.ensure(4ull * kBins * std::max<int>(f.NR, 1));
     cand_b_.ensure(8 * std::max<uint64_t>(c.cand_total, 1));
     next_cap_ = static_cast<uint32_t>(max_next);
-
     Plan P;
-    const size_t o_rid = P.add(rids), o_tiles = P.add(tiles);
-    uint8_t* D = upload(P, c.s);
+    f.o_rid = P.add(rids);
+    f.o_tiles = P.add(tiles);
+    f.D = upload(P, c.s);
     uint32_t* ctl = ctl_.as<uint32_t>();
-    GroupList gl{groups_.as<SortGroup>(), ctl + 1, static_cast<uint32_t>(group_base_ + max_groups)};
-    SlotList nextA{slotsA_.as<SegSlot>(), ctl + 3, next_cap_};
-    if (!hist_zeroed) check(cudaMemsetAsync(seg_hist_.p, 0, 4ull * kBins * NR, c.s), "memset");
-    launch_plan_rows(NR, at<uint32_t>(D, o_rid), count_.as<unsigned long long>(), c.d_cap,
-                     c.d_row_k, c.d_coff, kmin_.as<unsigned long long>(),
-                     kmax_.as<unsigned long long>(), slots0_.as<SegSlot>(), gl, ctl, row_fail_.as<uint32_t>(),
-                     c.s);
-    stats.kernel_launches += 1;
-    mark("plan_rows", c.s);
-    if (big_rows) {
-        launch_seg_hist(tiles.back(), slots0_.as<SegSlot>(), NR, at<uint64_t>(D, o_tiles),
-                        cand_a_.as<uint64_t>(), seg_hist_.as<uint32_t>(), c.s);
-        mark("seg_hist", c.s);
-        launch_seg_plan(NR, slots0_.as<SegSlot>(), seg_hist_.as<uint32_t>(), gcursor_.as<uint32_t>(),
-                        c.d_row_k, bstart_.as<uint32_t>(), gl, 1, nextA, ctl, c.s);
-        mark("seg_plan", c.s);
-        launch_seg_scatter(tiles.back(), slots0_.as<SegSlot>(), NR, at<uint64_t>(D, o_tiles),
+    f.gl = GroupList{groups_.as<SortGroup>(), ctl + 1, static_cast<uint32_t>(group_base_ + f.max_groups)};
+    f.nextA = SlotList{slotsA_.as<SegSlot>(), ctl + 3, next_cap_};
+    group_base_ += f.max_groups;
+    return f;
+}
+
+PlanArgs Engine::plan_args(const Call& c, const FinishPrep& f) {
+    PlanArgs pa{};
+    pa.cap = c.d_cap;
+    pa.row_k = c.d_row_k;
+    pa.cand_off = c.d_coff;
+    pa.count = count_.as<unsigned long long>();
+    pa.kmin = kmin_.as<unsigned long long>();
+    pa.kmax = kmax_.as<unsigned long long>();
+    pa.slots = slots0_.as<SegSlot>();
+    pa.groups = f.gl;
+    pa.flags = ctl_.as<uint32_t>();
+    pa.row_fail = row_fail_.as<uint32_t>();
+    pa.done = done_.as<uint32_t>();
+    return pa;
+}
+
+void Engine::launch_finish(Call& c, const FinishPrep& f) {
+    if (f.NR == 0) return;
+    if (f.big_rows) {
+        SegPlanArgs pa{seg_hist_.as<uint32_t>(), gcursor_.as<uint32_t>(), c.d_row_k, bstart_.as<uint32_t>(),
+                       f.gl, 1, f.nextA, ctl_.as<uint32_t>(), seg_ticket_.as<uint32_t>()};
+        launch_seg_hist(f.ntiles, slots0_.as<SegSlot>(), f.NR, at<uint64_t>(f.D, f.o_tiles),
+                        cand_a_.as<uint64_t>(), pa, c.s);
+        mark("seg_hist+plan", c.s);
+        launch_seg_scatter(f.ntiles, slots0_.as<SegSlot>(), f.NR, at<uint64_t>(f.D, f.o_tiles),
                            cand_a_.as<uint64_t>(), cand_b_.as<uint64_t>(), bstart_.as<uint32_t>(),
                            gcursor_.as<uint32_t>(), c.s);
-        stats.kernel_launches += 3;
+        stats.kernel_launches += 2;
         mark("seg_scatter", c.s);
     }
-    launch_sort_groups(static_cast<uint32_t>(max_groups), sort_args(c, gl), c.s);
-    mark("sort", c.s);
+    launch_sort_groups(static_cast<uint32_t>(f.max_groups), sort_args(c, f.gl), c.s);
+    mark("sort+pivots", c.s);
     stats.kernel_launches += 1;
-    group_base_ += max_groups;
 }
 
 SortArgs Engine::sort_args(const Call& c, const GroupList& gl) {
@@ -389,6 +408,7 @@ SortArgs Engine::sort_args(const Call& c, const GroupList& gl) {
     a.in_base = c.src.base;
     a.out_vals = c.d_vals;
     a.out_idx = c.d_idx;
+    a.pivots = c.d_pivots;
     a.gather = c.gather ? 1 : 0;
     a.dtype = c.src.dtype;
     a.smallest = c.src.smallest;
@@ -405,17 +425,15 @@ void Engine::drain(Call& c, uint32_t (&ctl)[8]) {
         check(cudaHostAlloc(reinterpret_cast<void**>(&hcount_), 8 * hcount_cap_, cudaHostAllocDefault), "cudaHostAlloc");
     }
     check(cudaMemcpyAsync(hctl_, ctl_.p, 32, cudaMemcpyDeviceToHost, c.s), "d2h");
-    check(cudaMemcpyAsync(hcount_, count_.p, 8 * c.R, cudaMemcpyDeviceToHost, c.s), "d2h");
+    if (count_stats_) check(cudaMemcpyAsync(hcount_, count_.p, 8 * c.R, cudaMemcpyDeviceToHost, c.s), "d2h");
     sync(c.s, "finish");
     std::memcpy(ctl, hctl_, 32);
     if (ctl[0] & kFlagOverflow) throw Error{RTK_INTERNAL, "device work list overflow"};
     const uint32_t sticky = ctl[0] & kFlagFail;  // rows for the exact path (kept across levels)
-    bool ran_levels = false;
     int src_buf = 1;  // level-0 buckets live in buffer B
     int list = 0;     // next-level slots are in list A (count ctl[3])
     uint32_t nslots = ctl[3];
     while (ctl[0] & kFlagMore) {
-        ran_levels = true;
         if (nslots > next_cap_) throw Error{RTK_INTERNAL, "MSD slot list overflow"};
         std::vector<SegSlot> sl(nslots);
         DevBuf& cur = list == 0 ? slotsA_ : slotsB_;
@@ -429,37 +447,38 @@ void Engine::drain(Call& c, uint32_t (&ctl)[8]) {
         seg_hist_.ensure(4ull * kBins * nslots);
         gcursor_.ensure(4ull * kBins * nslots);
         bstart_.ensure(4ull * kBins * nslots);
+        seg_ticket_.ensure(4ull * nslots);
         Plan P;
         const size_t o_tiles = P.add(tiles);
         uint8_t* D = upload(P, c.s);
         uint32_t* dctl = ctl_.as<uint32_t>();
         // flags = 0, work = groups so far, next list count = 0
-        uint32_t reset[1] = {0};
-        check(cudaMemcpyAsync(dctl, reset, 4, cudaMemcpyHostToDevice, c.s), "h2d");
+        check(cudaMemsetAsync(dctl, 0, 4, c.s), "memset");
         check(cudaMemcpyAsync(dctl + 2, dctl + 1, 4, cudaMemcpyDeviceToDevice, c.s), "work");
         check(cudaMemsetAsync(dctl + (list == 0 ? 4 : 3), 0, 4, c.s), "memset");
         check(cudaMemsetAsync(seg_hist_.p, 0, 4ull * kBins * nslots, c.s), "memset");
+        check(cudaMemsetAsync(seg_ticket_.p, 0, 4ull * nslots, c.s), "memset");
         GroupList gl{groups_.as<SortGroup>(), dctl + 1, static_cast<uint32_t>(group_base_ + max_groups)};
         SlotList nl{nxt.as<SegSlot>(), dctl + (list == 0 ? 4 : 3), next_cap_};
         uint64_t* bsrc = src_buf ? cand_b_.as<uint64_t>() : cand_a_.as<uint64_t>();
         uint64_t* bdst = src_buf ? cand_a_.as<uint64_t>() : cand_b_.as<uint64_t>();
-        launch_seg_hist(tiles.back(), cur.as<SegSlot>(), nslots, at<uint64_t>(D, o_tiles), bsrc,
-                        seg_hist_.as<uint32_t>(), c.s);
-        launch_seg_plan(nslots, cur.as<SegSlot>(), seg_hist_.as<uint32_t>(), gcursor_.as<uint32_t>(), c.d_row_k,
-                        bstart_.as<uint32_t>(), gl, src_buf ? 0 : 1, nl, dctl, c.s);
+        SegPlanArgs pa{seg_hist_.as<uint32_t>(), gcursor_.as<uint32_t>(), c.d_row_k, bstart_.as<uint32_t>(), gl,
+                       static_cast<uint32_t>(src_buf ? 0 : 1), nl, dctl, seg_ticket_.as<uint32_t>()};
+        launch_seg_hist(tiles.back(), cur.as<SegSlot>(), nslots, at<uint64_t>(D, o_tiles), bsrc, pa, c.s);
         launch_seg_scatter(tiles.back(), cur.as<SegSlot>(), nslots, at<uint64_t>(D, o_tiles), bsrc, bdst,
                            bstart_.as<uint32_t>(), gcursor_.as<uint32_t>(), c.s);
         launch_sort_groups(static_cast<uint32_t>(max_groups), sort_args(c, gl), c.s);
-        stats.kernel_launches += 4;
+        stats.kernel_launches += 3;
         group_base_ += max_groups;
-        check(cudaMemcpyAsync(ctl, ctl_.p, 32, cudaMemcpyDeviceToHost, c.s), "d2h");
+        check(cudaMemcpyAsync(hctl_, ctl_.p, 32, cudaMemcpyDeviceToHost, c.s), "d2h");
         sync(c.s, "msd level");
+        std::memcpy(ctl, hctl_, 32);
         if (ctl[0] & kFlagOverflow) throw Error{RTK_INTERNAL, "device work list overflow"};
         nslots = list == 0 ? ctl[4] : ctl[3];
         list ^= 1;
         src_buf ^= 1;
     }
-    ctl[0] |= sticky | (ran_levels ? kFlagMore : 0u);
+    ctl[0] |= sticky;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -554,13 +573,22 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
         check(cudaMemsetAsync(kmin_.as<uint64_t>() + r, 0xFF, 8, s), "memset");
         check(cudaMemsetAsync(kmax_.as<uint64_t>() + r, 0, 8, s), "memset");
         check(cudaMemsetAsync(row_fail_.as<uint32_t>() + r, 0, 4, s), "memset");
+        check(cudaMemsetAsync(done_.as<uint32_t>() + r, 0, 4, s), "memset");
     }
+    // control words: flags = 0, slot lists empty, work = groups so far
+    check(cudaMemsetAsync(ctl_.p, 0, 4, s), "memset");
+    check(cudaMemsetAsync(ctl_.as<uint32_t>() + 3, 0, 8, s), "memset");
+    check(cudaMemcpyAsync(ctl_.as<uint32_t>() + 2, ctl_.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToDevice, s), "work");
+    FinishPrep fp = prepare_finish(c, fb);
+    check(cudaMemsetAsync(seg_hist_.p, 0, 4ull * kBins * fb.size(), s), "memset");
+    check(cudaMemsetAsync(seg_ticket_.p, 0, 4ull * fb.size(), s), "memset");
     Rows rr{static_cast<int>(fb.size()), at<uint32_t>(D, o_rid), at<uint64_t>(D, o_off),
             at<uint64_t>(D, o_len), at<uint32_t>(D, o_lead), at<uint64_t>(D, o_tile)};
     launch_compact(tiles.back(), rr, src, T_.as<uint64_t>(), cand_a_.as<uint64_t>(),
                    c.d_coff, c.d_cap, count_.as<unsigned long long>(),
-                   kmin_.as<unsigned long long>(), kmax_.as<unsigned long long>(), s);
+                   kmin_.as<unsigned long long>(), kmax_.as<unsigned long long>(), plan_args(c, fp), s);
     ++stats.kernel_launches;
+    launch_finish(c, fp);
     std::vector<uint64_t> count(R);
     check(cudaMemcpyAsync(count.data(), count_.p, 8 * R, cudaMemcpyDeviceToHost, s), "d2h");
     sync(s, "fallback compact");

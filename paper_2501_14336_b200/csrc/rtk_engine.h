@@ -90,6 +90,7 @@ private:
         std::chrono::steady_clock::time_point host;
     };
     bool profile_ = false;
+    bool count_stats_ = false;   // read candidate counts back (stats.candidates)
     std::vector<Mark> marks_;
     // State of one run() call shared by the finish / fallback stages.
     struct Call {
@@ -108,10 +109,21 @@ private:
         int R;
         const uint64_t* d_cap;   // device copies of cap / cand_off (plan arena)
         const uint64_t* d_coff;
+        uint32_t* d_pivots;
     };
+    struct FinishPrep {
+        int NR = 0;
+        uint64_t big_rows = 0, max_groups = 0, ntiles = 0;
+        uint8_t* D = nullptr;
+        size_t o_rid = 0, o_tiles = 0;
+        GroupList gl{};
+        SlotList nextA{};
+    };
+    FinishPrep prepare_finish(Call& c, const std::vector<uint32_t>& rids);
+    PlanArgs plan_args(const Call& c, const FinishPrep& f);
+    void launch_finish(Call& c, const FinishPrep& f);
     void fallback(const uint32_t* d_base, const InputSrc& src, const std::vector<RowReq>& rows,
                   const std::vector<uint32_t>& fb, Call& c, cudaStream_t s);
-    void finish_device(Call& c, const std::vector<uint32_t>& rids, bool hist_zeroed);
     void drain(Call& c, uint32_t (&ctl)[8]);
     SortArgs sort_args(const Call& c, const GroupList& gl);
 
@@ -127,7 +139,8 @@ private:
     size_t hcount_cap_ = 0;
     cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
     DevBuf sel_, T_, count_, kmin_, kmax_, ghist_, samples_, cand_a_, cand_b_, seg_hist_,
-        gcursor_, bstart_, dcap_, dcoff_, ctl_, row_fail_, groups_, slots0_, slotsA_, slotsB_;
+        gcursor_, bstart_, dcap_, dcoff_, ctl_, row_fail_, groups_, slots0_, slotsA_, slotsB_, done_,
+        seg_ticket_, dbg_;
     uint64_t group_base_ = 0;
     uint32_t next_cap_ = 0;
 };

@@ -20,6 +20,7 @@
 
 #include "rtk_device.cuh"
 #include "rtk_kernels.h"
+#include "rtk_plan.cuh"
 
 namespace rtk_b200 {
 
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(kThreads) k_radix_pass(Rows rows, InputSrc in,
 // k_init_call: reset every per-call counter in one launch.
 __global__ void k_init_call(int R, unsigned long long* count, unsigned long long* kmin,
                             unsigned long long* kmax, uint64_t* T, uint32_t* row_fail, uint32_t* ctl,
-                            uint32_t* seg_hist) {
+                            uint32_t* seg_hist, uint32_t* done, uint32_t* seg_ticket) {
     const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = i0; i < static_cast<uint64_t>(R); i += stride) {
@@ -232,6 +233,8 @@ __global__ void k_init_call(int R, unsigned long long* count, unsigned long long
         kmax[i] = 0;
         T[i] = 0;
         row_fail[i] = 0;
+        done[i] = 0;
+        seg_ticket[i] = 0;
     }
     if (i0 < 16) ctl[i0] = 0;
     for (uint64_t i = i0; i < static_cast<uint64_t>(R) * kBins; i += stride) seg_hist[i] = 0;
@@ -247,11 +250,24 @@ __global__ void k_init_call(int R, unsigned long long* count, unsigned long long
 // The loop stops once #{sample K >= T} <= target (or the composite is exhausted), so heavy
 // key ties in the sample are split by index inside the same loop. T[rid] = that composite.
 // ----------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc in, uint64_t* T) {
+    unsigned long long* dbg = sr.dbg;
+    int ndbg = 0;
+    auto stamp = [&]() {
+        if (dbg && blockIdx.x == 0 && threadIdx.x == 0 && ndbg < 30) dbg[ndbg++] = gtimer();
+    };
+    stamp();
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ unsigned long long smp[];
-    __shared__ uint32_t hist[kBins];
+    __shared__ __align__(16) uint32_t hist[kBins];
+    __shared__ __align__(16) uint32_t hred[kBins];  // this CTA's reduced slice (first SL bins)
     __shared__ uint32_t s_wsum[32];
     __shared__ unsigned long long s_res[3];
     const unsigned CS = cluster.num_blocks();
@@ -265,8 +281,11 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
     const uint64_t stride_fp = ((n - 32) << 16) / (nseg > 1 ? nseg - 1 : 1);
     // gather: element e of this CTA's share = lane (e % 32) of segment s0 + e / 32; each
     // thread issues all of its loads before the first use (memory-level parallelism)
-    const uint32_t local = static_cast<uint32_t>((s1 - s0) * 32);
-    constexpr int kG = 16;  // per_cta <= 16384 = 16 x 1024
+    uint32_t local = static_cast<uint32_t>((s1 - s0) * 32);
+    constexpr int kG = 8;  // per_cta <= 8192 = 8 x 1024 (double-buffered: 2 x 64 KB)
+    unsigned long long* cur = smp;
+    unsigned long long* alt = smp + kG * 1024;
+    __shared__ uint32_t s_cnt;
     uint32_t raw[kG];
 #pragma unroll
     for (int q = 0; q < kG; ++q) {
@@ -281,35 +300,54 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
         const uint32_t e = q * 1024u + tid;
         if (e < local) {
             const uint64_t sg = s0 + e / 32;
-            smp[e] = composite(make_key(in, raw[q]), ((sg * stride_fp) >> 16) + (e & 31));
+            cur[e] = composite(make_key(in, raw[q]), ((sg * stride_fp) >> 16) + (e & 31));
         }
     }
     __syncthreads();
+    stamp();
 
     unsigned long long prefix = 0, k_rem = sr.k[j], above = 0;
     const unsigned long long target = sr.target[j];
     unsigned int pos = 53;
     for (;;) {
-        for (int b = tid; b < kBins; b += blockDim.x) hist[b] = 0;
+        for (int b = tid; b < kBins; b += blockDim.x) { hist[b] = 0; hred[b] = 0; }
         __syncthreads();
         const unsigned int hi = digit_hi(pos);
         const unsigned long long pm = hi >= 64 ? 0ull : (prefix >> hi);
         const uint32_t dmask = (1u << (hi - pos)) - 1u;
+        // every element left in `cur` matches the prefix (compacted after each pass)
+        (void)pm;
         for (uint32_t i = tid; i < ((local + 31) & ~31u); i += blockDim.x) {
             const bool in_range = i < local;
-            const unsigned long long K = in_range ? smp[i] : 0ull;
-            const bool match = in_range && (hi >= 64 || (K >> hi) == pm);
-            hist_add(hist, static_cast<uint32_t>(K >> pos) & dmask, match);
+            const unsigned long long K = in_range ? cur[i] : 0ull;
+            hist_add(hist, static_cast<uint32_t>(K >> pos) & dmask, in_range);
+        }
+        stamp();
+        cluster.sync();
+        stamp();
+        // cluster reduction of the CS histograms in two vectorised DSMEM rounds:
+        //  A) CTA c sums bin slice [c*SL, (c+1)*SL) over all ranks (uint4 loads) into hred;
+        //  B) every thread fetches the reduced counts of its two bins from the slice owner.
+        const uint32_t SL = kBins / CS;
+        if (tid < static_cast<int>(CS * SL / 4) && tid < 1024) {
+            const unsigned rk = tid / (SL / 4);
+            const uint32_t b4 = crank * SL + (tid % (SL / 4)) * 4;
+            const uint4 v4 = *reinterpret_cast<const uint4*>(cluster.map_shared_rank(hist, rk) + b4);
+            const uint32_t o = b4 - crank * SL;
+            if (v4.x) atomicAdd(&hred[o], v4.x);
+            if (v4.y) atomicAdd(&hred[o + 1], v4.y);
+            if (v4.z) atomicAdd(&hred[o + 2], v4.z);
+            if (v4.w) atomicAdd(&hred[o + 3], v4.w);
         }
         cluster.sync();
-        // every CTA reduces all CS histograms (DSMEM) for its two bins per thread, descending:
-        // thread t owns bins 2047-2t and 2046-2t
-        uint32_t c0 = 0, c1 = 0;
+        stamp();
+        uint32_t c0, c1;
         const int b0 = kBins - 1 - 2 * tid, b1 = b0 - 1;
-        for (unsigned rk = 0; rk < CS; ++rk) {
-            const uint32_t* hr = cluster.map_shared_rank(hist, rk);
-            c0 += hr[b0];
-            c1 += hr[b1];
+        {
+            const unsigned owner = b1 / SL;
+            const uint2 v2 = *reinterpret_cast<const uint2*>(cluster.map_shared_rank(hred, owner) + (b1 - owner * SL));
+            c1 = v2.x;
+            c0 = v2.y;
         }
         // block exclusive scan of (c0 + c1) in descending-bin order
         const uint32_t v = c0 + c1;
@@ -330,17 +368,38 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
             if (before + c0 >= k_rem) { s_res[0] = b0; s_res[1] = before; s_res[2] = c0; }
             else { s_res[0] = b1; s_res[1] = before + c0; s_res[2] = c1; }
         }
+        stamp();
         cluster.sync();  // all DSMEM reads done before anyone rewrites its histogram
+        stamp();
         if (s_res[0] == ~0ull) break;  // rank outside sample (cannot happen: k <= sample size)
         prefix |= s_res[0] << pos;
         above += s_res[1];
         k_rem -= s_res[1];
         const unsigned long long count_ge = above + s_res[2];
-        __syncthreads();
         if (count_ge <= target || pos == 0) break;
+        // keep only the samples inside the selected bin for the next pass
+        if (tid == 0) s_cnt = 0;
+        __syncthreads();
+        const unsigned long long want = prefix >> pos;
+        for (uint32_t i = tid; i < ((local + 31) & ~31u); i += blockDim.x) {
+            const bool keep = i < local && (cur[i] >> pos) == want;
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            uint32_t base = 0;
+            if (lane == 0 && bal) base = atomicAdd(&s_cnt, __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (keep) alt[base + __popc(bal & ((1u << lane) - 1u))] = cur[i];
+        }
+        __syncthreads();
+        stamp();
+        local = s_cnt;
+        unsigned long long* t = cur;
+        cur = alt;
+        alt = t;
         pos = pos == 9 ? 0u : pos - 11u;
     }
     if (crank == 0 && tid == 0) T[sr.rid[j]] = prefix;
+    stamp();
+    if (dbg && blockIdx.x == 0 && threadIdx.x == 0) dbg[31] = ndbg;
 }
 
 // ----------------------------------------------------------------------------------------
@@ -363,8 +422,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
                                                          const uint64_t* cap,
                                                          unsigned long long* count,
                                                          unsigned long long* kmin,
-                                                         unsigned long long* kmax) {
+                                                         unsigned long long* kmax, PlanArgs pa) {
     __shared__ unsigned long long stage_all[kThreads / 32][kWarpStage];
+    __shared__ int s_last;
     const uint64_t ntiles = rows.tile_start[rows.R];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned full = 0xffffffffu;
@@ -375,7 +435,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
     unsigned long long thr = 0, mn = ~0ull, mx = 0;
     uint32_t thi = 0, tlo = 0, wcur = 0;
     uint64_t off = 0, len = 0, coff = 0, ccap = 0, tile0 = 0, tile1 = 0;
-    uint32_t lead = 0, r = 0;
+    uint32_t lead = 0, r = 0, mine_tiles = 0;
+    int cur_j = -1;
 
     auto warp_flush = [&]() {  // warp-uniform
         if (wcur == 0) return;
@@ -403,6 +464,21 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         if (lane == 0 && a <= b) { atomicMin(kmin + r, a); atomicMax(kmax + r, b); }
         mn = ~0ull;
         mx = 0;
+        // the CTA that finishes the row's last tile plans its ordering (k_plan_rows fused)
+        if (pa.done) {
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const uint32_t tiles = static_cast<uint32_t>(tile1 - tile0);
+                const uint32_t old = atomicAdd(pa.done + r, mine_tiles);
+                s_last = old + mine_tiles == tiles;
+                if (s_last) {
+                    __threadfence();
+                    plan_row(cur_j, r, pa);
+                }
+            }
+            __syncthreads();
+        }
     };
 
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -410,6 +486,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
             if (cur >= 0) finish_row();
             const int j = row_of_tile(rows, t);
             cur = j;
+            cur_j = j;
+            mine_tiles = 0;
             r = rows.rid[j];
             thr = T[r];
             thi = static_cast<uint32_t>(thr >> 32);
@@ -422,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
             tile0 = rows.tile_start[j];
             tile1 = rows.tile_start[j + 1];
         }
+        ++mine_tiles;
         const uint64_t span0 = (t - tile0) * kTile;
         const uint64_t span_len = len + lead;
         // validity window of this tile in tile-local positions (32-bit math from here on)
@@ -594,20 +673,23 @@ void launch_radix_pass(int src, uint64_t tiles, const Rows& rows, const InputSrc
 }
 
 void launch_init_call(int R, unsigned long long* count, unsigned long long* kmin, unsigned long long* kmax,
-                      uint64_t* T, uint32_t* row_fail, uint32_t* ctl, uint32_t* seg_hist, cudaStream_t s) {
+                      uint64_t* T, uint32_t* row_fail, uint32_t* ctl, uint32_t* seg_hist, uint32_t* done,
+                      uint32_t* seg_ticket, cudaStream_t s) {
     const uint64_t work = static_cast<uint64_t>(R) * kBins;
     const int grid = static_cast<int>(std::min<uint64_t>((work + 255) / 256, 1024));
-    k_init_call<<<grid, 256, 0, s>>>(R, count, kmin, kmax, T, row_fail, ctl, seg_hist);
+    k_init_call<<<grid, 256, 0, s>>>(R, count, kmin, kmax, T, row_fail, ctl, seg_hist, done, seg_ticket);
 }
 
 void launch_sample_select(int rows, int cs, uint32_t per_cta, const SampleRows& sr, const InputSrc& in,
                           uint64_t* T, cudaStream_t s) {
     if (rows <= 0) return;
-    const size_t smem = static_cast<size_t>(per_cta) * sizeof(unsigned long long);
-    static size_t configured = 0;
-    if (smem > configured) {
+    const size_t smem = 2 * 8192 * sizeof(unsigned long long);  // double buffer (per_cta <= 8192)
+    (void)per_cta;
+    static bool configured = false;
+    if (!configured) {
         cudaFuncSetAttribute(k_sample_select, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured = smem;
+        cudaFuncSetAttribute(k_sample_select, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        configured = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(rows * cs);
@@ -628,22 +710,22 @@ template <int KM>
 static void compact_km(uint64_t tiles, const Rows& rows, const InputSrc& in, const uint64_t* T,
                        uint64_t* cand, const uint64_t* cand_off, const uint64_t* cap,
                        unsigned long long* count, unsigned long long* kmin, unsigned long long* kmax,
-                       cudaStream_t s) {
+                       const PlanArgs& pa, cudaStream_t s) {
     const int grid = persistent_grid(k_compact<KM>, kThreads, 0, tiles);
-    k_compact<KM><<<grid, kThreads, 0, s>>>(rows, in, T, cand, cand_off, cap, count, kmin, kmax);
+    k_compact<KM><<<grid, kThreads, 0, s>>>(rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa);
 }
 
 void launch_compact(uint64_t tiles, const Rows& rows, const InputSrc& in, const uint64_t* T,
                     uint64_t* cand, const uint64_t* cand_off, const uint64_t* cap,
                     unsigned long long* count, unsigned long long* kmin, unsigned long long* kmax,
-                    cudaStream_t s) {
+                    const PlanArgs& pa, cudaStream_t s) {
     switch (key_mode(in.dtype, in.smallest, in.scaled)) {
-        case kKmF32L: compact_km<kKmF32L>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, s); break;
-        case kKmF32S: compact_km<kKmF32S>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, s); break;
-        case kKmF32LScaled: compact_km<kKmF32LScaled>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, s); break;
-        case kKmF32SScaled: compact_km<kKmF32SScaled>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, s); break;
-        case kKmU32L: compact_km<kKmU32L>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, s); break;
-        default: compact_km<kKmU32S>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, s); break;
+        case kKmF32L: compact_km<kKmF32L>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
+        case kKmF32S: compact_km<kKmF32S>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
+        case kKmF32LScaled: compact_km<kKmF32LScaled>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
+        case kKmF32SScaled: compact_km<kKmF32SScaled>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
+        case kKmU32L: compact_km<kKmU32L>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
+        default: compact_km<kKmU32S>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
     }
 }
 

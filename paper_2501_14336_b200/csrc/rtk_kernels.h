@@ -8,8 +8,8 @@
 
 namespace rtk_b200 {
 
-constexpr uint32_t kSortCap = 4096;    // largest group one CTA sorts in shared memory
-constexpr uint32_t kGroupPack = 2048;  // small buckets are packed per quantum of this size
+constexpr uint32_t kSortCap = 2048;    // largest group one CTA sorts in shared memory
+constexpr uint32_t kGroupPack = 1024;  // small buckets are packed per quantum of this size
 constexpr uint32_t kFlagFail = 1;      // some row's sampled threshold missed (exact path)
 constexpr uint32_t kFlagMore = 2;      // some bucket needs a deeper MSD level
 constexpr uint32_t kFlagOverflow = 4;  // a device work list overflowed its capacity
@@ -21,6 +21,7 @@ struct SampleRows {       // rows whose threshold comes from a stratified sample
     const uint64_t* nseg;    // 32-element segments sampled
     const uint64_t* k;       // sample rank r'
     const uint64_t* target;  // stop once #{sample K >= T} <= target
+    unsigned long long* dbg; // optional phase timestamps (RTK_PROFILE)
 };
 
 struct SortGroup {
@@ -52,6 +53,32 @@ struct SlotList {
     uint32_t cap;
 };
 
+struct SegPlanArgs {      // bucket plan of one MSD level (fused into k_seg_hist)
+    uint32_t* ghist;
+    uint32_t* gcursor;
+    const uint64_t* row_k;
+    uint32_t* bstart;
+    GroupList groups;
+    uint32_t dst_buf;
+    SlotList next;
+    uint32_t* flags;
+    uint32_t* ticket;        // per slot: tiles finished
+};
+
+struct PlanArgs {         // per-row plan after the compaction (fused into k_compact)
+    const uint64_t* cap;
+    const uint64_t* row_k;
+    const uint64_t* cand_off;
+    const unsigned long long* count;
+    const unsigned long long* kmin;
+    const unsigned long long* kmax;
+    SegSlot* slots;          // indexed by launch row
+    GroupList groups;
+    uint32_t* flags;
+    uint32_t* row_fail;
+    uint32_t* done;          // per state row: tiles finished
+};
+
 struct SortArgs {
     GroupList groups;
     uint32_t* work;
@@ -63,6 +90,7 @@ struct SortArgs {
     const uint32_t* in_base;      // gather mode only
     uint32_t* out_vals;
     uint64_t* out_idx;
+    uint32_t* pivots;        // per state row, nullable
     int gather;
     int dtype;
     int smallest;
@@ -93,22 +121,16 @@ void launch_init_sel(int R, const uint32_t* rid, const uint64_t* k, const uint64
 void launch_radix_pass(int src, uint64_t tiles, const Rows& rows, const InputSrc& in,
                        const uint64_t* buf, RowSel* sel, unsigned long long* ghist, cudaStream_t s);
 void launch_init_call(int R, unsigned long long* count, unsigned long long* kmin, unsigned long long* kmax,
-                      uint64_t* T, uint32_t* row_fail, uint32_t* ctl, uint32_t* seg_hist, cudaStream_t s);
+                      uint64_t* T, uint32_t* row_fail, uint32_t* ctl, uint32_t* seg_hist, uint32_t* done,
+                      uint32_t* seg_ticket, cudaStream_t s);
 void launch_sample_select(int rows, int cs, uint32_t per_cta, const SampleRows& sr, const InputSrc& in,
                           uint64_t* T, cudaStream_t s);
 void launch_compact(uint64_t tiles, const Rows& rows, const InputSrc& in, const uint64_t* T,
                     uint64_t* cand, const uint64_t* cand_off, const uint64_t* cap,
                     unsigned long long* count, unsigned long long* kmin, unsigned long long* kmax,
-                    cudaStream_t s);
-void launch_plan_rows(int R, const uint32_t* rid, const unsigned long long* count, const uint64_t* cap,
-                      const uint64_t* row_k, const uint64_t* cand_off, const unsigned long long* kmin,
-                      const unsigned long long* kmax, SegSlot* slots, const GroupList& groups,
-                      uint32_t* flags, uint32_t* row_fail, cudaStream_t s);
+                    const PlanArgs& pa, cudaStream_t s);
 void launch_seg_hist(uint64_t tiles, const SegSlot* slots, int nslots, const uint64_t* tile_start,
-                     const uint64_t* src, uint32_t* ghist, cudaStream_t s);
-void launch_seg_plan(int nslots, const SegSlot* slots, uint32_t* ghist, uint32_t* gcursor,
-                     const uint64_t* row_k, uint32_t* bstart, const GroupList& groups, uint32_t dst_buf,
-                     const SlotList& next, uint32_t* flags, cudaStream_t s);
+                     const uint64_t* src, const SegPlanArgs& pa, cudaStream_t s);
 void launch_seg_scatter(uint64_t tiles, const SegSlot* slots, int nslots, const uint64_t* tile_start,
                         const uint64_t* src, uint64_t* dst, const uint32_t* bstart, uint32_t* gcursor,
                         cudaStream_t s);

@@ -1,0 +1,28 @@
+// rtk_plan.cuh — per-row plan after the compaction (device side, single thread).
+#pragma once
+#include "rtk_device.cuh"
+#include "rtk_kernels.h"
+
+namespace rtk_b200 {
+
+// m = #{K >= T}: m < k or overflow -> exact path; m <= kSortCap -> one sort group;
+// larger -> an MSD slot whose first digit sits just below the common prefix of kmin..kmax.
+__device__ __forceinline__ void plan_row(int j, uint32_t r, const PlanArgs& pa) {
+    const uint64_t m = __ldcg(pa.count + r);
+    SegSlot sl{pa.cand_off[r], 0, 0, r, 0};
+    if (m < pa.row_k[r] || m > pa.cap[r]) {
+        pa.row_fail[r] = 1;
+        atomicOr(pa.flags, kFlagFail);
+    } else if (m <= kSortCap) {
+        const uint32_t g = atomicAdd(pa.groups.count, 1u);
+        pa.groups.groups[g] = SortGroup{pa.cand_off[r], static_cast<uint32_t>(m), r, 0, 0, 0};
+    } else {
+        const unsigned long long x = __ldcg(pa.kmin + r) ^ __ldcg(pa.kmax + r);
+        const int hb = 63 - __clzll(x ? x : 1ull);
+        sl.len = m;
+        sl.pos = static_cast<uint32_t>(hb >= kDigit - 1 ? hb - (kDigit - 1) : 0);
+    }
+    pa.slots[j] = sl;
+}
+
+}  // namespace rtk_b200

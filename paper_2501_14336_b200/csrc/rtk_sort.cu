@@ -20,33 +20,9 @@
 
 #include "rtk_device.cuh"
 #include "rtk_kernels.h"
+#include "rtk_plan.cuh"
 
 namespace rtk_b200 {
-
-// ---- k_plan_rows --------------------------------------------------------------------------
-__global__ void k_plan_rows(int R, const uint32_t* rid, const unsigned long long* count,
-                            const uint64_t* cap, const uint64_t* row_k, const uint64_t* cand_off,
-                            const unsigned long long* kmin, const unsigned long long* kmax,
-                            SegSlot* slots, GroupList groups, uint32_t* flags, uint32_t* row_fail) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= R) return;
-    const uint32_t r = rid[j];
-    const uint64_t m = count[r];
-    SegSlot sl{cand_off[r], 0, 0, r, 0};
-    if (m < row_k[r] || m > cap[r]) {
-        row_fail[r] = 1;
-        atomicOr(flags, kFlagFail);
-    } else if (m <= kSortCap) {
-        const uint32_t g = atomicAdd(groups.count, 1u);
-        groups.groups[g] = SortGroup{cand_off[r], static_cast<uint32_t>(m), r, 0, 0, 0};
-    } else {
-        const unsigned long long x = kmin[r] ^ kmax[r];
-        const int hb = 63 - __clzll(x ? x : 1ull);
-        sl.len = m;
-        sl.pos = static_cast<uint32_t>(hb >= kDigit - 1 ? hb - (kDigit - 1) : 0);
-    }
-    slots[j] = sl;
-}
 
 // ---- k_seg_hist ---------------------------------------------------------------------------
 // Tiles are laid out over per-slot UPPER BOUNDS (tile_start, host-known); each tile reads the
@@ -60,48 +36,6 @@ __device__ __forceinline__ int slot_of_tile(const uint64_t* tile_start, int n, u
     return lo;
 }
 
-__global__ void __launch_bounds__(kThreads) k_seg_hist(const SegSlot* slots, int nslots,
-                                                       const uint64_t* tile_start,
-                                                       const uint64_t* src, uint32_t* ghist) {
-    __shared__ uint32_t h[kBins];
-    for (int b = threadIdx.x; b < kBins; b += kThreads) h[b] = 0;
-    __syncthreads();
-    const uint64_t ntiles = tile_start[nslots];
-    int cur = -1;
-    bool dirty = false;
-    SegSlot sl{};
-    auto flush = [&](int j) {
-        __syncthreads();
-        for (int b = threadIdx.x; b < kBins; b += kThreads)
-            if (h[b]) { atomicAdd(ghist + static_cast<uint64_t>(j) * kBins + b, h[b]); h[b] = 0; }
-        __syncthreads();
-    };
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int j = slot_of_tile(tile_start, nslots, t);
-        if (j != cur) {
-            if (cur >= 0 && dirty) flush(cur);
-            cur = j;
-            dirty = false;
-            sl = slots[j];
-        }
-        const uint32_t lead = static_cast<uint32_t>(sl.off & 3);
-        const uint64_t span_len = sl.len ? sl.len + lead : 0;
-        const uint64_t e0 = (t - tile_start[j]) * kTile64;
-        if (e0 >= span_len) continue;
-        dirty = true;
-        uint64_t v[4][kVec64];
-        load_u64_tile(src + sl.off - lead, span_len, lead, e0, v);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int i = 0; i < kVec64; ++i) {
-                const uint64_t q = e0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec64 + i;
-                hist_add(h, static_cast<uint32_t>(v[u][i] >> sl.pos) & (kBins - 1), q >= lead && q < span_len);
-            }
-    }
-    if (cur >= 0 && dirty) flush(cur);
-}
-
 // ---- k_seg_plan ---------------------------------------------------------------------------
 // One CTA (256 threads x 8 bins, thread 0 owns the top bins) per slot. Bucket classes, in
 // descending digit order over the kept prefix (first rank < k):
@@ -110,20 +44,21 @@ __global__ void __launch_bounds__(kThreads) k_seg_hist(const SegSlot* slots, int
 //   small (<= kGroupPack)                    -> packed with its neighbours while their starts
 //                                               stay in one kGroupPack quantum (group <= 2Q)
 // A group ends at the next boundary (group start or big bucket) or at the kept end.
-__global__ void __launch_bounds__(kThreads) k_seg_plan(const SegSlot* slots, int nslots,
-                                                       uint32_t* ghist, uint32_t* gcursor,
-                                                       const uint64_t* row_k, uint32_t* bstart,
-                                                       GroupList groups, uint32_t dst_buf,
-                                                       SlotList next, uint32_t* flags) {
+__device__ void seg_plan_block(int j, const SegSlot& sl, const SegPlanArgs& a) {
     constexpr int per = kBins / kThreads;
     constexpr uint32_t INF = 0xffffffffu;
     __shared__ unsigned long long s_warp[32];
     __shared__ uint32_t s_wmin[kThreads / 32];
     __shared__ uint32_t s_kept_end;
-    const int j = blockIdx.x;
-    if (j >= nslots) return;
-    const SegSlot sl = slots[j];
-    if (sl.len == 0) return;
+    if (sl.len == 0) return;  // block-uniform
+    uint32_t* ghist = a.ghist;
+    uint32_t* gcursor = a.gcursor;
+    const uint64_t* row_k = a.row_k;
+    uint32_t* bstart = a.bstart;
+    const GroupList& groups = a.groups;
+    const uint32_t dst_buf = a.dst_buf;
+    const SlotList& next = a.next;
+    uint32_t* flags = a.flags;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t* h = ghist + static_cast<uint64_t>(j) * kBins;
     uint32_t* bs = bstart + static_cast<uint64_t>(j) * kBins;
@@ -133,7 +68,7 @@ __global__ void __launch_bounds__(kThreads) k_seg_plan(const SegSlot* slots, int
 #pragma unroll
     for (int i = 0; i < per; ++i) {
         const int b = kBins - 1 - (tid * per + i);
-        c[i] = h[b];
+        c[i] = __ldcg(h + b);
         h[b] = 0;   // histogram is left zeroed for the next level / call
         gc[b] = 0;  // scatter cursors start at zero
         sum += c[i];
@@ -244,6 +179,63 @@ __global__ void __launch_bounds__(kThreads) k_seg_plan(const SegSlot* slots, int
     }
 }
 
+__global__ void __launch_bounds__(kThreads) k_seg_hist(const SegSlot* slots, int nslots,
+                                                       const uint64_t* tile_start,
+                                                       const uint64_t* src, SegPlanArgs pa) {
+    __shared__ uint32_t h[kBins];
+    __shared__ int s_last;
+    for (int b = threadIdx.x; b < kBins; b += kThreads) h[b] = 0;
+    __syncthreads();
+    const uint64_t ntiles = tile_start[nslots];
+    int cur = -1;
+    uint32_t mine = 0;
+    SegSlot sl{};
+    // flush this CTA's histogram of slot j; the CTA that completes the slot's last tile runs
+    // the bucket plan for it (k_seg_plan fused: no extra launch, no host round trip)
+    auto finish_slot = [&](int j) {
+        __syncthreads();
+        for (int b = threadIdx.x; b < kBins; b += kThreads)
+            if (h[b]) { atomicAdd(pa.ghist + static_cast<uint64_t>(j) * kBins + b, h[b]); h[b] = 0; }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t tiles = static_cast<uint32_t>(tile_start[j + 1] - tile_start[j]);
+            const uint32_t old = atomicAdd(pa.ticket + j, mine);
+            s_last = old + mine == tiles;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            seg_plan_block(j, sl, pa);
+        }
+        __syncthreads();
+    };
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int j = slot_of_tile(tile_start, nslots, t);
+        if (j != cur) {
+            if (cur >= 0) finish_slot(cur);
+            cur = j;
+            mine = 0;
+            sl = slots[j];
+        }
+        ++mine;
+        const uint32_t lead = static_cast<uint32_t>(sl.off & 3);
+        const uint64_t span_len = sl.len ? sl.len + lead : 0;
+        const uint64_t e0 = (t - tile_start[j]) * kTile64;
+        if (e0 >= span_len) continue;
+        uint64_t v[4][kVec64];
+        load_u64_tile(src + sl.off - lead, span_len, lead, e0, v);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int i = 0; i < kVec64; ++i) {
+                const uint64_t q = e0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec64 + i;
+                hist_add_spread(h, static_cast<uint32_t>(v[u][i] >> sl.pos) & (kBins - 1), q >= lead && q < span_len);
+            }
+    }
+    if (cur >= 0) finish_slot(cur);
+}
+
 // ---- k_seg_scatter ------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_seg_scatter(const SegSlot* slots, int nslots,
                                                           const uint64_t* tile_start,
@@ -301,11 +293,11 @@ __global__ void __launch_bounds__(kThreads) k_seg_scatter(const SegSlot* slots, 
 // and therefore stay last. Then the gather: rank = rank_base + position; ranks < k are
 // written as value bits (decoded from the key, or re-read from the original input for scaled
 // runs, scaling.hpp:74-75) and the u64 row-local index (engine.hpp:106).
-constexpr int kSortThreads = 512;
+constexpr int kSortThreads = 256;
 constexpr int kSortItems = kSortCap / kSortThreads;  // 8
 static_assert(kSortItems == 8, "sort layout");
 
-__global__ void __launch_bounds__(kSortThreads, 2) k_sort_groups(SortArgs g) {
+__global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
     extern __shared__ unsigned long long buf[];  // kSortCap entries (dynamic: > 48 KB static)
     __shared__ uint32_t cnt[kSortThreads / 32][256];
     __shared__ uint32_t s_scan[kSortThreads / 32];
@@ -356,13 +348,13 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_sort_groups(SortArgs g) {
                 __syncwarp();
             }
             __syncthreads();
-            // exclusive scan over counters in (digit, warp) order: thread t -> digit t/2,
-            // warps 8*(t&1) .. 8*(t&1)+7
+            // exclusive scan over counters in (digit, warp) order: thread t -> digit t, all 8 warps
             {
-                const int d = tid >> 1, w0 = (tid & 1) * 8;
-                uint32_t c[8], sum = 0;
+                constexpr int NW = kSortThreads / 32;
+                const int d = tid, w0 = 0;
+                uint32_t c[NW], sum = 0;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) { c[i] = cnt[w0 + i][d]; sum += c[i]; }
+                for (int i = 0; i < NW; ++i) { c[i] = cnt[w0 + i][d]; sum += c[i]; }
                 uint32_t inc = sum;
 #pragma unroll
                 for (int dd = 1; dd < 32; dd <<= 1) {
@@ -374,7 +366,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_sort_groups(SortArgs g) {
                 uint32_t pre = inc - sum;
                 for (int w = 0; w < warp; ++w) pre += s_scan[w];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) { cnt[w0 + i][d] = pre; pre += c[i]; }
+                for (int i = 0; i < NW; ++i) { cnt[w0 + i][d] = pre; pre += c[i]; }
             }
             __syncthreads();
 #pragma unroll
@@ -402,33 +394,17 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_sort_groups(SortArgs g) {
             else val = g.smallest ? ~kk : kk;
             g.out_vals[oo + rank] = val;
             g.out_idx[oo + rank] = idx;
+            if (rank == kr - 1 && g.pivots) g.pivots[r] = val;  // engine.hpp:333
         }
         __syncthreads();
     }
 }
 
 // ---- launchers ----------------------------------------------------------------------------
-void launch_plan_rows(int R, const uint32_t* rid, const unsigned long long* count, const uint64_t* cap,
-                      const uint64_t* row_k, const uint64_t* cand_off, const unsigned long long* kmin,
-                      const unsigned long long* kmax, SegSlot* slots, const GroupList& groups,
-                      uint32_t* flags, uint32_t* row_fail, cudaStream_t s) {
-    if (R > 0)
-        k_plan_rows<<<(R + 127) / 128, 128, 0, s>>>(R, rid, count, cap, row_k, cand_off, kmin, kmax,
-                                                     slots, groups, flags, row_fail);
-}
-
 void launch_seg_hist(uint64_t tiles, const SegSlot* slots, int nslots, const uint64_t* tile_start,
-                     const uint64_t* src, uint32_t* ghist, cudaStream_t s) {
+                     const uint64_t* src, const SegPlanArgs& pa, cudaStream_t s) {
     const int grid = persistent_grid(k_seg_hist, kThreads, 0, tiles);
-    k_seg_hist<<<grid, kThreads, 0, s>>>(slots, nslots, tile_start, src, ghist);
-}
-
-void launch_seg_plan(int nslots, const SegSlot* slots, uint32_t* ghist, uint32_t* gcursor,
-                     const uint64_t* row_k, uint32_t* bstart, const GroupList& groups, uint32_t dst_buf,
-                     const SlotList& next, uint32_t* flags, cudaStream_t s) {
-    if (nslots > 0)
-        k_seg_plan<<<nslots, kThreads, 0, s>>>(slots, nslots, ghist, gcursor, row_k, bstart, groups,
-                                               dst_buf, next, flags);
+    k_seg_hist<<<grid, kThreads, 0, s>>>(slots, nslots, tile_start, src, pa);
 }
 
 void launch_seg_scatter(uint64_t tiles, const SegSlot* slots, int nslots, const uint64_t* tile_start,
