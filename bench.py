@@ -119,6 +119,10 @@ def main():
     ap.add_argument("--sweep", type=str, default="256,16384", help="extra k values (device value only)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch-ks", type=str, default="50,4096,128256",
+                    help="C3 batched LLM-vocab top-k: k values measured into batch_llm (empty = skip)")
+    ap.add_argument("--batch-rows", type=int, default=256)
+    ap.add_argument("--vocab", type=int, default=128256)
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -220,6 +224,39 @@ def main():
     comp_ms = statistics.mean(comp)
     achieved = 4 * n / (comp_ms * 1e-3) / 1e9
 
+    # C3: batched LLM sampling top-k, rows sharded across ranks (no collective)
+    batch_llm = {}
+    if args.batch_ks:
+        from paper_2501_14336_b200 import sharded as SH
+        r0, r1 = SH.row_shard(args.batch_rows, world, rank)
+        rows_here = r1 - r0
+        V = args.vocab
+        logits = torch.randn(rows_here, V, device=dev, generator=gen)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2: flush between steps
+        for kb in [int(v) for v in args.batch_ks.split(",") if v]:
+            kb = min(kb, V)
+            for _ in range(3):
+                rtk.batch_topk_dense(logits, kb)
+            times = []
+            for _ in range(max(5, args.steps // 2)):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                rtk.batch_topk_dense(logits, kb)
+                b.record(stream)
+                torch.cuda.synchronize()
+                times.append(a.elapsed_time(b))
+            ms_b = statistics.mean(times)
+            if world > 1:
+                t = torch.tensor([ms_b], device=dev)
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                ms_b = float(t.item())
+            q = args.batch_rows / (ms_b * 1e-3)
+            byts = args.batch_rows * (4 * V + 12 * kb)
+            batch_llm[str(kb)] = {"ms_per_batch": ms_b, "queries_per_s": q, "effective_GBps": byts / (ms_b * 1e-3) / 1e9,
+                                  "fraction_of_hbm_peak": byts / (ms_b * 1e-3) / 1e9 / peak}
+        del logits, flush
+
     # e2e through the host entry point (rank 0 / N=1 semantics: per-GPU query from pinned host)
     e2e = None
     if rank == 0:
@@ -265,7 +302,10 @@ def main():
                             "peak_kind": peak_kind, "kernel_ms": comp_ms,
                             "kernel_share_of_step": comp_ms / mean_ms},
                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-               "k_sweep": sweep, "step_ms_all": ms}
+               "k_sweep": sweep,
+               "batch_llm": {"config": f"{args.batch_rows} x {args.vocab} fp32 N(0,1) logits, rows sharded over "
+                                       f"{world} GPU(s), L2 flushed between batches", "results": batch_llm},
+               "step_ms_all": ms}
         print(json.dumps(out))
     if world > 1:
         torch.distributed.destroy_process_group()

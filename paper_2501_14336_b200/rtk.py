@@ -337,15 +337,45 @@ def batch_topk(batch: BatchInput, order: SelectionOrder = SelectionOrder.Largest
                                        C.c_void_p(idx.ctypes.data), p_oo, C.c_void_p(pivs.ctypes.data),
                                        C.byref(c), C.byref(o))
         _raise(st, "rtk_topk_batched_host")
-    out = []
-    for t in range(B):
-        s, e = int(oo[t]), int(oo[t]) + int(ks[t])
-        p = pivs[t]
-        out.append(TopKResult(vals[s:e], idx[s:e], p.item() if hasattr(p, "item") else p))
+    kl = [int(v) for v in ks]
+    if hasattr(vals, "split"):
+        vs, ix = vals.split(kl), idx.split(kl)
+        pl = pivs.tolist()
+    else:
+        cut = np.cumsum(kl)[:-1] if B else []
+        vs, ix = np.split(vals, cut), np.split(idx, cut)
+        pl = list(pivs[:B])
+    out = [TopKResult(vs[t], ix[t], pl[t]) for t in range(B)]
     if info is not None:
         info.task_passes = [1] * B
         info.phase_b_rounds = 0
     return out
+
+
+def batch_topk_dense(x, k: int, order: SelectionOrder = SelectionOrder.Largest,
+                     cfg: Optional[EngineConfig] = None) -> TopKResult:
+    """Dense fast path of batch_topk for a [B, V] CUDA tensor (e.g. LLM logits): every row
+    gets the same k; returns values [B, k], indices [B, k] (row-local) and pivots [B]."""
+    import torch
+    cfg = cfg or EngineConfig()
+    lib = L.load()
+    x = x.contiguous()
+    B, V = x.shape
+    offs, p_off = _arr64(np.arange(B, dtype=np.uint64) * V)
+    lens, p_len = _arr64(np.full(B, V, dtype=np.uint64))
+    kks, p_ks = _arr64(np.full(B, k, dtype=np.uint64))
+    oo, p_oo = _arr64(np.arange(B, dtype=np.uint64) * k)
+    vals = torch.empty((B, k), dtype=x.dtype, device=x.device)
+    idx = torch.empty((B, k), dtype=torch.int64, device=x.device)
+    piv = torch.empty(B, dtype=x.dtype, device=x.device)
+    c = cfg._c()
+    o = L.rtk_batch_opts(1, 1)
+    st = lib.rtk_topk_batched(_handle(x.device.index or 0), C.c_void_p(x.data_ptr()), x.numel(), p_off, p_len,
+                              p_ks, B, _dtype_code(x), int(order), C.c_void_p(vals.data_ptr()),
+                              C.c_void_p(idx.data_ptr()), p_oo, C.c_void_p(piv.data_ptr()), C.byref(c),
+                              C.byref(o), _stream_ptr(x))
+    _raise(st, "rtk_topk_batched")
+    return TopKResult(vals, idx, piv)
 
 
 def scaled_topk(input, k: int, order: SelectionOrder = SelectionOrder.Largest,
