@@ -124,7 +124,7 @@ void Engine::report_marks() {
     if (dbg_.p) {
         unsigned long long d[32];
         cudaMemcpy(d, dbg_.p, sizeof(d), cudaMemcpyDeviceToHost);
-        std::fprintf(stderr, "[rtk sample phases ns]");
+        std::fprintf(stderr, "[rtk dbg phases ns]");
         for (unsigned long long i = 1; i < d[31] && i < 31; ++i) std::fprintf(stderr, " %llu", d[i] - d[i - 1]);
         std::fprintf(stderr, "\n");
     }
@@ -188,6 +188,29 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         uint32_t per_cta = 0;
     } sg[2];  // [0]: one CTA per row, [1]: a 16-CTA cluster per row
     uint64_t cand_total = 0;
+    // K6 routing: short rows with small k finish in one CTA each (k_rows_fused); the rest take
+    // the general multi-CTA pipeline (sampled threshold -> k_compact -> MSD -> sort groups)
+    std::vector<uint32_t> grow, frow[2];
+    std::vector<uint64_t> f_off[2], f_len[2], f_k[2];
+    // returns -1 (general path), 0 (large-buffer fused variant) or 1 (small-buffer variant)
+    auto fused_class = [&](const RowReq& q) {
+        if (q.k == 0 || q.k > rows_fused_kmax(false)) return -1;
+        if (q.n > (uint64_t(1) << 18) && R < 64) return -1;  // long rows want many CTAs
+        for (int small = 1; small >= 0; --small) {
+            if (q.k > rows_fused_kmax(small)) continue;
+            const uint64_t cap = rows_fused_cand(small);
+            if (q.n <= cap) return small;
+            // expected candidates above the rp-th sample and their spread: (n/s) * Gamma(rp)
+            const double s = rows_fused_sample(small);
+            const double rr = static_cast<double>(q.k) * s / static_cast<double>(q.n);
+            const double rp = std::ceil(rr + 4.0 * std::sqrt(rr) + 3.0);
+            const double gap = static_cast<double>(q.n) / s;
+            if (q.n > s && gap * (rp + 5.0 * std::sqrt(rp)) <= static_cast<double>(cap)) return small;
+        }
+        return -1;
+    };
+    std::vector<uint64_t> g_off, g_len, g_tile{0};
+    std::vector<uint32_t> g_lead;
     for (int r = 0; r < R; ++r) {
         const RowReq& q = rows[r];
         rid[r] = r;
@@ -198,6 +221,22 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         row_k[r] = q.k;
         row_out[r] = q.out_off;
         row_in[r] = q.in_off;
+        const int fc = fused_class(q);
+        if (fc >= 0) {
+            frow[fc].push_back(r);
+            f_off[fc].push_back(q.in_off);
+            f_len[fc].push_back(q.n);
+            f_k[fc].push_back(q.k);
+            cap[r] = q.n;  // only used if the row falls back to the exact path
+            cand_off[r] = 0;
+            stats.elements_scanned += q.n;
+            continue;
+        }
+        grow.push_back(r);
+        g_off.push_back(q.in_off);
+        g_len.push_back(q.n);
+        g_lead.push_back(lead[r]);
+        g_tile.push_back(g_tile.back() + ceil_div(lead[r] + q.n, kTile));
         bool samp = q.k < q.n && q.n >= 4 * kSortCap;
         uint64_t ns = 0, rp = 0;
         if (samp) {
@@ -241,7 +280,16 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
     Plan P;
     const size_t o_rid = P.add(rid), o_off = P.add(off), o_len = P.add(len), o_lead = P.add(lead),
                  o_tile = P.add(tile_start), o_coff = P.add(cand_off), o_cap = P.add(cap),
-                 o_k = P.add(row_k), o_out = P.add(row_out), o_in = P.add(row_in);
+                 o_k = P.add(row_k), o_out = P.add(row_out), o_in = P.add(row_in),
+                 o_grow = P.add(grow), o_goff = P.add(g_off), o_glen = P.add(g_len), o_glead = P.add(g_lead),
+                 o_gtile = P.add(g_tile);
+    size_t o_f[2][4];
+    for (int v = 0; v < 2; ++v) {
+        o_f[v][0] = P.add(frow[v]);
+        o_f[v][1] = P.add(f_off[v]);
+        o_f[v][2] = P.add(f_len[v]);
+        o_f[v][3] = P.add(f_k[v]);
+    }
     size_t o_sg[2][6];
     for (int g = 0; g < 2; ++g) {
         o_sg[g][0] = P.add(sg[g].rid);
@@ -284,17 +332,34 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
     Call c{src, gather, at<uint64_t>(D, o_k), at<uint64_t>(D, o_out), at<uint64_t>(D, o_in), d_vals,
            d_idx, s, cap, cand_off, cand_total, std::vector<uint64_t>(R), R,
            at<uint64_t>(D, o_cap), at<uint64_t>(D, o_coff), d_pivots};
-    FinishPrep fp = prepare_finish(c, rid);
-    Rows all{R, at<uint32_t>(D, o_rid), at<uint64_t>(D, o_off), at<uint64_t>(D, o_len),
-             at<uint32_t>(D, o_lead), at<uint64_t>(D, o_tile)};
+    for (int v = 0; v < 2; ++v) {
+        if (frow[v].empty()) continue;
+        RowsFusedArgs fa{at<uint32_t>(D, o_f[v][0]), at<uint64_t>(D, o_f[v][1]), at<uint64_t>(D, o_f[v][2]),
+                         at<uint64_t>(D, o_f[v][3]), src, c.d_row_out, d_vals, d_idx, d_pivots,
+                         row_fail_.as<uint32_t>(), ctl_.as<uint32_t>(), nullptr};
+        if (profile_) {
+            dbg_.ensure(256);
+            fa.dbg = dbg_.as<unsigned long long>();
+        }
+        launch_rows_fused(static_cast<int>(frow[v].size()), fa, v == 1, s);
+        ++stats.kernel_launches;
+        mark("rows_fused", s);
+    }
     check(cudaEventRecord(ev_[1], s), "event");
-    launch_compact(tile_start.back(), all, src, T_.as<uint64_t>(), cand_a_.as<uint64_t>(), c.d_coff, c.d_cap,
-                   count_.as<unsigned long long>(), kmin_.as<unsigned long long>(),
-                   kmax_.as<unsigned long long>(), plan_args(c, fp), s);
-    check(cudaEventRecord(ev_[2], s), "event");
-    mark("compact", s);
-    stats.kernel_launches += 1;
-    launch_finish(c, fp);
+    if (!grow.empty()) {
+        FinishPrep fp = prepare_finish(c, grow);
+        Rows all{static_cast<int>(grow.size()), at<uint32_t>(D, o_grow), at<uint64_t>(D, o_goff),
+                 at<uint64_t>(D, o_glen), at<uint32_t>(D, o_glead), at<uint64_t>(D, o_gtile)};
+        launch_compact(g_tile.back(), all, src, T_.as<uint64_t>(), cand_a_.as<uint64_t>(), c.d_coff, c.d_cap,
+                       count_.as<unsigned long long>(), kmin_.as<unsigned long long>(),
+                       kmax_.as<unsigned long long>(), plan_args(c, fp), s);
+        stats.kernel_launches += 1;
+        check(cudaEventRecord(ev_[2], s), "event");
+        mark("compact", s);
+        launch_finish(c, fp);
+    } else {
+        check(cudaEventRecord(ev_[2], s), "event");
+    }
     check(cudaEventRecord(ev_[3], s), "event");
     uint32_t ctl[8];
     drain(c, ctl);

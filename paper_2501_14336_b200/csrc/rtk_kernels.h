@@ -24,6 +24,21 @@ struct SampleRows {       // rows whose threshold comes from a stratified sample
     unsigned long long* dbg; // optional phase timestamps (RTK_PROFILE)
 };
 
+struct RowsFusedArgs {    // K6 fast path: one CTA per short row (rtk_rows.cu)
+    const uint32_t* rid;
+    const uint64_t* off;
+    const uint64_t* len;
+    const uint64_t* k;
+    InputSrc in;
+    const uint64_t* row_out_off;  // by state row
+    uint32_t* out_vals;
+    uint64_t* out_idx;
+    uint32_t* pivots;             // by state row, nullable
+    uint32_t* row_fail;
+    uint32_t* flags;
+    unsigned long long* dbg;      // optional phase timestamps (RTK_PROFILE)
+};
+
 struct SortGroup {
     uint64_t off;        // element offset into buffer `buf`
     uint32_t len;        // <= kSortCap
@@ -139,6 +154,10 @@ void launch_pivots(int R, const uint64_t* row_out_off, const uint64_t* row_k, co
                    uint32_t* pivots, cudaStream_t s);
 void launch_first_digit_hist(uint64_t tiles, const Rows& rows, const InputSrc& in, unsigned int d,
                              unsigned long long* ghist, cudaStream_t s);
+void launch_rows_fused(int R, const RowsFusedArgs& a, bool small, cudaStream_t s);
+uint32_t rows_fused_kmax(bool small);
+uint32_t rows_fused_cand(bool small);
+uint32_t rows_fused_sample(bool small);
 void launch_remap_idx(uint64_t n, const uint64_t* cand_idx, uint32_t nblocks,
                       const uint64_t* block_start, const uint64_t* shard_base, uint64_t* idx,
                       cudaStream_t s);

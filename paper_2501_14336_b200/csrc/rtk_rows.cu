@@ -1,0 +1,528 @@
+// rtk_rows.cu — K6 fast path: one CTA owns one short row (LLM-vocab sampling, small k) and
+// finishes it in ONE kernel, entirely in shared memory after a single HBM read of the row.
+//
+//   1. threshold: stratified 2048-element sample -> in-CTA radix select -> T (composite)
+//      (rows with n <= kRowCand skip the sample: T = 0)
+//   2. stream the row once (32-byte loads, fused key transform), append K >= T to smem
+//   3. exact in-CTA radix select on the candidates: the k-th composite T2, #{K >= T2} == k
+//   4. keep exactly k, LSD radix sort them (descending) in smem, write (value, u64 index),
+//      pivot
+// A row whose sample threshold missed (count < k) or whose candidates overflow the smem
+// buffer is flagged and rerun by the host on the general multi-CTA path; correctness never
+// depends on the sample. The reference's per-task semantics (batch.hpp:284-291: each task
+// equals rtk::topk on its view) hold row by row.
+#include <cuda_runtime.h>
+
+#include "rtk_device.cuh"
+#include "rtk_kernels.h"
+
+namespace rtk_b200 {
+
+constexpr int kRowThreads = 512;
+constexpr int kRowWarps = kRowThreads / 32;
+constexpr int kRowCand = 8192;    // smem candidate capacity (u64), large-k variant
+constexpr int kRowKMax = 4096;    // largest k finished in the CTA
+constexpr int kRowCandS = 2048;   // small-k variant (k <= kRowKMaxS): smaller buffer, deeper ring
+constexpr int kRowKMaxS = 512;
+constexpr int kRowSampleS = 2048;  // sample size of the small variant (64 segments x 32)
+constexpr int kRowSampleL = 4096;  // large variant
+constexpr int kRowChunk = 2048;   // elements per TMA bulk chunk (8 KB)
+constexpr int kRowStages = 4;     // ring depth of the large-k variant (32 KB in flight per CTA)
+constexpr int kRowStagesS = 8;    // small-k variant (64 KB in flight per CTA)
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+                 "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// TMA 1-D bulk copy global -> shared, completion signalled on `bar` (expect_tx armed here)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(b),
+        "r"(parity)
+        : "memory");
+}
+
+__host__ __device__ __forceinline__ unsigned int rows_digit_hi(unsigned int pos) {
+    return pos == 53 ? 64u : (pos == 0 ? 9u : pos + 11u);
+}
+
+// Block-wide exclusive scan (kRowThreads) of a u32; *total = sum.
+__device__ __forceinline__ uint32_t row_block_scan(uint32_t v, uint32_t* s_w, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kRowWarps; ++w) {
+        const uint32_t x = s_w[w];
+        if (w < warp) pre += x;
+        tot += x;
+    }
+    __syncthreads();
+    *total = tot;
+    return pre + inc - v;
+}
+
+// In-CTA radix select over buf[0, m): the composite prefix T such that #{K >= T} ends in
+// [k, target] (target == k: exact k-th element). Returns T; *count_ge = #{K >= T}.
+// Early stop exactly as select_bin + radix_select (engine.hpp:231-241, 293-312).
+__device__ unsigned long long cta_radix_select(const unsigned long long* buf, uint32_t m, uint64_t k,
+                                               uint64_t target, uint32_t* hist, uint32_t* s_w,
+                                               unsigned long long* s_res, uint64_t* count_ge) {
+    constexpr int per = kBins / kRowThreads;  // 4 bins per thread, thread 0 owns the top bins
+    const int tid = threadIdx.x;
+    unsigned long long prefix = 0;
+    uint64_t k_rem = k, above = 0;
+    unsigned int pos = 53;
+    for (;;) {
+        for (int b = tid; b < kBins; b += kRowThreads) hist[b] = 0;
+        __syncthreads();
+        const unsigned int hi = rows_digit_hi(pos);
+        const unsigned long long pm = hi >= 64 ? 0ull : (prefix >> hi);
+        const uint32_t dmask = (1u << (hi - pos)) - 1u;
+        for (uint32_t i = tid; i < ((m + 31) & ~31u); i += kRowThreads) {
+            const bool in = i < m;
+            const unsigned long long K = in ? buf[i] : 0ull;
+            hist_add(hist, static_cast<uint32_t>(K >> pos) & dmask, in && (hi >= 64 || (K >> hi) == pm));
+        }
+        __syncthreads();
+        uint32_t c[per], sum = 0;
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            c[i] = hist[kBins - 1 - (tid * per + i)];
+            sum += c[i];
+        }
+        uint32_t tot;
+        const uint32_t before = row_block_scan(sum, s_w, &tot);
+        if (tid == 0) s_res[0] = ~0ull;
+        __syncthreads();
+        if (before < k_rem && before + sum >= k_rem) {
+            uint32_t cum = before;
+#pragma unroll
+            for (int i = 0; i < per; ++i) {
+                if (cum + c[i] >= k_rem) {
+                    s_res[0] = kBins - 1 - (tid * per + i);
+                    s_res[1] = cum;
+                    s_res[2] = c[i];
+                    break;
+                }
+                cum += c[i];
+            }
+        }
+        __syncthreads();
+        const unsigned long long bin = s_res[0], ab = s_res[1], cb = s_res[2];
+        __syncthreads();
+        if (bin == ~0ull) {  // cannot happen for k <= m
+            *count_ge = 0;
+            return 0;
+        }
+        prefix |= bin << pos;
+        above += ab;
+        k_rem -= ab;
+        const uint64_t cge = above + cb;
+        if (cge <= target || pos == 0) {
+            *count_ge = cge;
+            return prefix;
+        }
+        pos = pos == 9 ? 0u : pos - 11u;
+    }
+}
+
+// Bitonic sort (descending) of buf[0, n2) in shared memory, n2 a power of two; small k only.
+__device__ void cta_bitonic_desc(unsigned long long* buf, int n2) {
+    for (int kk = 2; kk <= n2; kk <<= 1) {
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            for (int i = threadIdx.x; i < (n2 >> 1); i += kRowThreads) {
+                const int lo = ((i & ~(jj - 1)) << 1) | (i & (jj - 1));
+                const int hi = lo + jj;
+                const unsigned long long x = buf[lo], y = buf[hi];
+                const bool desc = (lo & kk) == 0;
+                if (desc ? (x < y) : (x > y)) { buf[lo] = y; buf[hi] = x; }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <int KM, int CAND, int STAGES, int SAMPLE>
+__global__ void __launch_bounds__(kRowThreads, 2) k_rows_fused(RowsFusedArgs a) {
+    constexpr int kRowCand = CAND;
+    constexpr int kRowStages = STAGES;
+    constexpr int kRowSample = SAMPLE;
+    extern __shared__ unsigned long long cand[];  // kRowCand entries
+    __shared__ uint32_t hist[kBins];
+    __shared__ uint32_t s_w[kRowWarps];
+    __shared__ unsigned long long s_res[3];
+    __shared__ uint32_t s_m;
+    __shared__ unsigned long long bar[STAGES];
+    const int j = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned full = 0xffffffffu;
+    const uint32_t r = a.rid[j];
+    const uint64_t n = a.len[j], off = a.off[j], k = a.k[j];
+    const uint32_t* row = a.in.base + off;
+    unsigned long long* dbg = a.dbg;
+    int ndbg = 0;
+    auto stamp = [&]() {
+        if (dbg && blockIdx.x == 0 && threadIdx.x == 0 && ndbg < 30) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            dbg[ndbg++] = t;
+        }
+    };
+    stamp();
+
+    // ---- streaming ring: TMA 1-D bulk copies (cp.async.bulk) of 8 KB chunks into a 4-stage
+    // shared-memory ring with mbarrier completion; the first stages are in flight while the
+    // threshold is being selected.
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(row);
+    const uint32_t head = static_cast<uint32_t>(((16 - (a0 & 15)) & 15) >> 2);  // to 16-B alignment
+    const uint64_t body = n > head ? n - head : 0;
+    const uint64_t nchunks = body / kRowChunk;
+    const uint32_t* bsrc = row + head;
+    uint32_t* ring = reinterpret_cast<uint32_t*>(cand + kRowCand);
+    if (tid == 0) {
+        for (int st = 0; st < kRowStages; ++st) mbar_init(&bar[st], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (uint64_t c = 0; c < nchunks && c < static_cast<uint64_t>(kRowStages); ++c)
+            bulk_g2s(ring + c * kRowChunk, bsrc + c * kRowChunk, kRowChunk * 4, &bar[c]);
+    }
+
+    // ---- 1. threshold -------------------------------------------------------------------
+    stamp();
+    unsigned long long T = 0;
+    if (n > static_cast<uint64_t>(kRowCand)) {
+        const uint64_t nseg = kRowSample / 32;
+        const uint64_t stride_fp = ((n - 32) << 16) / (nseg - 1);
+        for (int e = tid; e < kRowSample; e += kRowThreads) {
+            const uint64_t idx = ((static_cast<uint64_t>(e / 32) * stride_fp) >> 16) + (e & 31);
+            cand[e] = composite(make_key(a.in, __ldg(row + idx)), idx);
+        }
+        __syncthreads();
+        const double rr = static_cast<double>(k) * kRowSample / static_cast<double>(n);
+        const uint64_t rp = static_cast<uint64_t>(ceil(rr + 4.0 * sqrt(rr) + 3.0));
+        uint64_t cge;
+        // exact rp-th sample composite: keeps the candidate count (and its spread) minimal
+        const uint64_t rpc = rp < kRowSample ? rp : kRowSample;
+        T = cta_radix_select(cand, kRowSample, rpc, rpc, hist, s_w, s_res, &cge);
+    }
+    if (tid == 0) s_m = 0;
+    __syncthreads();
+    stamp();
+
+    // ---- 2. one streaming read of the row --------------------------------------------------
+    const uint32_t thi = static_cast<uint32_t>(T >> 32), tlo = static_cast<uint32_t>(T);
+    auto append = [&](uint32_t mask, const uint32_t* keys, uint32_t (*idx_of)(uint32_t, const void*),
+                      const void* ctx) {};
+    (void)append;
+    // appends up to 4 hits per thread (bit i of mask = element i) with one warp-aggregated
+    // shared atomic; idx = ibase + i
+    auto push4 = [&](uint32_t mask, const uint32_t (&key)[4], uint32_t ibase) {
+        if (!__any_sync(full, mask)) return;
+        const uint32_t c = __popc(mask);
+        uint32_t inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(full, inc, d);
+            if (lane >= d) inc += o;
+        }
+        const uint32_t wtot = __shfl_sync(full, inc, 31);
+        uint32_t wbase = 0;
+        if (lane == 31) wbase = atomicAdd(&s_m, wtot);
+        wbase = __shfl_sync(full, wbase, 31);
+        uint32_t o = wbase + inc - c;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if ((mask >> i) & 1u) {
+                if (o < kRowCand)
+                    cand[o] = (static_cast<unsigned long long>(key[i]) << 32) | ~(ibase + i);
+                ++o;
+            }
+    };
+    auto test4 = [&](uint32_t (&key)[4], uint32_t ibase, uint32_t valid) {
+        uint32_t mask = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            key[i] = key_of<KM>(key[i], a.in.a_s);
+            const bool hit = ((valid >> i) & 1u) && (key[i] > thi || (key[i] == thi && ~(ibase + i) >= tlo));
+            mask |= static_cast<uint32_t>(hit) << i;
+        }
+        return mask;
+    };
+    // consume the ring in groups of half its depth: one block barrier per group, then the
+    // group's stages are refilled while the other half is being consumed
+    constexpr int G = kRowStages / 2;
+    for (uint64_t c0 = 0; c0 < nchunks; c0 += G) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const uint64_t c = c0 + g;
+            if (c >= nchunks) break;
+            const int st = static_cast<int>(c % kRowStages);
+            mbar_wait(&bar[st], static_cast<uint32_t>((c / kRowStages) & 1));
+            const uint4 q = reinterpret_cast<const uint4*>(ring + st * kRowChunk)[tid];
+            uint32_t key[4] = {q.x, q.y, q.z, q.w};
+            const uint32_t ibase = head + static_cast<uint32_t>(c * kRowChunk) + tid * 4;
+            const uint32_t mask = test4(key, ibase, 0xFu);
+            push4(mask, key, ibase);
+        }
+        __syncthreads();  // the group's stages are fully consumed
+        if (tid == 0) {
+            for (int g = 0; g < G; ++g) {
+                const uint64_t c = c0 + g;
+                if (c + kRowStages < nchunks)
+                    bulk_g2s(ring + (c % kRowStages) * kRowChunk, bsrc + (c + kRowStages) * kRowChunk,
+                             kRowChunk * 4, &bar[c % kRowStages]);
+            }
+        }
+    }
+    // head (< 4 elements before 16-byte alignment) and tail (< one chunk) with plain loads
+    {
+        const uint64_t t0 = head + nchunks * kRowChunk;
+        const uint64_t rest = n - t0;  // < kRowChunk + ...
+        for (uint64_t b0 = 0; b0 < rest + head; b0 += 4 * kRowThreads) {
+            uint32_t key[4];
+            uint32_t valid = 0;
+            uint32_t ib = 0;
+            const uint64_t e = b0 + tid * 4;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                // positions [0, head) then [t0, n)
+                const uint64_t g = e + i;
+                uint64_t idx = g < head ? g : t0 + (g - head);
+                const bool ok = g < head ? true : (g - head) < rest;
+                key[i] = ok ? __ldg(row + idx) : 0u;
+                valid |= static_cast<uint32_t>(ok) << i;
+                if (i == 0) ib = static_cast<uint32_t>(idx);
+            }
+            // indices are not contiguous across the head/tail seam: push one element at a time
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint64_t g = e + i;
+                const uint32_t idx = static_cast<uint32_t>(g < head ? g : t0 + (g - head));
+                uint32_t one[4] = {key[i], 0u, 0u, 0u};
+                const uint32_t m1 = test4(one, idx, (valid >> i) & 1u);
+                push4(m1, one, idx);
+            }
+            (void)ib;
+        }
+    }
+    __syncthreads();
+    stamp();
+    const uint32_t m = s_m;
+    if (m < k || m > static_cast<uint32_t>(kRowCand)) {  // sample missed / overflow: general path
+        if (tid == 0) {
+            a.row_fail[r] = 1;
+            atomicOr(a.flags, kFlagFail);
+        }
+        return;
+    }
+
+    // ---- 3. exact k-th composite among the candidates, keep exactly k ----------------------
+    if (m > k) {
+        uint64_t cge;
+        const unsigned long long T2 = cta_radix_select(cand, m, k, k, hist, s_w, s_res, &cge);
+        // compaction to cand[0, k): read everything first, then write
+        constexpr int PT = kRowCand / kRowThreads;  // 16
+        unsigned long long keep[PT];
+        uint32_t km = 0;
+#pragma unroll
+        for (int q = 0; q < PT; ++q) {
+            const uint32_t i = q * kRowThreads + tid;
+            keep[q] = (i < m) ? cand[i] : 0ull;
+            km |= static_cast<uint32_t>(i < m && keep[q] >= T2) << q;
+        }
+        if (tid == 0) s_m = 0;
+        __syncthreads();
+        const uint32_t c = __popc(km);
+        uint32_t inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o2 = __shfl_up_sync(full, inc, d);
+            if (lane >= d) inc += o2;
+        }
+        const uint32_t wtot = __shfl_sync(full, inc, 31);
+        uint32_t wbase = 0;
+        if (lane == 31 && wtot) wbase = atomicAdd(&s_m, wtot);
+        wbase = __shfl_sync(full, wbase, 31);
+        uint32_t o = wbase + inc - c;
+#pragma unroll
+        for (int q = 0; q < PT; ++q)
+            if ((km >> q) & 1u) cand[o++] = keep[q];
+        __syncthreads();
+    }
+    const uint32_t kk = static_cast<uint32_t>(k);
+    stamp();
+
+    if (kk <= static_cast<uint32_t>(kRowKMaxS)) {
+        // ---- 4'. small k: bitonic sort in smem (pad with 0 = smallest composite) ------------
+        int n2 = 1;
+        while (n2 < static_cast<int>(kk)) n2 <<= 1;
+        for (int i = kk + tid; i < n2; i += kRowThreads) cand[i] = 0ull;
+        __syncthreads();
+        cta_bitonic_desc(cand, n2);
+        const uint64_t oo = a.row_out_off[r];
+        for (uint32_t p = tid; p < kk; p += kRowThreads) {
+            const unsigned long long K = cand[p];
+            const uint32_t kv = static_cast<uint32_t>(K >> 32);
+            const uint32_t idx = ~static_cast<uint32_t>(K);
+            uint32_t val;
+            if (a.in.scaled) val = __ldg(row + idx);
+            else if (a.in.dtype == kF32) val = decode_f32_bits(kv, a.in.smallest);
+            else val = a.in.smallest ? ~kv : kv;
+            a.out_vals[oo + p] = val;
+            a.out_idx[oo + p] = idx;
+            if (p == kk - 1 && a.pivots) a.pivots[r] = val;
+        }
+        stamp();
+        return;
+    }
+    // ---- 4. LSD radix sort of the k survivors (descending), 8 items per thread -------------
+    // warp w owns positions [256w, 256w+256); item q of lane l is 256w + 32q + l.
+    constexpr int IT = kRowKMax / kRowThreads;  // 8
+    unsigned long long key[IT];
+    unsigned long long orv = 0;
+    const unsigned long long ref = cand[0];
+#pragma unroll
+    for (int q = 0; q < IT; ++q) {
+        const uint32_t p = warp * 256 + q * 32 + lane;
+        key[q] = p < kk ? cand[p] : 0ull;
+        if (p < kk) orv |= key[q] ^ ref;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) orv |= __shfl_xor_sync(full, orv, d);
+    __syncthreads();
+    if (tid == 0) s_res[0] = 0;
+    __syncthreads();
+    if (lane == 0) atomicOr(&s_res[0], orv);
+    __syncthreads();
+    orv = s_res[0];
+    const int nbits = orv ? 64 - __clzll(orv) : 0;
+    unsigned long long* tmp = cand + kRowKMax;
+    // per-warp digit counters live in the (now idle) streaming ring
+    uint32_t (*cnt)[256] = reinterpret_cast<uint32_t (*)[256]>(cand + kRowCand);
+    const unsigned lt = (1u << lane) - 1u;
+    for (int lo = 0; lo < nbits; lo += 8) {
+        if (((orv >> lo) & 0xFFull) == 0) continue;  // digit constant across the group: no-op pass
+        for (int i = tid; i < kRowWarps * 256; i += kRowThreads) (&cnt[0][0])[i] = 0;
+        __syncthreads();
+        uint32_t dig[IT], rk[IT];
+#pragma unroll
+        for (int q = 0; q < IT; ++q) {
+            const uint32_t p = warp * 256 + q * 32 + lane;
+            dig[q] = p < kk ? 255u - static_cast<uint32_t>((key[q] >> lo) & 0xFFu) : 255u;
+            const unsigned peers = __match_any_sync(full, dig[q]);
+            const uint32_t b0 = cnt[warp][dig[q]];
+            rk[q] = b0 + __popc(peers & lt);
+            __syncwarp();
+            if ((peers & lt) == 0) cnt[warp][dig[q]] = b0 + __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        {
+            // exclusive scan over (digit, warp): thread t < 256 handles digit t, all warps
+            uint32_t cs[kRowWarps], sum = 0;
+            if (tid < 256) {
+#pragma unroll
+                for (int w = 0; w < kRowWarps; ++w) { cs[w] = cnt[w][tid]; sum += cs[w]; }
+            }
+            uint32_t tot;
+            uint32_t pre = row_block_scan(tid < 256 ? sum : 0u, s_w, &tot);
+            if (tid < 256) {
+#pragma unroll
+                for (int w = 0; w < kRowWarps; ++w) { cnt[w][tid] = pre; pre += cs[w]; }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < IT; ++q) tmp[cnt[warp][dig[q]] + rk[q]] = key[q];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < IT; ++q) key[q] = tmp[warp * 256 + q * 32 + lane];
+        __syncthreads();
+    }
+
+    stamp();
+    // ---- 5. gather ------------------------------------------------------------------------
+    const uint64_t oo = a.row_out_off[r];
+#pragma unroll
+    for (int q = 0; q < IT; ++q) {
+        const uint32_t p = warp * 256 + q * 32 + lane;
+        if (p >= kk) continue;
+        const unsigned long long K = key[q];
+        const uint32_t kv = static_cast<uint32_t>(K >> 32);
+        const uint32_t idx = ~static_cast<uint32_t>(K);
+        uint32_t val;
+        if (a.in.scaled) val = __ldg(row + idx);
+        else if (a.in.dtype == kF32) val = decode_f32_bits(kv, a.in.smallest);
+        else val = a.in.smallest ? ~kv : kv;
+        a.out_vals[oo + p] = val;
+        a.out_idx[oo + p] = idx;
+        if (p == kk - 1 && a.pivots) a.pivots[r] = val;
+    }
+    stamp();
+    if (dbg && blockIdx.x == 0 && threadIdx.x == 0) dbg[31] = ndbg;
+}
+
+template <int KM, int CAND, int STAGES, int SAMPLE>
+static void rows_km(int R, const RowsFusedArgs& a, cudaStream_t s) {
+    constexpr size_t smem = CAND * sizeof(unsigned long long) + STAGES * kRowChunk * sizeof(uint32_t);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_rows_fused<KM, CAND, STAGES, SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        configured = true;
+    }
+    k_rows_fused<KM, CAND, STAGES, SAMPLE><<<R, kRowThreads, smem, s>>>(a);
+}
+
+template <int CAND, int STAGES, int SAMPLE>
+static void rows_variant(int R, const RowsFusedArgs& a, cudaStream_t s) {
+    switch (key_mode(a.in.dtype, a.in.smallest, a.in.scaled)) {
+        case kKmF32L: rows_km<kKmF32L, CAND, STAGES, SAMPLE>(R, a, s); break;
+        case kKmF32S: rows_km<kKmF32S, CAND, STAGES, SAMPLE>(R, a, s); break;
+        case kKmF32LScaled: rows_km<kKmF32LScaled, CAND, STAGES, SAMPLE>(R, a, s); break;
+        case kKmF32SScaled: rows_km<kKmF32SScaled, CAND, STAGES, SAMPLE>(R, a, s); break;
+        case kKmU32L: rows_km<kKmU32L, CAND, STAGES, SAMPLE>(R, a, s); break;
+        default: rows_km<kKmU32S, CAND, STAGES, SAMPLE>(R, a, s); break;
+    }
+}
+
+// small = rows whose k and expected candidate count fit the small-buffer variant
+void launch_rows_fused(int R, const RowsFusedArgs& a, bool small, cudaStream_t s) {
+    if (R <= 0) return;
+    if (small) rows_variant<kRowCandS, kRowStagesS, kRowSampleS>(R, a, s);
+    else rows_variant<kRowCand, kRowStages, kRowSampleL>(R, a, s);
+}
+
+uint32_t rows_fused_kmax(bool small) { return small ? kRowKMaxS : kRowKMax; }
+uint32_t rows_fused_cand(bool small) { return small ? kRowCandS : kRowCand; }
+uint32_t rows_fused_sample(bool small) { return small ? kRowSampleS : kRowSampleL; }
+
+}  // namespace rtk_b200

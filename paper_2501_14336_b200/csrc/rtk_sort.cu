@@ -332,6 +332,8 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
         const int nbits = orv ? 64 - __clzll(orv) : 0;
 
         for (int lo = 0; lo < nbits; lo += 8) {
+            if (((orv >> lo) & 0xFFull) == 0) continue;  // digit constant across the group
+        if (((orv >> lo) & 0xFFull) == 0) continue;  // digit constant across the group: no-op pass
             for (int i = tid; i < (kSortThreads / 32) * 256; i += kSortThreads) (&cnt[0][0])[i] = 0;
             __syncthreads();
             uint32_t dig[kSortItems], rk[kSortItems];
