@@ -66,6 +66,8 @@ void DevBuf::release() {
 Engine::Engine(int device) : device_(device) {
     const char* p = std::getenv("RTK_PROFILE");
     profile_ = p && *p && *p != '0';
+    if (const char* sr = std::getenv("RTK_SAMPLE_R")) sample_r_ = std::max(1.0, std::atof(sr));
+    if (const char* mq = std::getenv("RTK_MSD_Q")) msd_q_max_ = std::max(1, std::atoi(mq));
     const char* cs = std::getenv("RTK_COUNT_STATS");
     count_stats_ = profile_ || (cs && *cs && *cs != '0');
 }
@@ -77,7 +79,7 @@ Engine::~Engine() {
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     for (DevBuf* b : {&arena_, &sel_, &T_, &count_, &kmin_, &kmax_, &ghist_, &samples_, &cand_a_,
-                      &cand_b_, &seg_hist_, &gcursor_, &bstart_, &dcap_, &dcoff_, &ctl_, &row_fail_, &groups_, &slots0_, &slotsA_, &slotsB_, &done_, &seg_ticket_, &io_in, &io_vals, &io_idx,
+                      &cand_b_, &seg_hist_, &gcursor_, &bstart_, &dcap_, &dcoff_, &ctl_, &row_fail_, &groups_, &slots0_, &slotsA_, &slotsB_, &done_, &seg_ticket_, &wgroups_, &ctot_, &io_in, &io_vals, &io_idx,
                       &io_piv, &io_aux})
         b->release();
 }
@@ -175,6 +177,8 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
     check(cudaEventRecord(ev_[0], s), "event");
     mark("start", s);
     group_base_ = 0;
+    wgroup_base_ = 0;
+    bar_gen_ = 0;
     InputSrc src{d_base, dtype, smallest, scaled ? 1 : 0, a_s};
     const uint64_t base_words = reinterpret_cast<uintptr_t>(d_base) / 4;
 
@@ -186,6 +190,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         std::vector<uint32_t> rid;
         std::vector<uint64_t> off, len, nseg, k, target;
         uint32_t per_cta = 0;
+        int cs = 1;  // cluster size
     } sg[2];  // [0]: one CTA per row, [1]: a 16-CTA cluster per row
     uint64_t cand_total = 0;
     // K6 routing: short rows with small k finish in one CTA each (k_rows_fused); the rest take
@@ -241,8 +246,16 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         uint64_t ns = 0, rp = 0;
         if (samp) {
             // stratified sample: 2^-7 of huge rows (cluster of 8 CTAs), 2^-6 of the others
-            ns = q.n >= (uint64_t(1) << 22) ? std::min<uint64_t>(uint64_t(1) << 17, q.n / 128)
-                                             : std::min<uint64_t>(8192, std::max<uint64_t>(2048, q.n / 64));
+            // huge rows: enough samples that ~sample_r_ of them land above the threshold
+            // (r = k s / n), 2^14..2^17 and <= n/128; a 16-CTA cluster per row when s > 8192
+            if (q.n >= (uint64_t(1) << 22)) {
+                const double want = static_cast<double>(sample_r_) * static_cast<double>(q.n) / static_cast<double>(q.k);
+                uint64_t p2 = uint64_t(1) << 14;
+                while (p2 < want && p2 < (uint64_t(1) << 17)) p2 <<= 1;
+                ns = std::min<uint64_t>(p2, q.n / 128);
+            } else {
+                ns = std::min<uint64_t>(8192, std::max<uint64_t>(2048, q.n / 64));
+            }
             ns &= ~uint64_t(31);
             const double rr = static_cast<double>(q.k) * static_cast<double>(ns) / static_cast<double>(q.n);
             rp = static_cast<uint64_t>(std::ceil(rr + 4.0 * std::sqrt(rr) + 3.0));
@@ -260,7 +273,8 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
             g.nseg.push_back(ns / 32);
             g.k.push_back(rp);
             g.target.push_back(rp + rp / 10 + 8);
-            g.per_cta = std::max<uint32_t>(g.per_cta, static_cast<uint32_t>(ns / (grp ? 16 : 1)));
+            if (grp) g.cs = std::max<int>(g.cs, static_cast<int>(std::min<uint64_t>(16, ns / 4096)));
+            g.per_cta = std::max<uint32_t>(g.per_cta, static_cast<uint32_t>(ns / g.cs));
         } else {
             cap[r] = q.n;
         }
@@ -321,7 +335,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         SampleRows sr{at<uint32_t>(D, o_sg[g][0]), at<uint64_t>(D, o_sg[g][1]), at<uint64_t>(D, o_sg[g][2]),
                       at<uint64_t>(D, o_sg[g][3]), at<uint64_t>(D, o_sg[g][4]), at<uint64_t>(D, o_sg[g][5]),
                       profile_ ? dbg_.as<unsigned long long>() : nullptr};
-        launch_sample_select(static_cast<int>(sg[g].rid.size()), g ? 16 : 1, sg[g].per_cta, sr, src,
+        launch_sample_select(static_cast<int>(sg[g].rid.size()), sg[g].cs, sg[g].per_cta, sr, src,
                              T_.as<uint64_t>(), s);
         check(cudaGetLastError(), "sample_select launch");
         ++stats.kernel_launches;
@@ -396,16 +410,23 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
 Engine::FinishPrep Engine::prepare_finish(Call& c, const std::vector<uint32_t>& rids) {
     FinishPrep f{};
     f.NR = static_cast<int>(rids.size());
-    std::vector<uint64_t> tiles(f.NR + 1, 0);
+    // level-0 MSD bounds from the capacity (the device picks bits = fine_bits(m) <= fine_bits(cap))
+    uint64_t cta_groups = f.NR, warp_groups = 0, max_cap = 0;
     for (int j = 0; j < f.NR; ++j) {
         const uint64_t cp = c.cap[rids[j]];
-        const bool big = cp > kSortCap;
-        f.big_rows += big;
-        tiles[j + 1] = tiles[j] + (big ? ceil_div(cp + 3, kTile64) : 0);
+        if (cp <= kSortCap) continue;
+        ++f.big_rows;
+        max_cap = std::max(max_cap, cp);
+        const uint64_t bins = uint64_t(1) << fine_bits(cp);
+        cta_groups += std::min<uint64_t>(bins, cp / (kWarpGroupMax + 1) + 1);
+        warp_groups += std::min<uint64_t>(bins, cp);
     }
-    f.ntiles = tiles.back();
-    f.max_groups = f.NR + f.big_rows * kBins;
+    f.cs = msd_cluster_size(max_cap);
+    f.max_cap = max_cap;
+    f.max_groups = cta_groups;
+    f.max_wgroups = warp_groups;
     groups_.ensure(sizeof(SortGroup) * (group_base_ + f.max_groups), /*keep=*/true, c.s);
+    wgroups_.ensure(sizeof(SortGroup) * std::max<uint64_t>(wgroup_base_ + f.max_wgroups, 1), /*keep=*/true, c.s);
     slots0_.ensure(sizeof(SegSlot) * std::max(f.NR, 1));
     const uint64_t max_next = c.cand_total / kSortCap + f.NR + 1;
     slotsA_.ensure(sizeof(SegSlot) * max_next);
@@ -415,14 +436,13 @@ Engine::FinishPrep Engine::prepare_finish(Call& c, const std::vector<uint32_t>& 
     bstart_.ensure(4ull * kBins * std::max<int>(f.NR, 1));
     cand_b_.ensure(8 * std::max<uint64_t>(c.cand_total, 1));
     next_cap_ = static_cast<uint32_t>(max_next);
-    Plan P;
-    f.o_rid = P.add(rids);
-    f.o_tiles = P.add(tiles);
-    f.D = upload(P, c.s);
     uint32_t* ctl = ctl_.as<uint32_t>();
     f.gl = GroupList{groups_.as<SortGroup>(), ctl + 1, static_cast<uint32_t>(group_base_ + f.max_groups)};
+    f.wgl = GroupList{wgroups_.as<SortGroup>(), ctl + 5, static_cast<uint32_t>(wgroup_base_ + f.max_wgroups)};
     f.nextA = SlotList{slotsA_.as<SegSlot>(), ctl + 3, next_cap_};
     group_base_ += f.max_groups;
+    wgroup_base_ += f.max_wgroups;
+    wgroup_cap_ = static_cast<uint32_t>(wgroup_base_);
     return f;
 }
 
@@ -445,18 +465,37 @@ PlanArgs Engine::plan_args(const Call& c, const FinishPrep& f) {
 void Engine::launch_finish(Call& c, const FinishPrep& f) {
     if (f.NR == 0) return;
     if (f.big_rows) {
-        SegPlanArgs pa{seg_hist_.as<uint32_t>(), gcursor_.as<uint32_t>(), c.d_row_k, bstart_.as<uint32_t>(),
-                       f.gl, 1, f.nextA, ctl_.as<uint32_t>(), seg_ticket_.as<uint32_t>()};
-        launch_seg_hist(f.ntiles, slots0_.as<SegSlot>(), f.NR, at<uint64_t>(f.D, f.o_tiles),
-                        cand_a_.as<uint64_t>(), pa, c.s);
-        mark("seg_hist+plan", c.s);
-        launch_seg_scatter(f.ntiles, slots0_.as<SegSlot>(), f.NR, at<uint64_t>(f.D, f.o_tiles),
-                           cand_a_.as<uint64_t>(), cand_b_.as<uint64_t>(), bstart_.as<uint32_t>(),
-                           gcursor_.as<uint32_t>(), c.s);
-        stats.kernel_launches += 2;
-        mark("seg_scatter", c.s);
+        FineArgs fa{c.d_row_k, f.gl, f.wgl, f.nextA, ctl_.as<uint32_t>(), nullptr, 1, nullptr, nullptr, 0};
+        if (profile_) {
+            dbg_.ensure(256);
+            fa.dbg = dbg_.as<unsigned long long>();
+        }
+        // one huge slot: spread it over Q co-resident 8-CTA clusters (>= ~8K composites per CTA)
+        int cs = f.cs;
+        if (f.NR == 1 && f.cs == 16) {
+            const uint64_t want = std::max<uint64_t>(1, f.max_cap / (8 * 8192));
+            const uint32_t Q = static_cast<uint32_t>(std::min<uint64_t>(
+                std::min<uint64_t>(msd_q_max_, static_cast<uint64_t>(msd_max_clusters(8))), want));
+            if (Q > 1) {
+                cs = 8;
+                fa.Q = Q;
+                ctot_.ensure(4ull * fa.Q << kMsdMaxBits);
+                fa.ctot = ctot_.as<uint32_t>();
+                fa.bar = ctl_.as<uint32_t>() + 7;
+                bar_gen_ += fa.Q * cs;
+                fa.bar_target = bar_gen_;
+            }
+        }
+        if (!launch_msd_cluster(f.NR, cs, slots0_.as<SegSlot>(), cand_a_.as<uint64_t>(), cand_b_.as<uint64_t>(), fa, c.s)) {
+            bar_gen_ -= fa.Q * cs;
+            fa.Q = 1;
+            launch_msd_cluster(f.NR, f.cs, slots0_.as<SegSlot>(), cand_a_.as<uint64_t>(), cand_b_.as<uint64_t>(), fa, c.s);
+        }
+        check(cudaGetLastError(), "msd launch");
+        stats.kernel_launches += 1;
+        mark("msd", c.s);
     }
-    launch_sort_groups(static_cast<uint32_t>(f.max_groups), sort_args(c, f.gl), c.s);
+    launch_sort_groups(static_cast<uint32_t>(f.max_groups + f.max_wgroups / 8 + 1), sort_args(c, f.gl), c.s);
     mark("sort+pivots", c.s);
     stats.kernel_launches += 1;
 }
@@ -465,6 +504,8 @@ SortArgs Engine::sort_args(const Call& c, const GroupList& gl) {
     SortArgs a{};
     a.groups = gl;
     a.work = ctl_.as<uint32_t>() + 2;
+    a.wgroups = GroupList{wgroups_.as<SortGroup>(), ctl_.as<uint32_t>() + 5, wgroup_cap_};
+    a.wwork = ctl_.as<uint32_t>() + 6;
     a.buf0 = cand_a_.as<unsigned long long>();
     a.buf1 = cand_b_.as<unsigned long long>();
     a.row_k = c.d_row_k;
@@ -520,6 +561,7 @@ void Engine::drain(Call& c, uint32_t (&ctl)[8]) {
         // flags = 0, work = groups so far, next list count = 0
         check(cudaMemsetAsync(dctl, 0, 4, c.s), "memset");
         check(cudaMemcpyAsync(dctl + 2, dctl + 1, 4, cudaMemcpyDeviceToDevice, c.s), "work");
+        check(cudaMemcpyAsync(dctl + 6, dctl + 5, 4, cudaMemcpyDeviceToDevice, c.s), "wwork");
         check(cudaMemsetAsync(dctl + (list == 0 ? 4 : 3), 0, 4, c.s), "memset");
         check(cudaMemsetAsync(seg_hist_.p, 0, 4ull * kBins * nslots, c.s), "memset");
         check(cudaMemsetAsync(seg_ticket_.p, 0, 4ull * nslots, c.s), "memset");
@@ -644,6 +686,7 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
     check(cudaMemsetAsync(ctl_.p, 0, 4, s), "memset");
     check(cudaMemsetAsync(ctl_.as<uint32_t>() + 3, 0, 8, s), "memset");
     check(cudaMemcpyAsync(ctl_.as<uint32_t>() + 2, ctl_.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToDevice, s), "work");
+    check(cudaMemcpyAsync(ctl_.as<uint32_t>() + 6, ctl_.as<uint32_t>() + 5, 4, cudaMemcpyDeviceToDevice, s), "wwork");
     FinishPrep fp = prepare_finish(c, fb);
     check(cudaMemsetAsync(seg_hist_.p, 0, 4ull * kBins * fb.size(), s), "memset");
     check(cudaMemsetAsync(seg_ticket_.p, 0, 4ull * fb.size(), s), "memset");

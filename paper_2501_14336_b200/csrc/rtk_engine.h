@@ -91,6 +91,7 @@ private:
     };
     bool profile_ = false;
     bool count_stats_ = false;   // read candidate counts back (stats.candidates)
+    double sample_r_ = 512.0;    // huge rows: target sample rank k*s/n (RTK_SAMPLE_R)
     std::vector<Mark> marks_;
     // State of one run() call shared by the finish / fallback stages.
     struct Call {
@@ -116,7 +117,10 @@ private:
         uint64_t big_rows = 0, max_groups = 0, ntiles = 0;
         uint8_t* D = nullptr;
         size_t o_rid = 0, o_tiles = 0;
-        GroupList gl{};
+        uint64_t max_wgroups = 0;
+        int cs = 2;
+        uint64_t max_cap = 0;
+        GroupList gl{}, wgl{};
         SlotList nextA{};
     };
     FinishPrep prepare_finish(Call& c, const std::vector<uint32_t>& rids);
@@ -140,9 +144,12 @@ private:
     cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
     DevBuf sel_, T_, count_, kmin_, kmax_, ghist_, samples_, cand_a_, cand_b_, seg_hist_,
         gcursor_, bstart_, dcap_, dcoff_, ctl_, row_fail_, groups_, slots0_, slotsA_, slotsB_, done_,
-        seg_ticket_, dbg_;
-    uint64_t group_base_ = 0;
+        seg_ticket_, dbg_, wgroups_, ctot_;
+    uint64_t group_base_ = 0, wgroup_base_ = 0;
     uint32_t next_cap_ = 0;
+    uint32_t wgroup_cap_ = 0;
+    uint32_t bar_gen_ = 0;        // grid-barrier target of the level-0 MSD (ctl[7], reset per call)
+    int msd_q_max_ = 8;           // clusters per huge slot (RTK_MSD_Q)
 };
 
 }  // namespace rtk_b200

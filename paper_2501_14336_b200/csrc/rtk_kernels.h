@@ -53,7 +53,9 @@ struct SegSlot {        // one MSD segment; len == 0 means inactive
     uint64_t len;
     uint64_t rank_base;
     uint32_t rid;
-    uint32_t pos;        // digit = (K >> pos) & 2047
+    uint32_t pos;        // digit = (K >> pos) & (2^bits - 1)
+    uint32_t bits;       // level 0 (fine MSD): 11..16; deeper levels: kDigit
+    uint32_t pad;
 };
 
 struct GroupList {
@@ -80,6 +82,42 @@ struct SegPlanArgs {      // bucket plan of one MSD level (fused into k_seg_hist
     uint32_t* ticket;        // per slot: tiles finished
 };
 
+// Level-0 MSD (k_msd_cluster): one thread-block cluster of CS CTAs per slot, chunk c of the
+// slot per CTA. Shared-memory histograms of one 2^bits-bin digit; the column scan over the CS
+// CTAs runs through distributed shared memory (per-chunk bucket offsets + totals), CTA 0 plans
+// the buckets, every CTA scatters its chunk with shared-memory cursors — one kernel, no global
+// matrix, no global atomics on the data path. Buckets of <= kWarpGroupMax elements become warp
+// groups (tiny/mid ones packed), <= kSortCap CTA groups, larger ones the next (11-bit) level.
+constexpr uint32_t kTinyMax = 32;       // packed by 32-quantum  -> warp group <= 63
+constexpr uint32_t kMidMax = 128;       // packed by 128-quantum -> warp group <= 255
+constexpr uint32_t kWarpGroupMax = 256; // solo warp group up to this size
+constexpr int kMsdMaxBits = 14;
+struct FineArgs {
+    const uint64_t* row_k;
+    GroupList groups;        // CTA groups
+    GroupList wgroups;       // warp groups (<= kWarpGroupMax)
+    SlotList next;
+    uint32_t* flags;
+    unsigned long long* dbg; // optional phase timestamps (RTK_PROFILE)
+    // multi-cluster mode (Q > 1): ONE slot over Q co-resident clusters (cooperative launch),
+    // cluster totals exchanged through ctot (Q x 2^bits) after one grid barrier
+    uint32_t Q;
+    uint32_t* ctot;
+    uint32_t* bar;           // grid barrier counter (monotonic within a call)
+    uint32_t bar_target;
+};
+
+// digit bits of the level-0 MSD for m candidates (device: m; host: the capacity bound)
+__host__ __device__ inline uint32_t fine_bits(uint64_t m) {
+    return m <= 16384 ? 11u : (m <= (uint64_t(1) << 18) ? 13u : 14u);
+}
+// cluster size for the largest slot of a launch
+inline int msd_cluster_size(uint64_t max_cap) {
+    int cs = 2;
+    while (cs < 16 && static_cast<uint64_t>(cs) * 16384 < max_cap) cs <<= 1;
+    return cs;
+}
+
 struct PlanArgs {         // per-row plan after the compaction (fused into k_compact)
     const uint64_t* cap;
     const uint64_t* row_k;
@@ -97,6 +135,8 @@ struct PlanArgs {         // per-row plan after the compaction (fused into k_com
 struct SortArgs {
     GroupList groups;
     uint32_t* work;
+    GroupList wgroups;       // warp-sized groups (<= kWarpGroupMax)
+    uint32_t* wwork;
     const unsigned long long* buf0;
     const unsigned long long* buf1;
     const uint64_t* row_k;
@@ -149,6 +189,10 @@ void launch_seg_hist(uint64_t tiles, const SegSlot* slots, int nslots, const uin
 void launch_seg_scatter(uint64_t tiles, const SegSlot* slots, int nslots, const uint64_t* tile_start,
                         const uint64_t* src, uint64_t* dst, const uint32_t* bstart, uint32_t* gcursor,
                         cudaStream_t s);
+int msd_max_clusters(int cs);  // co-resident clusters of cs CTAs (occupancy API)
+// returns false if a multi-cluster (fa.Q > 1) cooperative launch was refused
+bool launch_msd_cluster(int nslots, int cs, const SegSlot* slots, const uint64_t* src, uint64_t* dst,
+                        const FineArgs& fa, cudaStream_t s);
 void launch_sort_groups(uint32_t max_groups, const SortArgs& g, cudaStream_t s);
 void launch_pivots(int R, const uint64_t* row_out_off, const uint64_t* row_k, const uint32_t* vals,
                    uint32_t* pivots, cudaStream_t s);

@@ -6,10 +6,11 @@
 namespace rtk_b200 {
 
 // m = #{K >= T}: m < k or overflow -> exact path; m <= kSortCap -> one sort group;
-// larger -> an MSD slot whose first digit sits just below the common prefix of kmin..kmax.
+// larger -> an MSD slot whose first (fine, 11..16-bit) digit sits just below the common prefix
+// of kmin..kmax.
 __device__ __forceinline__ void plan_row(int j, uint32_t r, const PlanArgs& pa) {
     const uint64_t m = __ldcg(pa.count + r);
-    SegSlot sl{pa.cand_off[r], 0, 0, r, 0};
+    SegSlot sl{pa.cand_off[r], 0, 0, r, 0, 0, 0};
     if (m < pa.row_k[r] || m > pa.cap[r]) {
         pa.row_fail[r] = 1;
         atomicOr(pa.flags, kFlagFail);
@@ -19,8 +20,10 @@ __device__ __forceinline__ void plan_row(int j, uint32_t r, const PlanArgs& pa) 
     } else {
         const unsigned long long x = __ldcg(pa.kmin + r) ^ __ldcg(pa.kmax + r);
         const int hb = 63 - __clzll(x ? x : 1ull);
+        const int bits = static_cast<int>(fine_bits(m));  // level 0: fine MSD digit
         sl.len = m;
-        sl.pos = static_cast<uint32_t>(hb >= kDigit - 1 ? hb - (kDigit - 1) : 0);
+        sl.bits = static_cast<uint32_t>(bits);
+        sl.pos = static_cast<uint32_t>(hb >= bits - 1 ? hb - (bits - 1) : 0);
     }
     pa.slots[j] = sl;
 }

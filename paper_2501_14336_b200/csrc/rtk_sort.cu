@@ -16,6 +16,8 @@
 //
 // The host only reads two flags after the final synchronisation; deeper MSD levels and
 // the exact path run only when a flag asks for them.
+#include <cooperative_groups.h>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "rtk_device.cuh"
@@ -160,7 +162,7 @@ __device__ void seg_plan_block(int j, const SegSlot& sl, const SegPlanArgs& a) {
             const uint32_t q = atomicAdd(next.count, 1u);
             if (q < next.cap)
                 next.slots[q] = SegSlot{sl.off + start[i], c[i], sl.rank_base + start[i], sl.rid,
-                                        sl.pos >= kDigit ? sl.pos - kDigit : 0u};
+                                        sl.pos >= kDigit ? sl.pos - kDigit : 0u, kDigit, 0};
             atomicOr(flags, kFlagMore);
         } else if (gst[i]) {
             uint32_t end = INF;
@@ -236,6 +238,485 @@ __global__ void __launch_bounds__(kThreads) k_seg_hist(const SegSlot* slots, int
     if (cur >= 0) finish_slot(cur);
 }
 
+
+// ---- level-0 MSD (upsweep / downsweep) -------------------------------------------------------
+// One 2^bits-bin digit (11 or 13 bits) just below the common prefix of the row's candidates.
+// k_msd_up: CTA (j, c) histograms chunk c of slot j in shared memory and stores it as row c of
+// the slot's count matrix; the CTA that finishes the slot last turns the matrix columns into
+// per-chunk offsets and plans the buckets (three sweeps over the totals in shared memory, block
+// scans in between). k_msd_down: CTA (j, c) re-reads its chunk and scatters with shared-memory
+// cursors seeded from its matrix row. No global atomics on the data path.
+constexpr int kMsdThreads = 1024;
+constexpr int kMsdWarps = kMsdThreads / 32;
+
+// bucket classes: 0 empty, 1 tiny (packed, quantum 32), 2 mid (packed, quantum 128), 3 solo warp,
+// 4 small (packed, quantum kGroupPack, CTA), 5 solo CTA, 6 big (next level). Classes 1-3 form warp
+// groups (<= kWarpGroupMax), 4-5 CTA groups (<= kSortCap).
+__device__ __forceinline__ uint32_t fine_class(uint32_t c) {
+    return c == 0 ? 0u : c <= kTinyMax ? 1u : c <= kMidMax ? 2u : c <= kWarpGroupMax ? 3u
+         : c <= kGroupPack ? 4u : c <= kSortCap ? 5u : 6u;
+}
+
+// Boundary rule for a kept, non-empty bucket (start s, class cl) after the previous kept
+// bucket `prev` (0: none, else ((start + 1) << 3) | class). Packable buckets join the open group
+// while the class is unchanged and their starts share its quantum (group < 2 x quantum); solo
+// buckets are their own group; big ones are a boundary but no group.
+__device__ __forceinline__ void fine_rule(uint32_t s, uint32_t cl, unsigned long long prev, bool& bnd,
+                                          bool& gst) {
+    if (cl == 6) { bnd = true; gst = false; return; }
+    if (cl == 3 || cl == 5 || prev == 0) { bnd = gst = true; return; }
+    const uint32_t pcl = static_cast<uint32_t>(prev & 7), ps = static_cast<uint32_t>((prev >> 3) - 1);
+    const uint32_t q = cl == 1 ? kTinyMax : cl == 2 ? kMidMax : kGroupPack;
+    gst = pcl != cl || s / q != ps / q;
+    bnd = gst;
+}
+
+// Plan of one slot from its bucket totals cnt[0, B) (shared memory), kMsdThreads threads; cnt
+// is overwritten in place with the bucket starts (~0: dropped, rank >= k).
+// Thread t owns buckets [B - (t+1)*per, B - t*per) walked downward (thread 0: top digits).
+__device__ void msd_plan_block(const SegSlot& sl, uint32_t* cnt, uint32_t B, const FineArgs& a) {
+    constexpr uint32_t INF = 0xffffffffu;
+    __shared__ unsigned long long s_w64[kMsdWarps];
+    __shared__ uint32_t s_w32[kMsdWarps];
+    __shared__ unsigned long long s_cw[kMsdWarps];
+    __shared__ uint32_t s_suf[kMsdWarps], s_ke[kMsdWarps];
+    __shared__ unsigned long long s_base[3];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned full = 0xffffffffu;
+    const uint32_t per = B / kMsdThreads;  // 2, 8 or 16
+    uint32_t* bs = cnt;
+    const uint64_t kr = a.row_k[sl.rid];
+    const uint64_t krel = kr > sl.rank_base ? kr - sl.rank_base : 0;  // kept: start < krel
+    const uint32_t lo = B - (tid + 1) * per;
+
+    // sweep 1: bucket total + last non-empty bucket (local start, class)
+    uint32_t sum = 0, last_ls = 0, last_cl = 0;
+    for (uint32_t i = 0; i < per; ++i) {
+        const uint32_t c = cnt[lo + per - 1 - i];
+        if (c) { last_ls = sum; last_cl = fine_class(c); }
+        sum += c;
+    }
+    // scan 1: exclusive sum (bucket starts) and exclusive max of the last bucket (predecessor)
+    uint32_t inc = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(full, inc, d);
+        if (lane >= d) inc += o;
+    }
+    if (lane == 31) s_w32[warp] = inc;
+    __syncthreads();
+    uint32_t before = inc - sum;
+    for (int w = 0; w < warp; ++w) before += s_w32[w];
+    const unsigned long long L =
+        last_cl ? (static_cast<unsigned long long>(before + last_ls) + 1) << 3 | last_cl : 0ull;
+    unsigned long long prev;
+    {
+        unsigned long long v = L;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long o = __shfl_up_sync(full, v, d);
+            if (lane >= d) v = max(v, o);
+        }
+        const unsigned long long ex = __shfl_up_sync(full, v, 1);
+        if (lane == 31) s_w64[warp] = v;
+        __syncthreads();
+        unsigned long long wpre = 0;
+        for (int w = 0; w < warp; ++w) wpre = max(wpre, s_w64[w]);
+        prev = max(wpre, lane ? ex : 0ull);
+    }
+
+    // sweep 2: count groups / next-level slots, first boundary, kept end
+    uint32_t nw = 0, nc = 0, nb = 0, first_bnd = INF, kept_end = 0;
+    {
+        uint32_t s = before;
+        unsigned long long pv = prev;
+        for (uint32_t i = 0; i < per; ++i) {
+            const uint32_t c = cnt[lo + per - 1 - i];
+            if (c && s < krel) {
+                const uint32_t cl = fine_class(c);
+                bool bnd, gst;
+                fine_rule(s, cl, pv, bnd, gst);
+                if (bnd && first_bnd == INF) first_bnd = s;
+                if (cl == 6) ++nb;
+                else if (gst) { if (cl <= 3) ++nw; else ++nc; }
+                kept_end = s + c;
+                pv = (static_cast<unsigned long long>(s) + 1) << 3 | cl;
+            }
+            s += c;
+        }
+    }
+    // scan 2: packed (nw, nc, nb) exclusive sum; suffix min of first_bnd; max kept_end
+    const unsigned long long cnt3 = static_cast<unsigned long long>(nw) |
+                                    static_cast<unsigned long long>(nc) << 21 |
+                                    static_cast<unsigned long long>(nb) << 42;
+    unsigned long long cinc = cnt3;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = __shfl_up_sync(full, cinc, d);
+        if (lane >= d) cinc += o;
+    }
+    uint32_t suf = first_bnd, ke = kept_end;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_down_sync(full, suf, d);
+        if (lane + d < 32) suf = min(suf, o);
+    }
+    const uint32_t suf_after_lane = __shfl_down_sync(full, suf, 1);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) ke = max(ke, __shfl_xor_sync(full, ke, d));
+    if (lane == 31) s_cw[warp] = cinc;
+    if (lane == 0) { s_suf[warp] = suf; s_ke[warp] = ke; }
+    __syncthreads();
+    unsigned long long cpre = cinc - cnt3, ctot = 0;
+    uint32_t after = lane < 31 ? suf_after_lane : INF, kend = 0;
+    for (int w = 0; w < kMsdWarps; ++w) {
+        if (w < warp) cpre += s_cw[w];
+        ctot += s_cw[w];
+        if (w > warp) after = min(after, s_suf[w]);
+        kend = max(kend, s_ke[w]);
+    }
+    if (tid == 0) {
+        const uint32_t tw = static_cast<uint32_t>(ctot & 0x1FFFFF);
+        const uint32_t tc = static_cast<uint32_t>((ctot >> 21) & 0x1FFFFF);
+        const uint32_t tb = static_cast<uint32_t>(ctot >> 42);
+        s_base[0] = tw ? atomicAdd(a.wgroups.count, tw) : 0;
+        s_base[1] = tc ? atomicAdd(a.groups.count, tc) : 0;
+        s_base[2] = tb ? atomicAdd(a.next.count, tb) : 0;
+        if (tb) atomicOr(a.flags, kFlagMore);
+    }
+    __syncthreads();
+    uint32_t iw = static_cast<uint32_t>(s_base[0] + (cpre & 0x1FFFFF));
+    uint32_t ic = static_cast<uint32_t>(s_base[1] + ((cpre >> 21) & 0x1FFFFF));
+    uint32_t ib = static_cast<uint32_t>(s_base[2] + (cpre >> 42));
+
+    // sweep 3: emit groups / slots and the bucket starts for the scatter
+    bool open = false, overflow = false;
+    uint32_t os = 0, ocl = 0;
+    auto emit = [&](uint32_t end) {
+        const SortGroup gr{sl.off + os, end - os, sl.rid, 1u, 0u, sl.rank_base + os};
+        if (ocl <= 3) {
+            if (iw < a.wgroups.cap) a.wgroups.groups[iw] = gr; else overflow = true;
+            ++iw;
+        } else {
+            if (ic < a.groups.cap) a.groups.groups[ic] = gr; else overflow = true;
+            ++ic;
+        }
+    };
+    {
+        uint32_t s = before;
+        unsigned long long pv = prev;
+        for (uint32_t i = 0; i < per; ++i) {
+            const uint32_t b = lo + per - 1 - i;
+            const uint32_t c = cnt[b];
+            const bool kept = c && s < krel;
+            bs[b] = kept ? s : ~0u;
+            if (kept) {
+                const uint32_t cl = fine_class(c);
+                bool bnd, gst;
+                fine_rule(s, cl, pv, bnd, gst);
+                if (bnd) {
+                    if (open) emit(s);
+                    open = gst;
+                    os = s;
+                    ocl = cl;
+                    if (cl == 6) {
+                        if (ib < a.next.cap)
+                            a.next.slots[ib] = SegSlot{sl.off + s, c, sl.rank_base + s, sl.rid,
+                                                       sl.pos >= kDigit ? sl.pos - kDigit : 0u, kDigit, 0};
+                        else
+                            overflow = true;
+                        ++ib;
+                    }
+                }
+                pv = (static_cast<unsigned long long>(s) + 1) << 3 | cl;
+            }
+            s += c;
+        }
+    }
+    if (open) emit(min(after, kend));
+    if (overflow) atomicOr(a.flags, kFlagOverflow);
+}
+
+// chunk c of G over m elements: [c*ch, min(m, (c+1)*ch)), ch a multiple of 4
+__device__ __forceinline__ void msd_chunk(uint64_t m, uint32_t G, uint32_t c, uint64_t& e0, uint64_t& e1) {
+    const uint64_t ch = ((m + G - 1) / G + 3) & ~uint64_t(3);
+    e0 = min(m, c * ch);
+    e1 = min(m, e0 + ch);
+}
+
+__device__ __forceinline__ unsigned long long msd_timer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Visit the composites of [e0, e1) (32-byte aligned start): f(K, valid) for every lane slot,
+// 2 x 32-byte loads per thread in flight, block-uniform trip count (warp collectives allowed).
+template <typename F>
+__device__ __forceinline__ void msd_stream(const uint64_t* p, uint64_t e0, uint64_t e1, F f) {
+    constexpr uint64_t step = 2ull * kMsdThreads * kVec64;
+    for (uint64_t base = e0; base < e1; base += step) {
+        uint64_t v[2][kVec64];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const uint64_t e = base + (static_cast<uint64_t>(u) * kMsdThreads + threadIdx.x) * kVec64;
+            if (e + kVec64 <= e1) {
+                ldg256_u64(p + e, v[u]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < kVec64; ++i) v[u][i] = e + i < e1 ? __ldcg(p + e + i) : 0ull;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int i = 0; i < kVec64; ++i) {
+                const uint64_t e = base + (static_cast<uint64_t>(u) * kMsdThreads + threadIdx.x) * kVec64 + i;
+                f(v[u][i], e < e1);
+            }
+    }
+}
+
+__device__ __forceinline__ void grid_barrier(uint32_t* ctr, uint32_t target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        uint32_t v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v < target) __nanosleep(100);
+        } while (v < target);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Plan of this CTA's bucket slice [s0, s0 + slice) (totals tot[0, slice), shared memory), whose
+// first (highest) bucket starts at rank `off` of the slot. tot becomes the bucket starts (~0 for
+// empty or dropped buckets). Every kept bucket is one group: <= kWarpGroupMax -> warp group,
+// <= kSortCap -> CTA group, larger -> next-level slot. emit == false: starts only.
+__device__ void msd_plan_slice(const SegSlot& sl, uint32_t* tot, uint32_t slice, uint32_t off, bool emit,
+                               const FineArgs& a) {
+    __shared__ uint32_t s_w[kMsdWarps];
+    __shared__ unsigned long long s_c[kMsdWarps];
+    __shared__ uint32_t s_base[3];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned full = 0xffffffffu;
+    const uint32_t nt = slice < kMsdThreads ? slice : kMsdThreads;
+    const uint32_t per = slice / nt;
+    const bool act = static_cast<uint32_t>(tid) < nt;
+    const uint32_t lo = act ? slice - (tid + 1) * per : 0;  // descending: thread 0 owns the top buckets
+    const uint64_t kr = a.row_k[sl.rid];
+    const uint64_t krel = kr > sl.rank_base ? kr - sl.rank_base : 0;
+    uint32_t sum = 0;
+    if (act)
+        for (uint32_t i = 0; i < per; ++i) sum += tot[lo + i];
+    uint32_t inc = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(full, inc, d);
+        if (lane >= d) inc += o;
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    uint32_t before = off + inc - sum;
+    for (int w = 0; w < warp; ++w) before += s_w[w];
+    // classes of the kept buckets -> list positions
+    uint32_t nw = 0, nc = 0, nb = 0;
+    if (act) {
+        uint32_t st = before;
+        for (uint32_t i = per; i-- > 0;) {
+            const uint32_t c = tot[lo + i];
+            if (c && st < krel) {
+                if (c <= kWarpGroupMax) ++nw; else if (c <= kSortCap) ++nc; else ++nb;
+            }
+            st += c;
+        }
+    }
+    const unsigned long long c3 = static_cast<unsigned long long>(nw) | static_cast<unsigned long long>(nc) << 21 |
+                                  static_cast<unsigned long long>(nb) << 42;
+    unsigned long long ci = c3;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = __shfl_up_sync(full, ci, d);
+        if (lane >= d) ci += o;
+    }
+    if (lane == 31) s_c[warp] = ci;
+    __syncthreads();
+    unsigned long long cpre = ci - c3, ctot = 0;
+    for (int w = 0; w < kMsdWarps; ++w) {
+        if (w < warp) cpre += s_c[w];
+        ctot += s_c[w];
+    }
+    if (tid == 0 && emit) {
+        const uint32_t tw = static_cast<uint32_t>(ctot & 0x1FFFFF), tc = static_cast<uint32_t>((ctot >> 21) & 0x1FFFFF),
+                       tb = static_cast<uint32_t>(ctot >> 42);
+        s_base[0] = tw ? atomicAdd(a.wgroups.count, tw) : 0;
+        s_base[1] = tc ? atomicAdd(a.groups.count, tc) : 0;
+        s_base[2] = tb ? atomicAdd(a.next.count, tb) : 0;
+        if (tb) atomicOr(a.flags, kFlagMore);
+    }
+    __syncthreads();
+    uint32_t iw = s_base[0] + static_cast<uint32_t>(cpre & 0x1FFFFF);
+    uint32_t ic = s_base[1] + static_cast<uint32_t>((cpre >> 21) & 0x1FFFFF);
+    uint32_t ib = s_base[2] + static_cast<uint32_t>(cpre >> 42);
+    bool overflow = false;
+    if (act) {
+        uint32_t st = before;
+        for (uint32_t i = per; i-- > 0;) {
+            const uint32_t c = tot[lo + i];
+            const bool kept = c && st < krel;
+            tot[lo + i] = kept ? st : ~0u;
+            if (kept && emit) {
+                const SortGroup gr{sl.off + st, c, sl.rid, 1u, 0u, sl.rank_base + st};
+                if (c <= kWarpGroupMax) {
+                    if (iw < a.wgroups.cap) a.wgroups.groups[iw] = gr; else overflow = true;
+                    ++iw;
+                } else if (c <= kSortCap) {
+                    if (ic < a.groups.cap) a.groups.groups[ic] = gr; else overflow = true;
+                    ++ic;
+                } else {
+                    if (ib < a.next.cap)
+                        a.next.slots[ib] = SegSlot{sl.off + st, c, sl.rank_base + st, sl.rid,
+                                                   sl.pos >= kDigit ? sl.pos - kDigit : 0u, kDigit, 0};
+                    else
+                        overflow = true;
+                    ++ib;
+                }
+            }
+            st += c;
+        }
+    }
+    if (overflow) atomicOr(a.flags, kFlagOverflow);
+    __syncthreads();
+}
+
+// Level-0 MSD of the slots, one cluster (or, fa.Q > 1, Q co-resident clusters) per slot:
+//  1 chunk histograms (shared memory)           2 intra-cluster column scan over DSMEM
+//  3 [Q > 1: cluster totals -> global, grid barrier, cross-cluster column scan]
+//  4 each CTA plans its bucket slice (slice offsets exchanged over DSMEM; only cluster 0 emits)
+//  5 cursors = bucket start + cross-cluster + intra-cluster offset; scatter of the chunk
+__global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* slots, const uint64_t* src,
+                                                                uint64_t* dst, FineArgs fa) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    // [0,B): counts -> intra-cluster offsets -> cursors; [B, B+slice): slice totals -> starts;
+    // [B+slice, B+2 slice): cross-cluster offsets (Q > 1)
+    extern __shared__ uint32_t sm[];
+    __shared__ uint32_t s_ssum[16];
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const uint32_t CS = cluster.num_blocks();
+    const uint32_t r = cluster.block_rank();
+    const uint32_t cid = blockIdx.x / CS;
+    const uint32_t Q = fa.Q;
+    const uint32_t j = Q > 1 ? 0 : cid, q = Q > 1 ? cid : 0;
+    const SegSlot sl = slots[j];
+    if (sl.len == 0) return;  // uniform over the cluster (and over the grid when Q > 1)
+    const uint32_t B = 1u << sl.bits, dmask = B - 1;
+    const uint32_t slice = B / CS, s0 = r * slice;
+    uint32_t* h = sm;
+    uint32_t* tot = sm + B;
+    uint32_t* qoff = sm + B + slice;
+    const bool dbg = fa.dbg && blockIdx.x == 0 && threadIdx.x == 0;
+    if (dbg) fa.dbg[0] = msd_timer();
+    for (uint32_t b = threadIdx.x; b < B; b += kMsdThreads) h[b] = 0;
+    __syncthreads();
+    uint64_t e0, e1;
+    msd_chunk(sl.len, Q * CS, q * CS + r, e0, e1);
+    const uint64_t* p = src + sl.off;
+    msd_stream(p, e0, e1, [&](unsigned long long K, bool valid) {
+        const uint32_t d = static_cast<uint32_t>(K >> sl.pos) & dmask;
+        const uint32_t d0 = __shfl_sync(full, d, 0);
+        if (__all_sync(full, valid && d == d0)) {
+            if (lane == 0) atomicAdd(h + d0, 32u);  // tie-heavy rows: one atomic per warp
+        } else if (valid) {
+            atomicAdd(h + d, 1u);
+        }
+    });
+    cluster.sync();
+    if (dbg) fa.dbg[1] = msd_timer();
+    // 2: intra-cluster column scan of this CTA's slice through DSMEM
+    for (uint32_t i = threadIdx.x; i < slice; i += kMsdThreads) {
+        const uint32_t b = s0 + i;
+        uint32_t v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = c < static_cast<int>(CS) ? *cluster.map_shared_rank(h + b, c) : 0u;
+        uint32_t run = 0;
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+            if (c < static_cast<int>(CS)) {
+                *cluster.map_shared_rank(h + b, c) = run;
+                run += v[c];
+            }
+        tot[i] = run;
+        if (Q > 1) fa.ctot[static_cast<uint64_t>(q) * B + b] = run;
+    }
+    if (Q > 1) {
+        // 3: cross-cluster column scan (redundant per cluster: no second barrier)
+        grid_barrier(fa.bar, fa.bar_target);
+        if (dbg) fa.dbg[2] = msd_timer();
+        for (uint32_t i = threadIdx.x; i < slice; i += kMsdThreads) {
+            uint32_t pre = 0, all = 0;
+            for (uint32_t q2 = 0; q2 < Q; ++q2) {
+                const uint32_t v = __ldcg(fa.ctot + static_cast<uint64_t>(q2) * B + s0 + i);
+                if (q2 < q) pre += v;
+                all += v;
+            }
+            qoff[i] = pre;
+            tot[i] = all;
+        }
+    }
+    __syncthreads();
+    // 4: slice sums -> slice offsets (descending digits: higher slices first), plan the slice
+    {
+        uint32_t part = 0;
+        for (uint32_t i = threadIdx.x; i < slice; i += kMsdThreads) part += tot[i];
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(full, part, d);
+        __shared__ uint32_t s_part[kMsdWarps];
+        if (lane == 0) s_part[threadIdx.x >> 5] = part;
+        __syncthreads();
+        if (threadIdx.x < CS) {
+            uint32_t ssum = 0;
+            for (int w = 0; w < kMsdWarps; ++w) ssum += s_part[w];
+            *cluster.map_shared_rank(s_ssum + r, threadIdx.x) = ssum;  // publish to every CTA
+        }
+    }
+    cluster.sync();
+    if (dbg) fa.dbg[3] = msd_timer();
+    uint32_t off = 0;
+    for (uint32_t r2 = r + 1; r2 < CS; ++r2) off += s_ssum[r2];
+    msd_plan_slice(sl, tot, slice, off, q == 0, fa);
+    cluster.sync();
+    if (dbg) fa.dbg[4] = msd_timer();
+    // 5: cursors from the owners' bucket starts (+ cross-cluster offsets), then the scatter
+    for (uint32_t b = threadIdx.x; b < B; b += kMsdThreads) {
+        const uint32_t ow = b / slice, i = b - ow * slice;
+        const uint32_t st = *cluster.map_shared_rank(tot + i, ow);
+        const uint32_t qo = Q > 1 ? *cluster.map_shared_rank(qoff + i, ow) : 0u;
+        h[b] = st == ~0u ? ~0u : st + qo + h[b];
+    }
+    cluster.sync();  // owners' shared memory is read by everyone before anyone exits
+    uint64_t* qd = dst + sl.off;
+    msd_stream(p, e0, e1, [&](unsigned long long K, bool valid) {
+        const uint32_t d = static_cast<uint32_t>(K >> sl.pos) & dmask;
+        const uint32_t d0 = __shfl_sync(full, d, 0);
+        if (__all_sync(full, valid && d == d0)) {  // tie-heavy: one shared atomic per warp
+            if (h[d0] != ~0u) {                     // warp-uniform (dropped buckets stay ~0)
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(h + d0, 32u);
+                base = __shfl_sync(full, base, 0);
+                qd[base + lane] = K;
+            }
+        } else if (valid) {
+            if (h[d] != ~0u) qd[atomicAdd(h + d, 1u)] = K;
+        }
+    });
+    if (dbg) { fa.dbg[5] = msd_timer(); fa.dbg[31] = 6; }
+}
+
 // ---- k_seg_scatter ------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_seg_scatter(const SegSlot* slots, int nslots,
                                                           const uint64_t* tile_start,
@@ -296,6 +777,69 @@ __global__ void __launch_bounds__(kThreads) k_seg_scatter(const SegSlot* slots, 
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = kSortCap / kSortThreads;  // 8
 static_assert(kSortItems == 8, "sort layout");
+
+// Bitonic sort (descending) of one group of <= 32*IPL composites by one warp: element
+// p = lane * IPL + e; strides < IPL compare inside the lane, larger ones across lanes (shuffles).
+// Ranks < k are written as (value bits, u64 index); rank k-1 also as the pivot.
+template <int IPL>
+__device__ __forceinline__ void warp_sort_group(const SortGroup& grp, const SortArgs& g, int lane) {
+    constexpr uint32_t N = 32 * IPL;
+    const unsigned full = 0xffffffffu;
+    const unsigned long long* src = (grp.buf ? g.buf1 : g.buf0) + grp.off;
+    unsigned long long a[IPL];
+#pragma unroll
+    for (int e = 0; e < IPL; ++e) {
+        const uint32_t p = lane * IPL + e;
+        a[e] = p < grp.len ? __ldcg(src + p) : 0ull;
+    }
+#pragma unroll
+    for (uint32_t kk = 2; kk <= N; kk <<= 1) {
+#pragma unroll
+        for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+            if (jj < IPL) {
+#pragma unroll
+                for (int e = 0; e < IPL; ++e) {
+                    if (e & jj) continue;
+                    const uint32_t p = lane * IPL + e;
+                    const bool desc = (p & kk) == 0;
+                    const unsigned long long x = a[e], y = a[e + jj];
+                    const unsigned long long hi = max(x, y), lo = min(x, y);
+                    a[e] = desc ? hi : lo;
+                    a[e + jj] = desc ? lo : hi;
+                }
+            } else {
+                const int lm = static_cast<int>(jj / IPL);
+                const bool lower = (lane & lm) == 0;
+#pragma unroll
+                for (int e = 0; e < IPL; ++e) {
+                    const uint32_t p = lane * IPL + e;
+                    const bool desc = (p & kk) == 0;
+                    const unsigned long long o = __shfl_xor_sync(full, a[e], lm);
+                    a[e] = (lower == desc) ? max(a[e], o) : min(a[e], o);
+                }
+            }
+        }
+    }
+    const uint32_t r = grp.rid;
+    const uint64_t kr = g.row_k[r];
+    const uint64_t oo = g.row_out_off[r];
+#pragma unroll
+    for (int e = 0; e < IPL; ++e) {
+        const uint32_t p = lane * IPL + e;
+        const uint64_t rank = grp.rank_base + p;
+        if (p >= grp.len || rank >= kr) continue;
+        const unsigned long long K = a[e];
+        const uint32_t kk = static_cast<uint32_t>(K >> 32);
+        const uint32_t idx = ~static_cast<uint32_t>(K);
+        uint32_t val;
+        if (g.gather) val = __ldg(g.in_base + g.row_in_off[r] + idx);
+        else if (g.dtype == kF32) val = decode_f32_bits(kk, g.smallest);
+        else val = g.smallest ? ~kk : kk;
+        g.out_vals[oo + rank] = val;
+        g.out_idx[oo + rank] = idx;
+        if (rank == kr - 1 && g.pivots) g.pivots[r] = val;
+    }
+}
 
 __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
     extern __shared__ unsigned long long buf[];  // kSortCap entries (dynamic: > 48 KB static)
@@ -400,6 +944,18 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
         }
         __syncthreads();
     }
+    // warp groups (<= kWarpGroupMax composites): one warp each, bitonic in registers, no shared
+    // memory, no block barriers; 2, 4 or 8 items per lane by group size
+    // static striding over the list (groups are similar-sized; a shared work counter would
+    // serialise thousands of same-address atomics); *wwork = first group of this launch
+    const uint32_t wend = min(*g.wgroups.count, g.wgroups.cap);
+    const uint32_t nwarps = gridDim.x * (kSortThreads / 32);
+    for (uint32_t gi = *g.wwork + blockIdx.x * (kSortThreads / 32) + warp; gi < wend; gi += nwarps) {
+        const SortGroup grp = g.wgroups.groups[gi];
+        if (grp.len <= 64) warp_sort_group<2>(grp, g, lane);
+        else if (grp.len <= 128) warp_sort_group<4>(grp, g, lane);
+        else warp_sort_group<8>(grp, g, lane);
+    }
 }
 
 // ---- launchers ----------------------------------------------------------------------------
@@ -414,6 +970,79 @@ void launch_seg_scatter(uint64_t tiles, const SegSlot* slots, int nslots, const 
                         cudaStream_t s) {
     const int grid = persistent_grid(k_seg_scatter, kThreads, 0, tiles);
     k_seg_scatter<<<grid, kThreads, 0, s>>>(slots, nslots, tile_start, src, dst, bstart, gcursor);
+}
+
+static size_t msd_smem(int cs) {
+    // counts (2^14) + slice totals + cross-cluster offsets (2 x 2^14 / cs)
+    return ((size_t(1) << kMsdMaxBits) + 2 * ((size_t(1) << kMsdMaxBits) / cs)) * sizeof(uint32_t);
+}
+
+static void msd_configure() {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_msd_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(k_msd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        configured = true;
+    }
+}
+
+int msd_max_clusters(int cs) {
+    static int cache[17] = {0};
+    if (cs < 1 || cs > 16) return 1;
+    if (!cache[cs]) {
+        msd_configure();
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(kMsdThreads);
+        cfg.dynamicSmemBytes = msd_smem(cs);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_msd_cluster, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            n = 1;
+        }
+        cache[cs] = n > 0 ? n : 1;
+    }
+    return cache[cs];
+}
+
+bool launch_msd_cluster(int nslots, int cs, const SegSlot* slots, const uint64_t* src, uint64_t* dst,
+                        const FineArgs& fa, cudaStream_t s) {
+    if (nslots <= 0) return true;
+    const size_t smem = msd_smem(cs);
+    msd_configure();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((fa.Q > 1 ? fa.Q : nslots) * cs);
+    cfg.blockDim = dim3(kMsdThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = fa.Q > 1 ? 2 : 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_msd_cluster, slots, src, dst, fa);
+    if (e != cudaSuccess && fa.Q > 1) {
+        cudaGetLastError();  // refused (co-residency): caller relaunches with Q = 1
+        if (fa.dbg) {
+            int ncl = 0;
+            cfg.numAttrs = 1;
+            cudaOccupancyMaxActiveClusters(&ncl, k_msd_cluster, &cfg);
+            fprintf(stderr, "[rtk] multi-cluster MSD refused: %s (max active clusters %d)\n", cudaGetErrorString(e), ncl);
+        }
+        return false;
+    }
+    return true;
 }
 
 void launch_sort_groups(uint32_t max_groups, const SortArgs& g, cudaStream_t s) {
