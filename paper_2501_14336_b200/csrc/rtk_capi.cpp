@@ -207,7 +207,7 @@ int rtk_handle_destroy(rtk_handle h) {
 int rtk_get_stats(rtk_handle h, rtk_stats* out) {
     return guarded([&] {
         if (!h || !out) throw Error{RTK_INVALID_ARGUMENT, "null argument"};
-        *out = h->engine.stats;
+        *out = h->engine.last_stats();
     });
 }
 

@@ -14,6 +14,7 @@
 #include "rtk_engine.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <chrono>
 #include <cstdio>
@@ -26,6 +27,9 @@ namespace rtk_b200 {
 
 namespace {
 
+// bumped whenever a device / pinned buffer is (re)allocated or freed: captured graphs embed
+// raw pointers and are only replayed while the generation is unchanged
+std::atomic<uint64_t> g_buf_gen{1};
 
 void check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)
@@ -48,6 +52,7 @@ void DevBuf::ensure(size_t bytes, bool keep, cudaStream_t s) {
     ncap = (ncap + 255) & ~size_t(255);
     void* np = nullptr;
     check(cudaMalloc(&np, ncap), "cudaMalloc");
+    g_buf_gen.fetch_add(1);
     if (keep && p && cap) {
         check(cudaMemcpyAsync(np, p, cap, cudaMemcpyDeviceToDevice, s), "grow copy");
         check(cudaStreamSynchronize(s), "grow sync");
@@ -58,6 +63,7 @@ void DevBuf::ensure(size_t bytes, bool keep, cudaStream_t s) {
 }
 
 void DevBuf::release() {
+    if (p) g_buf_gen.fetch_add(1);
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
@@ -68,18 +74,22 @@ Engine::Engine(int device) : device_(device) {
     profile_ = p && *p && *p != '0';
     if (const char* sr = std::getenv("RTK_SAMPLE_R")) sample_r_ = std::max(1.0, std::atof(sr));
     if (const char* mq = std::getenv("RTK_MSD_Q")) msd_q_max_ = std::max(1, std::atoi(mq));
+    if (const char* g = std::getenv("RTK_GRAPHS")) graphs_ = *g && *g != '0';
     const char* cs = std::getenv("RTK_COUNT_STATS");
     count_stats_ = profile_ || (cs && *cs && *cs != '0');
 }
 
 Engine::~Engine() {
+    if (graph_.exec) cudaGraphExecDestroy(graph_.exec);
+    if (cap_s_) cudaStreamDestroy(cap_s_);
+    if (hmap_) cudaFreeHost(hmap_);
     if (pin_) cudaFreeHost(pin_);
     if (hctl_) cudaFreeHost(hctl_);
     if (hcount_) cudaFreeHost(hcount_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     for (DevBuf* b : {&arena_, &sel_, &T_, &count_, &kmin_, &kmax_, &ghist_, &samples_, &cand_a_,
-                      &cand_b_, &seg_hist_, &gcursor_, &bstart_, &dcap_, &dcoff_, &ctl_, &row_fail_, &groups_, &slots0_, &slotsA_, &slotsB_, &done_, &seg_ticket_, &wgroups_, &ctot_, &io_in, &io_vals, &io_idx,
+                      &cand_b_, &seg_hist_, &gcursor_, &bstart_, &dcap_, &dcoff_, &ctl_, &row_fail_, &groups_, &slots0_, &slotsA_, &slotsB_, &done_, &seg_ticket_, &wgroups_, &ctot_, &sig_, &io_in, &io_vals, &io_idx,
                       &io_piv, &io_aux})
         b->release();
 }
@@ -93,6 +103,7 @@ uint8_t* Engine::upload(const Plan& p, cudaStream_t s) {
         arena_ = DevBuf{};
         arena_.ensure(std::max<size_t>(need * 2, size_t(4) << 20));
         arena_used_ = 0;
+        g_buf_gen.fetch_add(1);
     }
     uint8_t* d = arena_.as<uint8_t>() + arena_used_;
     arena_used_ += need;
@@ -103,6 +114,7 @@ uint8_t* Engine::upload(const Plan& p, cudaStream_t s) {
             pin_cap_ = std::max<size_t>(need * 2, size_t(4) << 20);
             check(cudaHostAlloc(reinterpret_cast<void**>(&pin_), pin_cap_, cudaHostAllocDefault), "cudaHostAlloc");
             pin_used_ = 0;
+            g_buf_gen.fetch_add(1);
         }
         uint8_t* h = pin_ + pin_used_;
         pin_used_ += need;
@@ -162,23 +174,138 @@ uint32_t Engine::read_word(const uint32_t* d, uint64_t i, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------------------
+bool Engine::CallKey::operator==(const CallKey& o) const {
+    if (base != o.base || dtype != o.dtype || smallest != o.smallest || scaled != o.scaled || gather != o.gather ||
+        a_s_bits != o.a_s_bits || vals != o.vals || idx != o.idx || piv != o.piv || s != o.s ||
+        rows.size() != o.rows.size())
+        return false;
+    for (size_t i = 0; i < rows.size(); ++i)
+        if (rows[i].in_off != o.rows[i].in_off || rows[i].n != o.rows[i].n || rows[i].k != o.rows[i].k ||
+            rows[i].out_off != o.rows[i].out_off)
+            return false;
+    return true;
+}
+
+const rtk_stats& Engine::last_stats() {
+    if (stats_pending_) {
+        cudaEventSynchronize(ev_[3]);
+        cudaEventElapsedTime(&stats.total_ms, ev_[0], ev_[3]);
+        stats_pending_ = false;
+    }
+    return stats;
+}
+
 void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, float a_s,
                  bool gather, const std::vector<RowReq>& rows, uint32_t* d_vals, uint64_t* d_idx,
                  uint32_t* d_pivots, cudaStream_t s) {
     check(cudaSetDevice(device_), "cudaSetDevice");
+    if (rows.empty()) return;
+    if (!ev_[0]) {
+        for (auto& e : ev_) check(cudaEventCreate(&e), "cudaEventCreate");
+    }
+    if (!hmap_) {
+        check(cudaHostAlloc(reinterpret_cast<void**>(&hmap_), 64, cudaHostAllocMapped), "cudaHostAlloc");
+        std::memset(hmap_, 0, 64);
+        check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_hmap_), hmap_, 0), "mapped pointer");
+        sig_.ensure(64);
+        check(cudaMemsetAsync(sig_.p, 0, 64, s), "memset");
+        check(cudaStreamSynchronize(s), "sync");
+        expected_seq_ = 0;
+    }
+    CallKey key;
+    key.base = d_base;
+    key.dtype = dtype;
+    key.smallest = smallest;
+    key.scaled = scaled ? 1 : 0;
+    key.gather = gather ? 1 : 0;
+    std::memcpy(&key.a_s_bits, &a_s, 4);
+    key.vals = d_vals;
+    key.idx = d_idx;
+    key.piv = d_pivots;
+    key.s = s;
+    key.rows = rows;
+    const bool usable = graphs_ && !profile_ && !count_stats_;
+    const uint64_t gen0 = g_buf_gen.load();
+    if (usable && graph_.valid && graph_.gen == gen0 && graph_.key == key) {
+        // replay: restore the plan bytes the captured upload reads, launch, finish on the host
+        if (!graph_.pinned.empty()) std::memcpy(pin_, graph_.pinned.data(), graph_.pinned.size());
+        stats = graph_.stats;
+        check(cudaGraphLaunch(graph_.exec, s), "graph launch");
+        expected_seq_ += graph_.seq_incr;
+        sig_pending_ = graph_.seq_incr > 0;
+        Call c = graph_.call;
+        complete(d_base, rows, c, s);
+        return;
+    }
+    const bool capture = usable && have_last_ && last_gen_ == gen0 && last_key_ == key;
+    Call c{};
+    // capture on a private stream (the caller's may be the legacy default stream, which cannot
+    // be captured); the graph is then launched into the caller's stream
+    if (capture && !cap_s_) {
+        if (cudaStreamCreateWithFlags(&cap_s_, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            cap_s_ = nullptr;
+        }
+    }
+    if (capture && cap_s_ && cudaStreamBeginCapture(cap_s_, cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+        const uint32_t seq0 = expected_seq_;
+        cudaGraph_t graph = nullptr;
+        bool ok = true;
+        capturing_ = true;
+        try {
+            enqueue(d_base, dtype, smallest, scaled, a_s, gather, rows, d_vals, d_idx, d_pivots, cap_s_, c);
+        } catch (const Error&) {
+            ok = false;
+        }
+        capturing_ = false;
+        c.s = s;
+        ok = cudaStreamEndCapture(cap_s_, &graph) == cudaSuccess && ok;
+        cudaGraphExec_t exec = nullptr;
+        ok = ok && g_buf_gen.load() == gen0 && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        if (!ok) {
+            if (exec) cudaGraphExecDestroy(exec);
+            graphs_ = false;  // capture not possible here: plain launches from now on
+            expected_seq_ = seq0;
+            run(d_base, dtype, smallest, scaled, a_s, gather, rows, d_vals, d_idx, d_pivots, s);
+            return;
+        }
+        if (graph_.exec) cudaGraphExecDestroy(graph_.exec);
+        graph_.exec = exec;
+        graph_.key = key;
+        graph_.gen = gen0;
+        graph_.pinned.assign(pin_, pin_ + pin_used_);
+        graph_.call = c;
+        graph_.stats = stats;
+        graph_.seq_incr = expected_seq_ - seq0;
+        graph_.valid = true;
+        check(cudaGraphLaunch(exec, s), "graph launch");
+    } else {
+        cudaGetLastError();
+        enqueue(d_base, dtype, smallest, scaled, a_s, gather, rows, d_vals, d_idx, d_pivots, s, c);
+    }
+    last_key_ = std::move(key);
+    last_gen_ = g_buf_gen.load();
+    have_last_ = true;
+    complete(d_base, rows, c, s);
+}
+
+// Everything up to the last kernel of the common path, stream-ordered, no host synchronisation
+// (capturable into a CUDA graph).
+void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scaled, float a_s, bool gather,
+                     const std::vector<RowReq>& rows, uint32_t* d_vals, uint64_t* d_idx, uint32_t* d_pivots,
+                     cudaStream_t s, Call& c_out) {
     arena_used_ = 0;
     pin_used_ = 0;
     stats = rtk_stats{};
     const int R = static_cast<int>(rows.size());
-    if (R == 0) return;
-    if (!ev_[0]) {
-        for (auto& e : ev_) check(cudaEventCreate(&e), "cudaEventCreate");
-    }
-    check(cudaEventRecord(ev_[0], s), "event");
+    record(0, s);
     mark("start", s);
     group_base_ = 0;
     wgroup_base_ = 0;
     bar_gen_ = 0;
+    sig_pending_ = false;
     InputSrc src{d_base, dtype, smallest, scaled ? 1 : 0, a_s};
     const uint64_t base_words = reinterpret_cast<uintptr_t>(d_base) / 4;
 
@@ -359,7 +486,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         ++stats.kernel_launches;
         mark("rows_fused", s);
     }
-    check(cudaEventRecord(ev_[1], s), "event");
+    record(1, s);
     if (!grow.empty()) {
         FinishPrep fp = prepare_finish(c, grow);
         Rows all{static_cast<int>(grow.size()), at<uint32_t>(D, o_grow), at<uint64_t>(D, o_goff),
@@ -368,13 +495,19 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
                        count_.as<unsigned long long>(), kmin_.as<unsigned long long>(),
                        kmax_.as<unsigned long long>(), plan_args(c, fp), s);
         stats.kernel_launches += 1;
-        check(cudaEventRecord(ev_[2], s), "event");
+        record(2, s);
         mark("compact", s);
         launch_finish(c, fp);
     } else {
-        check(cudaEventRecord(ev_[2], s), "event");
+        record(2, s);
     }
-    check(cudaEventRecord(ev_[3], s), "event");
+    record(3, s);
+    c_out = std::move(c);
+}
+
+// Wait for the common path, then the rare host-driven paths (deeper MSD levels, exact path).
+void Engine::complete(const uint32_t* d_base, const std::vector<RowReq>& rows, Call& c, cudaStream_t s) {
+    const int R = static_cast<int>(rows.size());
     uint32_t ctl[8];
     drain(c, ctl);
 
@@ -386,10 +519,10 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         for (int r = 0; r < R; ++r)
             if (fail[r]) fb.push_back(r);
         stats.fallback_rows = fb.size();
-        fallback(d_base, src, rows, fb, c, s);
+        fallback(d_base, c.src, rows, fb, c, s);
         drain(c, ctl);
         if (ctl[0] & kFlagFail) throw Error{RTK_INVARIANT_VIOLATION, "filter: pivot inconsistent after exact path"};
-        check(cudaEventRecord(ev_[3], s), "event");
+        record(3, s);
         sync(s, "finish");
     }
     if (count_stats_)
@@ -398,7 +531,8 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
     report_marks();
     release_retired();
     cudaEventElapsedTime(&stats.compact_ms, ev_[1], ev_[2]);
-    cudaEventElapsedTime(&stats.total_ms, ev_[0], ev_[3]);
+    stats_pending_ = true;
+    if (profile_) last_stats();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -495,13 +629,46 @@ void Engine::launch_finish(Call& c, const FinishPrep& f) {
         stats.kernel_launches += 1;
         mark("msd", c.s);
     }
-    launch_sort_groups(static_cast<uint32_t>(f.max_groups + f.max_wgroups / 8 + 1), sort_args(c, f.gl), c.s);
+    launch_sort(static_cast<uint32_t>(f.max_groups + f.max_wgroups / 8 + 1), sort_args(c, f.gl), c.s);
     mark("sort+pivots", c.s);
-    stats.kernel_launches += 1;
+}
+
+// stats events: inside a capture they must be external record nodes to be replayed
+void Engine::record(int i, cudaStream_t s) {
+    check(capturing_ ? cudaEventRecordWithFlags(ev_[i], s, cudaEventRecordExternal) : cudaEventRecord(ev_[i], s),
+          "event");
+}
+
+void Engine::launch_sort(uint32_t max_groups, const SortArgs& a, cudaStream_t s) {
+    launch_sort_groups(max_groups, a, s);
+    ++stats.kernel_launches;
+    ++expected_seq_;
+    sig_pending_ = true;
+}
+
+// Spin on the mapped signal word (the last sort CTA's sequence number). The stream is polled
+// now and then so a failed kernel surfaces as an error instead of a hang.
+void Engine::wait_signal(cudaStream_t s) {
+    const volatile uint32_t* f = hmap_;
+    for (uint64_t spin = 0;; ++spin) {
+        if (f[15] == expected_seq_) return;
+        if ((spin & 1023) == 1023) {
+            const cudaError_t e = cudaStreamQuery(s);
+            if (e == cudaSuccess) {
+                if (f[15] == expected_seq_) return;
+                throw Error{RTK_INTERNAL, "completion signal missing"};
+            }
+            if (e != cudaErrorNotReady) check(e, "kernel");
+        }
+    }
 }
 
 SortArgs Engine::sort_args(const Call& c, const GroupList& gl) {
     SortArgs a{};
+    a.ctl = ctl_.as<uint32_t>();
+    a.done_ctr = sig_.as<uint32_t>();
+    a.seq_ctr = sig_.as<uint32_t>() + 1;
+    a.hflags = d_hmap_;
     a.groups = gl;
     a.work = ctl_.as<uint32_t>() + 2;
     a.wgroups = GroupList{wgroups_.as<SortGroup>(), ctl_.as<uint32_t>() + 5, wgroup_cap_};
@@ -530,10 +697,18 @@ void Engine::drain(Call& c, uint32_t (&ctl)[8]) {
         hcount_cap_ = std::max<size_t>(c.R, 1024);
         check(cudaHostAlloc(reinterpret_cast<void**>(&hcount_), 8 * hcount_cap_, cudaHostAllocDefault), "cudaHostAlloc");
     }
-    check(cudaMemcpyAsync(hctl_, ctl_.p, 32, cudaMemcpyDeviceToHost, c.s), "d2h");
-    if (count_stats_) check(cudaMemcpyAsync(hcount_, count_.p, 8 * c.R, cudaMemcpyDeviceToHost, c.s), "d2h");
-    sync(c.s, "finish");
-    std::memcpy(ctl, hctl_, 32);
+    if (sig_pending_ && !count_stats_) {
+        wait_signal(c.s);  // the last sort CTA published ctl[0..7]: no copy, no stream sync
+        for (int i = 0; i < 8; ++i) ctl[i] = reinterpret_cast<volatile uint32_t*>(hmap_)[i];
+    } else {
+        check(cudaMemcpyAsync(hctl_, ctl_.p, 32, cudaMemcpyDeviceToHost, c.s), "d2h");
+        if (count_stats_) check(cudaMemcpyAsync(hcount_, count_.p, 8 * c.R, cudaMemcpyDeviceToHost, c.s), "d2h");
+        sync(c.s, "finish");
+        std::memcpy(ctl, hctl_, 32);
+    }
+    sig_pending_ = false;
+    if (profile_)
+        std::fprintf(stderr, "[rtk ctl] flags=%u cta_groups=%u next_slots=%u warp_groups=%u\n", ctl[0], ctl[1], ctl[3], ctl[5]);
     if (ctl[0] & kFlagOverflow) throw Error{RTK_INTERNAL, "device work list overflow"};
     const uint32_t sticky = ctl[0] & kFlagFail;  // rows for the exact path (kept across levels)
     int src_buf = 1;  // level-0 buckets live in buffer B
@@ -574,8 +749,8 @@ void Engine::drain(Call& c, uint32_t (&ctl)[8]) {
         launch_seg_hist(tiles.back(), cur.as<SegSlot>(), nslots, at<uint64_t>(D, o_tiles), bsrc, pa, c.s);
         launch_seg_scatter(tiles.back(), cur.as<SegSlot>(), nslots, at<uint64_t>(D, o_tiles), bsrc, bdst,
                            bstart_.as<uint32_t>(), gcursor_.as<uint32_t>(), c.s);
-        launch_sort_groups(static_cast<uint32_t>(max_groups), sort_args(c, gl), c.s);
-        stats.kernel_launches += 3;
+        launch_sort(static_cast<uint32_t>(max_groups), sort_args(c, gl), c.s);
+        stats.kernel_launches += 2;
         group_base_ += max_groups;
         check(cudaMemcpyAsync(hctl_, ctl_.p, 32, cudaMemcpyDeviceToHost, c.s), "d2h");
         sync(c.s, "msd level");

@@ -63,6 +63,9 @@ public:
 
     uint32_t read_word(const uint32_t* d, uint64_t i, cudaStream_t s);
 
+    // stats of the last call; total_ms is resolved lazily (waits for the call's last event)
+    const rtk_stats& last_stats();
+
     int device() const { return device_; }
     rtk_stats stats{};
     DevBuf io_in, io_vals, io_idx, io_piv, io_aux;
@@ -130,6 +133,46 @@ private:
                   const std::vector<uint32_t>& fb, Call& c, cudaStream_t s);
     void drain(Call& c, uint32_t (&ctl)[8]);
     SortArgs sort_args(const Call& c, const GroupList& gl);
+    void launch_sort(uint32_t max_groups, const SortArgs& a, cudaStream_t s);
+    void wait_signal(cudaStream_t s);
+    void record(int i, cudaStream_t s);
+    void enqueue(const uint32_t* d_base, int dtype, int smallest, bool scaled, float a_s, bool gather,
+                 const std::vector<RowReq>& rows, uint32_t* d_vals, uint64_t* d_idx, uint32_t* d_pivots,
+                 cudaStream_t s, Call& c);
+    void complete(const uint32_t* d_base, const std::vector<RowReq>& rows, Call& c, cudaStream_t s);
+
+    // CUDA-graph replay of the common path (plan upload .. sort) for repeated identical calls
+    struct CallKey {
+        const uint32_t* base = nullptr;
+        int dtype = 0, smallest = 0, scaled = 0, gather = 0;
+        uint32_t a_s_bits = 0;
+        void *vals = nullptr, *idx = nullptr, *piv = nullptr;
+        cudaStream_t s = nullptr;
+        std::vector<RowReq> rows;
+        bool operator==(const CallKey& o) const;
+    };
+    struct GraphCache {
+        bool valid = false;
+        CallKey key;
+        uint64_t gen = 0;
+        cudaGraphExec_t exec = nullptr;
+        std::vector<uint8_t> pinned;  // plan bytes the captured memcpy reads from pin_
+        Call call;
+        rtk_stats stats{};
+        uint32_t seq_incr = 0;
+    };
+    GraphCache graph_;
+    CallKey last_key_;
+    uint64_t last_gen_ = 0;
+    bool have_last_ = false;
+    bool graphs_ = true;          // RTK_GRAPHS=0 disables
+    bool stats_pending_ = false;
+    bool capturing_ = false;
+    bool sig_pending_ = false;    // a signalling sort launch is in flight
+    uint32_t expected_seq_ = 0;
+    cudaStream_t cap_s_ = nullptr; // private capture stream
+    uint32_t* hmap_ = nullptr;    // mapped pinned signal words (host view)
+    uint32_t* d_hmap_ = nullptr;  // device view
 
     int device_;
     DevBuf arena_;
@@ -144,7 +187,7 @@ private:
     cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
     DevBuf sel_, T_, count_, kmin_, kmax_, ghist_, samples_, cand_a_, cand_b_, seg_hist_,
         gcursor_, bstart_, dcap_, dcoff_, ctl_, row_fail_, groups_, slots0_, slotsA_, slotsB_, done_,
-        seg_ticket_, dbg_, wgroups_, ctot_;
+        seg_ticket_, dbg_, wgroups_, ctot_, sig_;
     uint64_t group_base_ = 0, wgroup_base_ = 0;
     uint32_t next_cap_ = 0;
     uint32_t wgroup_cap_ = 0;

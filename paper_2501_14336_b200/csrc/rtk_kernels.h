@@ -149,6 +149,12 @@ struct SortArgs {
     int gather;
     int dtype;
     int smallest;
+    // completion signal: the last CTA copies ctl[0..7] to mapped host memory and then writes
+    // a per-launch sequence number to hflags[15] (the host spins on it: no memcpy, no sync)
+    const uint32_t* ctl;
+    uint32_t* done_ctr;
+    uint32_t* seq_ctr;
+    volatile uint32_t* hflags;
 };
 
 inline int num_sms() {

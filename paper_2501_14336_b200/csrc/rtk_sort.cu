@@ -956,6 +956,21 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
         else if (grp.len <= 128) warp_sort_group<4>(grp, g, lane);
         else warp_sort_group<8>(grp, g, lane);
     }
+    if (g.hflags) {
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            if (atomicAdd(g.done_ctr, 1u) == gridDim.x - 1) {
+                __threadfence();
+                *g.done_ctr = 0;
+                const uint32_t seq = atomicAdd(g.seq_ctr, 1u) + 1;
+                const volatile uint32_t* c = g.ctl;
+                for (int i = 0; i < 8; ++i) g.hflags[i] = c[i];
+                __threadfence_system();
+                g.hflags[15] = seq;
+            }
+        }
+    }
 }
 
 // ---- launchers ----------------------------------------------------------------------------
