@@ -555,7 +555,21 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         const uint32_t wtot = __shfl_sync(full, incl, 31);
         if (wcur + wtot > kWarpStage) warp_flush();
         const uint32_t nidx0 = ~idx0;  // ~(idx0 + l) == nidx0 - l
-        if (wtot <= kWarpStage) {
+        if (wtot <= 96) {
+            // sparse hits (the common case): visit only the set bits; the element is re-read
+            // from L2 (its tile was just streamed) instead of indexing registers dynamically
+            const uint32_t* tp = in.base + off - lead + span0;
+            uint32_t o = wcur + incl - c;
+            uint32_t m = mask;
+            while (m) {
+                const uint32_t b = __ffs(m) - 1;
+                m &= m - 1;
+                const uint32_t l = ((b >> 3) * kThreads + threadIdx.x) * kVec + (b & 7);
+                const uint32_t key = key_of<KM>(__ldg(tp + l), in.a_s);
+                stage[o++] = (static_cast<unsigned long long>(key) << 32) | (nidx0 - l);
+            }
+            wcur += wtot;
+        } else if (wtot <= kWarpStage) {
             uint32_t o = wcur + incl - c;
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)

@@ -778,20 +778,12 @@ constexpr int kSortThreads = 256;
 constexpr int kSortItems = kSortCap / kSortThreads;  // 8
 static_assert(kSortItems == 8, "sort layout");
 
-// Bitonic sort (descending) of one group of <= 32*IPL composites by one warp: element
-// p = lane * IPL + e; strides < IPL compare inside the lane, larger ones across lanes (shuffles).
-// Ranks < k are written as (value bits, u64 index); rank k-1 also as the pivot.
-template <int IPL>
-__device__ __forceinline__ void warp_sort_group(const SortGroup& grp, const SortArgs& g, int lane) {
+// Bitonic network (descending) over one warp's registers: element p = lane * IPL + e; strides
+// < IPL compare inside the lane, larger ones across lanes (shuffles).
+template <int IPL, typename T>
+__device__ __forceinline__ void warp_bitonic_desc(T (&a)[IPL], int lane) {
     constexpr uint32_t N = 32 * IPL;
     const unsigned full = 0xffffffffu;
-    const unsigned long long* src = (grp.buf ? g.buf1 : g.buf0) + grp.off;
-    unsigned long long a[IPL];
-#pragma unroll
-    for (int e = 0; e < IPL; ++e) {
-        const uint32_t p = lane * IPL + e;
-        a[e] = p < grp.len ? __ldcg(src + p) : 0ull;
-    }
 #pragma unroll
     for (uint32_t kk = 2; kk <= N; kk <<= 1) {
 #pragma unroll
@@ -800,10 +792,9 @@ __device__ __forceinline__ void warp_sort_group(const SortGroup& grp, const Sort
 #pragma unroll
                 for (int e = 0; e < IPL; ++e) {
                     if (e & jj) continue;
-                    const uint32_t p = lane * IPL + e;
-                    const bool desc = (p & kk) == 0;
-                    const unsigned long long x = a[e], y = a[e + jj];
-                    const unsigned long long hi = max(x, y), lo = min(x, y);
+                    const bool desc = ((lane * IPL + e) & kk) == 0;
+                    const T x = a[e], y = a[e + jj];
+                    const T hi = max(x, y), lo = min(x, y);
                     a[e] = desc ? hi : lo;
                     a[e + jj] = desc ? lo : hi;
                 }
@@ -812,32 +803,83 @@ __device__ __forceinline__ void warp_sort_group(const SortGroup& grp, const Sort
                 const bool lower = (lane & lm) == 0;
 #pragma unroll
                 for (int e = 0; e < IPL; ++e) {
-                    const uint32_t p = lane * IPL + e;
-                    const bool desc = (p & kk) == 0;
-                    const unsigned long long o = __shfl_xor_sync(full, a[e], lm);
+                    const bool desc = ((lane * IPL + e) & kk) == 0;
+                    const T o = __shfl_xor_sync(full, a[e], lm);
                     a[e] = (lower == desc) ? max(a[e], o) : min(a[e], o);
                 }
             }
         }
     }
-    const uint32_t r = grp.rid;
-    const uint64_t kr = g.row_k[r];
-    const uint64_t oo = g.row_out_off[r];
+}
+
+__device__ __forceinline__ void emit_rank(const SortArgs& g, uint32_t r, uint64_t kr, uint64_t oo, uint64_t rank,
+                                          uint32_t key, uint32_t idx) {
+    uint32_t val;
+    if (g.gather) val = __ldg(g.in_base + g.row_in_off[r] + idx);
+    else if (g.dtype == kF32) val = decode_f32_bits(key, g.smallest);
+    else val = g.smallest ? ~key : key;
+    g.out_vals[oo + rank] = val;
+    g.out_idx[oo + rank] = idx;
+    if (rank == kr - 1 && g.pivots) g.pivots[r] = val;  // engine.hpp:333
+}
+
+// Sort one group of <= 32*IPL composites by one warp and write ranks < k as (value bits, u64
+// index). When the group's keys span < 2^(32 - b) values and its indices fit b bits, the
+// composite is packed order-preserving into 32 bits, ((key - kmin) << b) | (2^b - 1 - idx) >= 1
+// (padding = 0 sorts last), halving the network's shuffles and compares.
+template <int IPL>
+__device__ __forceinline__ void warp_sort_group(const SortGroup& grp, const SortArgs& g, int lane) {
+    const unsigned full = 0xffffffffu;
+    const unsigned long long* src = (grp.buf ? g.buf1 : g.buf0) + grp.off;
+    unsigned long long a[IPL];
+    uint32_t kmin = ~0u, kmax = 0, imax = 0;
 #pragma unroll
     for (int e = 0; e < IPL; ++e) {
         const uint32_t p = lane * IPL + e;
-        const uint64_t rank = grp.rank_base + p;
-        if (p >= grp.len || rank >= kr) continue;
-        const unsigned long long K = a[e];
-        const uint32_t kk = static_cast<uint32_t>(K >> 32);
-        const uint32_t idx = ~static_cast<uint32_t>(K);
-        uint32_t val;
-        if (g.gather) val = __ldg(g.in_base + g.row_in_off[r] + idx);
-        else if (g.dtype == kF32) val = decode_f32_bits(kk, g.smallest);
-        else val = g.smallest ? ~kk : kk;
-        g.out_vals[oo + rank] = val;
-        g.out_idx[oo + rank] = idx;
-        if (rank == kr - 1 && g.pivots) g.pivots[r] = val;
+        a[e] = p < grp.len ? __ldcg(src + p) : 0ull;
+        if (p < grp.len) {
+            const uint32_t key = static_cast<uint32_t>(a[e] >> 32), idx = ~static_cast<uint32_t>(a[e]);
+            kmin = min(kmin, key);
+            kmax = max(kmax, key);
+            imax = max(imax, idx);
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(full, kmin, d));
+        kmax = max(kmax, __shfl_xor_sync(full, kmax, d));
+        imax = max(imax, __shfl_xor_sync(full, imax, d));
+    }
+    const uint32_t r = grp.rid;
+    const uint64_t kr = g.row_k[r];
+    const uint64_t oo = g.row_out_off[r];
+    const int ib = imax >= 0x7fffffffu ? 32 : 32 - __clz(imax + 1);  // bits of imax + 1
+    if (ib < 32 && (kmax - kmin) < (1u << (32 - ib)) >> 0 && (static_cast<uint64_t>(kmax - kmin) << ib) < (1ull << 32)) {
+        const uint32_t mask = (1u << ib) - 1u;
+        uint32_t q[IPL];
+#pragma unroll
+        for (int e = 0; e < IPL; ++e) {
+            const uint32_t p = lane * IPL + e;
+            q[e] = p < grp.len ? ((static_cast<uint32_t>(a[e] >> 32) - kmin) << ib) | (mask - ~static_cast<uint32_t>(a[e]))
+                               : 0u;
+        }
+        warp_bitonic_desc<IPL>(q, lane);
+#pragma unroll
+        for (int e = 0; e < IPL; ++e) {
+            const uint32_t p = lane * IPL + e;
+            const uint64_t rank = grp.rank_base + p;
+            if (p >= grp.len || rank >= kr) continue;
+            emit_rank(g, r, kr, oo, rank, kmin + (q[e] >> ib), mask - (q[e] & mask));
+        }
+    } else {
+        warp_bitonic_desc<IPL>(a, lane);
+#pragma unroll
+        for (int e = 0; e < IPL; ++e) {
+            const uint32_t p = lane * IPL + e;
+            const uint64_t rank = grp.rank_base + p;
+            if (p >= grp.len || rank >= kr) continue;
+            emit_rank(g, r, kr, oo, rank, static_cast<uint32_t>(a[e] >> 32), ~static_cast<uint32_t>(a[e]));
+        }
     }
 }
 
