@@ -75,6 +75,8 @@ Engine::Engine(int device) : device_(device) {
     if (const char* sr = std::getenv("RTK_SAMPLE_R")) sample_r_ = std::max(1.0, std::atof(sr));
     if (const char* mq = std::getenv("RTK_MSD_Q")) msd_q_max_ = std::max(1, std::atoi(mq));
     if (const char* g = std::getenv("RTK_GRAPHS")) graphs_ = *g && *g != '0';
+    if (const char* g = std::getenv("RTK_SELFCLEAN")) self_clean_ok_ = *g && *g != '0';
+    if (const char* g = std::getenv("RTK_FORCE_INIT")) force_init_ = *g && *g != '0';
     const char* cs = std::getenv("RTK_COUNT_STATS");
     count_stats_ = profile_ || (cs && *cs && *cs != '0');
 }
@@ -226,15 +228,25 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
     key.rows = rows;
     const bool usable = graphs_ && !profile_ && !count_stats_;
     const uint64_t gen0 = g_buf_gen.load();
+    if (gen0 != last_gen_) needs_init_ = true;  // buffers reallocated: counters are garbage
     if (usable && graph_.valid && graph_.gen == gen0 && graph_.key == key) {
         // replay: restore the plan bytes the captured upload reads, launch, finish on the host
         if (!graph_.pinned.empty()) std::memcpy(pin_, graph_.pinned.data(), graph_.pinned.size());
         stats = graph_.stats;
+        const int R = static_cast<int>(rows.size());
+        if (!graph_.has_init && (needs_init_ || R > clean_upto_)) {
+            launch_init_call(R, count_.as<unsigned long long>(), kmin_.as<unsigned long long>(),
+                             kmax_.as<unsigned long long>(), T_.as<uint64_t>(), row_fail_.as<uint32_t>(),
+                             ctl_.as<uint32_t>(), seg_hist_.as<uint32_t>(), done_.as<uint32_t>(),
+                             seg_ticket_.as<uint32_t>(), s);
+        }
+        clean_rows_ = graph_.clean_rows;
         check(cudaGraphLaunch(graph_.exec, s), "graph launch");
         expected_seq_ += graph_.seq_incr;
         sig_pending_ = graph_.seq_incr > 0;
         Call c = graph_.call;
         complete(d_base, rows, c, s);
+        last_gen_ = g_buf_gen.load();
         return;
     }
     const bool capture = usable && have_last_ && last_gen_ == gen0 && last_key_ == key;
@@ -279,6 +291,8 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         graph_.call = c;
         graph_.stats = stats;
         graph_.seq_incr = expected_seq_ - seq0;
+        graph_.has_init = did_init_;
+        graph_.clean_rows = clean_rows_;
         graph_.valid = true;
         check(cudaGraphLaunch(exec, s), "graph launch");
     } else {
@@ -286,9 +300,9 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         enqueue(d_base, dtype, smallest, scaled, a_s, gather, rows, d_vals, d_idx, d_pivots, s, c);
     }
     last_key_ = std::move(key);
-    last_gen_ = g_buf_gen.load();
     have_last_ = true;
     complete(d_base, rows, c, s);
+    last_gen_ = g_buf_gen.load();
 }
 
 // Everything up to the last kernel of the common path, stream-ordered, no host synchronisation
@@ -306,6 +320,9 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     wgroup_base_ = 0;
     bar_gen_ = 0;
     sig_pending_ = false;
+    self_clean_ = !count_stats_ && self_clean_ok_;  // the main finish resets counters; fallback/deeper levels never
+    clean_rows_ = 0;
+    did_init_ = false;
     InputSrc src{d_base, dtype, smallest, scaled ? 1 : 0, a_s};
     const uint64_t base_words = reinterpret_cast<uintptr_t>(d_base) / 4;
 
@@ -448,12 +465,17 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     done_.ensure(4 * R);
     seg_ticket_.ensure(4 * R);
     seg_hist_.ensure(4ull * kBins * R);
-    // one kernel resets every per-call counter (unsampled rows keep T = 0)
+    // one kernel resets every per-call counter (unsampled rows keep T = 0) — unless the previous
+    // call's last sort CTA already did (self-cleaning, see SortArgs::R_clean)
+    if (needs_init_ || R > clean_upto_ || force_init_) {
+    needs_init_ = false;
+    did_init_ = true;
     launch_init_call(R, count_.as<unsigned long long>(), kmin_.as<unsigned long long>(),
                      kmax_.as<unsigned long long>(), T_.as<uint64_t>(), row_fail_.as<uint32_t>(),
                      ctl_.as<uint32_t>(), seg_hist_.as<uint32_t>(), done_.as<uint32_t>(),
                      seg_ticket_.as<uint32_t>(), s);
     ++stats.kernel_launches;
+    }
     mark("init", s);
 
     for (int g = 0; g < 2; ++g) {
@@ -509,7 +531,19 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
 void Engine::complete(const uint32_t* d_base, const std::vector<RowReq>& rows, Call& c, cudaStream_t s) {
     const int R = static_cast<int>(rows.size());
     uint32_t ctl[8];
+    self_clean_ = false;
+    // the next call may skip the init kernel only if this call's main sort cleaned every row and
+    // nothing else (deeper levels, exact path, errors) touches the counters afterwards
+    const bool cleaned = clean_rows_ >= R && sig_pending_;
+    needs_init_ = true;
     drain(c, ctl);
+    // first_flags_: the flag word as the main path left it (drain's deeper levels clear kFlagMore)
+    if (cleaned && (first_flags_ & (kFlagFail | kFlagMore | kFlagOverflow)) == 0) {
+        needs_init_ = false;
+        clean_upto_ = clean_rows_;
+    } else {
+        clean_upto_ = 0;
+    }
 
     // ---- exact path for rows whose sampled threshold missed (rare) ------------------------
     if (ctl[0] & kFlagFail) {
@@ -629,7 +663,18 @@ void Engine::launch_finish(Call& c, const FinishPrep& f) {
         stats.kernel_launches += 1;
         mark("msd", c.s);
     }
-    launch_sort(static_cast<uint32_t>(f.max_groups + f.max_wgroups / 8 + 1), sort_args(c, f.gl), c.s);
+    SortArgs sa = sort_args(c, f.gl);
+    if (self_clean_) {
+        sa.R_clean = c.R;
+        sa.c_count = count_.as<unsigned long long>();
+        sa.c_kmin = kmin_.as<unsigned long long>();
+        sa.c_kmax = kmax_.as<unsigned long long>();
+        sa.c_T = T_.as<uint64_t>();
+        sa.c_done = done_.as<uint32_t>();
+        sa.c_ticket = seg_ticket_.as<uint32_t>();
+        clean_rows_ = c.R;
+    }
+    launch_sort(static_cast<uint32_t>(f.max_groups + f.max_wgroups / 8 + 1), sa, c.s);
     mark("sort+pivots", c.s);
 }
 
@@ -707,6 +752,7 @@ void Engine::drain(Call& c, uint32_t (&ctl)[8]) {
         std::memcpy(ctl, hctl_, 32);
     }
     sig_pending_ = false;
+    first_flags_ = ctl[0];
     if (profile_)
         std::fprintf(stderr, "[rtk ctl] flags=%u cta_groups=%u next_slots=%u warp_groups=%u\n", ctl[0], ctl[1], ctl[3], ctl[5]);
     if (ctl[0] & kFlagOverflow) throw Error{RTK_INTERNAL, "device work list overflow"};

@@ -160,6 +160,8 @@ private:
         Call call;
         rtk_stats stats{};
         uint32_t seq_incr = 0;
+        bool has_init = false;
+        int clean_rows = 0;
     };
     GraphCache graph_;
     CallKey last_key_;
@@ -168,6 +170,14 @@ private:
     bool graphs_ = true;          // RTK_GRAPHS=0 disables
     bool stats_pending_ = false;
     bool capturing_ = false;
+    bool needs_init_ = true;      // per-call counters not known to be clean
+    bool self_clean_ = false;     // the next main sort launch resets the counters
+    bool self_clean_ok_ = true;   // RTK_SELFCLEAN=0 disables
+    bool force_init_ = false;     // RTK_FORCE_INIT=1: init kernel every call (debug)
+    int clean_rows_ = 0;
+    int clean_upto_ = 0;          // rows whose counters the last call left clean
+    bool did_init_ = false;
+    uint32_t first_flags_ = 0;    // flag word of the last drain's first readback
     bool sig_pending_ = false;    // a signalling sort launch is in flight
     uint32_t expected_seq_ = 0;
     cudaStream_t cap_s_ = nullptr; // private capture stream

@@ -155,6 +155,15 @@ struct SortArgs {
     uint32_t* done_ctr;
     uint32_t* seq_ctr;
     volatile uint32_t* hflags;
+    // self-cleaning (R_clean > 0): after publishing, the last CTA resets the per-call counters
+    // of R_clean state rows and the control words, so the next call needs no init kernel
+    int R_clean;
+    unsigned long long* c_count;
+    unsigned long long* c_kmin;
+    unsigned long long* c_kmax;
+    uint64_t* c_T;
+    uint32_t* c_done;
+    uint32_t* c_ticket;
 };
 
 inline int num_sms() {

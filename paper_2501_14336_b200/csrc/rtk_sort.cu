@@ -1010,7 +1010,22 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
                 for (int i = 0; i < 8; ++i) g.hflags[i] = c[i];
                 __threadfence_system();
                 g.hflags[15] = seq;
+                s_g = 1;
+            } else {
+                s_g = 0;
             }
+        }
+        __syncthreads();
+        if (s_g && g.R_clean > 0) {  // the last CTA: reset the call's counters for the next call
+            for (int r = tid; r < g.R_clean; r += kSortThreads) {
+                g.c_count[r] = 0;
+                g.c_kmin[r] = ~0ull;
+                g.c_kmax[r] = 0;
+                g.c_T[r] = 0;
+                g.c_done[r] = 0;
+                g.c_ticket[r] = 0;
+            }
+            if (tid < 16) const_cast<uint32_t*>(g.ctl)[tid] = 0;
         }
     }
 }
