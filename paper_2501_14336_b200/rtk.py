@@ -154,11 +154,27 @@ class Instrumentation:
     total_ms: float = 0.0
 
 
-@dataclass
 class TopKResult:
-    values: Any
-    indices: Any
-    pivot: Any = None
+    """rtk::TopKResult (engine.hpp:103-108). For device results the pivot stays on the device
+    until first read (no host synchronisation inside the call)."""
+
+    __slots__ = ("values", "indices", "_pivot", "_pivot_fn")
+
+    def __init__(self, values, indices, pivot=None, pivot_fn=None):
+        self.values, self.indices = values, indices
+        self._pivot, self._pivot_fn = pivot, pivot_fn
+
+    @property
+    def pivot(self):
+        if self._pivot_fn is not None:
+            self._pivot, self._pivot_fn = self._pivot_fn(), None
+        return self._pivot
+
+    def __iter__(self):
+        return iter((self.values, self.indices, self.pivot))
+
+    def __repr__(self):
+        return f"TopKResult(values={self.values!r}, indices={self.indices!r}, pivot={self.pivot!r})"
 
 
 # ---- handle management -------------------------------------------------------------------
@@ -238,7 +254,9 @@ def topk(input, k: int, order: SelectionOrder = SelectionOrder.Largest,
                           int(order), C.c_void_p(vals.data_ptr()), C.c_void_p(idx.data_ptr()),
                           C.c_void_p(piv.data_ptr()), C.byref(c), _stream_ptr(x))
         _raise(st, "rtk_topk")
-        return TopKResult(vals, idx, piv[0].item() if code == 0 else int(piv.view(torch.int32)[0].item()) & 0xFFFFFFFF)
+        if code == 0:
+            return TopKResult(vals, idx, pivot_fn=lambda: piv[0].item())
+        return TopKResult(vals, idx, pivot_fn=lambda: int(piv.view(torch.int32)[0].item()) & 0xFFFFFFFF)
     a = np.ascontiguousarray(input.numpy() if hasattr(input, "numpy") else np.asarray(input))
     n = a.size
     kk = max(int(k), 0)
@@ -403,7 +421,7 @@ def scaled_topk(input, k: int, order: SelectionOrder = SelectionOrder.Largest,
                                  C.c_void_p(idx.data_ptr()), C.c_void_p(piv.data_ptr()),
                                  C.byref(si), C.byref(c), _stream_ptr(x))
         _raise(st, "rtk_topk_scaled")
-        res = TopKResult(vals, idx, piv[0].item())
+        res = TopKResult(vals, idx, pivot_fn=lambda: piv[0].item())
     else:
         a = np.ascontiguousarray(input.numpy() if hasattr(input, "numpy") else np.asarray(input))
         if a.dtype != np.float32:
@@ -446,4 +464,4 @@ def merge_shards(cand_vals, cand_idx, block_len: Sequence[int], shard_base: Sequ
                               C.c_void_p(vals.data_ptr()), C.c_void_p(idx.data_ptr()),
                               C.c_void_p(piv.data_ptr()), _stream_ptr(cv))
     _raise(st, "rtk_merge_shards")
-    return TopKResult(vals, idx, piv[0].item())
+    return TopKResult(vals, idx, pivot_fn=lambda: piv[0].item())
