@@ -122,6 +122,7 @@ def main():
     ap.add_argument("--batch-ks", type=str, default="50,4096,128256",
                     help="C3 batched LLM-vocab top-k: k values measured into batch_llm (empty = skip)")
     ap.add_argument("--batch-rows", type=int, default=256)
+    ap.add_argument("--c4", type=int, default=1, help="C4 adversarial scaled_topk leg (1 = on)")
     ap.add_argument("--vocab", type=int, default=128256)
     args = ap.parse_args()
 
@@ -229,6 +230,29 @@ def main():
     comp_ms = statistics.mean(comp)
     achieved = 4 * n / (comp_ms * 1e-3) / 1e9
 
+    # C4: adversarial distribution (one first-pass bin, ~6.5K distinct values => heavy ties),
+    # scaled_topk with the reference's three scale policies (scaling.hpp:42-86)
+    adversarial = {}
+    if args.c4 and rank == 0:
+        na, ka = 1 << 26, 1 << 16
+        xa = (128.6 + 0.1 * torch.rand(na, device=dev, generator=gen)).float()
+        for name, mode in (("off", 0), ("always", 1), ("adaptive", 2)):
+            pol = R.ScalePolicy(mode=R.ScaleMode(mode), trigger_fraction=0.5, seed=31)
+            for _ in range(3):
+                rtk.scaled_topk(xa, ka, policy=pol)
+            times = []
+            for _ in range(max(5, args.steps // 2)):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                rtk.scaled_topk(xa, ka, policy=pol)
+                b.record(stream)
+                torch.cuda.synchronize()
+                times.append(a.elapsed_time(b))
+            ms_a = statistics.mean(times)
+            adversarial[name] = {"ms": ms_a, "GBps": (4 * na + 12 * ka) / (ms_a * 1e-3) / 1e9,
+                                 "fraction_of_hbm_peak": (4 * na + 12 * ka) / (ms_a * 1e-3) / 1e9 / peak}
+        del xa
+
     # C3: batched LLM sampling top-k, rows sharded across ranks (no collective)
     batch_llm = {}
     if args.batch_ks:
@@ -308,6 +332,8 @@ def main():
                             "kernel_share_of_step": comp_ms / mean_ms},
                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
                "k_sweep": sweep,
+               "adversarial_c4": {"config": "n=2^26 Uniform[128.6,128.7) fp32, k=2^16, largest, scaled_topk "
+                                            "tau=0.5 seed=31 (device-resident)", "results": adversarial},
                "batch_llm": {"config": f"{args.batch_rows} x {args.vocab} fp32 N(0,1) logits, rows sharded over "
                                        f"{world} GPU(s), L2 flushed between batches", "results": batch_llm},
                "step_ms_all": ms}

@@ -149,6 +149,7 @@ ScaleDecision decide_scale(Engine& e, const float* d_in, uint64_t n, uint64_t k,
 void run_scaled(Engine& e, const float* d_in, uint64_t n, uint64_t k, int order, int mode, double tau,
                 uint64_t seed, float* d_vals, uint64_t* d_idx, float* d_piv, rtk_scale_info* info,
                 const rtk_cfg& cfg, cudaStream_t s) {
+    e.stats = rtk_stats{};  // the trigger pass of this call is added to the run's counters below
     ScaleDecision d = decide_scale(e, d_in, n, k, order, mode, tau, seed, cfg, s);
     const rtk_stats pre = e.stats;
     e.run(reinterpret_cast<const uint32_t*>(d_in), RTK_F32, order, d.scale, d.a_s, /*gather=*/d.scale,

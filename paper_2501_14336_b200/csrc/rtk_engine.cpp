@@ -232,6 +232,10 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
     if (usable && graph_.valid && graph_.gen == gen0 && graph_.key == key) {
         // replay: restore the plan bytes the captured upload reads, launch, finish on the host
         if (!graph_.pinned.empty()) std::memcpy(pin_, graph_.pinned.data(), graph_.pinned.size());
+        arena_used_ = graph_.arena_used;  // later (host-driven) uploads go after the captured plan
+        pin_used_ = graph_.pin_used;
+        group_base_ = graph_.group_base;
+        wgroup_base_ = graph_.wgroup_base;
         stats = graph_.stats;
         const int R = static_cast<int>(rows.size());
         if (!graph_.has_init && (needs_init_ || R > clean_upto_)) {
@@ -292,6 +296,10 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         graph_.stats = stats;
         graph_.seq_incr = expected_seq_ - seq0;
         graph_.has_init = did_init_;
+        graph_.arena_used = arena_used_;
+        graph_.pin_used = pin_used_;
+        graph_.group_base = group_base_;
+        graph_.wgroup_base = wgroup_base_;
         graph_.clean_rows = clean_rows_;
         graph_.valid = true;
         check(cudaGraphLaunch(exec, s), "graph launch");

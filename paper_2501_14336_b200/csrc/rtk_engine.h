@@ -162,6 +162,8 @@ private:
         uint32_t seq_incr = 0;
         bool has_init = false;
         int clean_rows = 0;
+        size_t arena_used = 0, pin_used = 0;
+        uint64_t group_base = 0, wgroup_base = 0;
     };
     GraphCache graph_;
     CallKey last_key_;
