@@ -74,6 +74,7 @@ Engine::Engine(int device) : device_(device) {
     profile_ = p && *p && *p != '0';
     if (const char* sr = std::getenv("RTK_SAMPLE_R")) sample_r_ = std::max(1.0, std::atof(sr));
     if (const char* mq = std::getenv("RTK_MSD_Q")) msd_q_max_ = std::max(1, std::atoi(mq));
+    if (const char* mb = std::getenv("RTK_MSD_BITS")) msd_max_bits_ = std::min(kMsdMaxBits, std::max(11, std::atoi(mb)));
     if (const char* g = std::getenv("RTK_GRAPHS")) graphs_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_SELFCLEAN")) self_clean_ok_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_FORCE_INIT")) force_init_ = *g && *g != '0';
@@ -138,11 +139,15 @@ void Engine::report_marks() {
     if (!profile_ || marks_.empty()) return;
     cudaEventSynchronize(marks_.back().ev);
     if (dbg_.p) {
-        unsigned long long d[32];
+        unsigned long long d[64];
         cudaMemcpy(d, dbg_.p, sizeof(d), cudaMemcpyDeviceToHost);
-        std::fprintf(stderr, "[rtk dbg phases ns]");
-        for (unsigned long long i = 1; i < d[31] && i < 31; ++i) std::fprintf(stderr, " %llu", d[i] - d[i - 1]);
-        std::fprintf(stderr, "\n");
+        for (int blk = 0; blk < 2; ++blk) {
+            const unsigned long long* e = d + 32 * blk;
+            std::fprintf(stderr, "[rtk dbg %s phases ns]", blk ? "sample" : "msd/rows");
+            for (unsigned long long i = 1; i < e[31] && i < 31; ++i) std::fprintf(stderr, " %llu", e[i] - e[i - 1]);
+            std::fprintf(stderr, "\n");
+        }
+        cudaMemset(dbg_.p, 0, sizeof(d));
     }
     std::fprintf(stderr, "[rtk profile]");
     for (size_t i = 1; i < marks_.size(); ++i) {
@@ -488,10 +493,10 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
 
     for (int g = 0; g < 2; ++g) {
         if (sg[g].rid.empty()) continue;
-        if (profile_) dbg_.ensure(256);
+        if (profile_) dbg_.ensure(4096);
         SampleRows sr{at<uint32_t>(D, o_sg[g][0]), at<uint64_t>(D, o_sg[g][1]), at<uint64_t>(D, o_sg[g][2]),
                       at<uint64_t>(D, o_sg[g][3]), at<uint64_t>(D, o_sg[g][4]), at<uint64_t>(D, o_sg[g][5]),
-                      profile_ ? dbg_.as<unsigned long long>() : nullptr};
+                      profile_ ? dbg_.as<unsigned long long>() + 32 : nullptr};
         launch_sample_select(static_cast<int>(sg[g].rid.size()), sg[g].cs, sg[g].per_cta, sr, src,
                              T_.as<uint64_t>(), s);
         check(cudaGetLastError(), "sample_select launch");
@@ -509,7 +514,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
                          at<uint64_t>(D, o_f[v][3]), src, c.d_row_out, d_vals, d_idx, d_pivots,
                          row_fail_.as<uint32_t>(), ctl_.as<uint32_t>(), nullptr};
         if (profile_) {
-            dbg_.ensure(256);
+            dbg_.ensure(4096);
             fa.dbg = dbg_.as<unsigned long long>();
         }
         launch_rows_fused(static_cast<int>(frow[v].size()), fa, v == 1, s);
@@ -593,7 +598,7 @@ Engine::FinishPrep Engine::prepare_finish(Call& c, const std::vector<uint32_t>& 
         if (cp <= kSortCap) continue;
         ++f.big_rows;
         max_cap = std::max(max_cap, cp);
-        const uint64_t bins = uint64_t(1) << fine_bits(cp);
+        const uint64_t bins = uint64_t(1) << std::min<uint32_t>(fine_bits(cp), msd_max_bits_);
         cta_groups += std::min<uint64_t>(bins, cp / (kWarpGroupMax + 1) + 1);
         warp_groups += std::min<uint64_t>(bins, cp);
     }
@@ -635,6 +640,7 @@ PlanArgs Engine::plan_args(const Call& c, const FinishPrep& f) {
     pa.flags = ctl_.as<uint32_t>();
     pa.row_fail = row_fail_.as<uint32_t>();
     pa.done = done_.as<uint32_t>();
+    pa.max_bits = static_cast<uint32_t>(msd_max_bits_);
     return pa;
 }
 
@@ -643,7 +649,7 @@ void Engine::launch_finish(Call& c, const FinishPrep& f) {
     if (f.big_rows) {
         FineArgs fa{c.d_row_k, f.gl, f.wgl, f.nextA, ctl_.as<uint32_t>(), nullptr, 1, nullptr, nullptr, 0};
         if (profile_) {
-            dbg_.ensure(256);
+            dbg_.ensure(4096);
             fa.dbg = dbg_.as<unsigned long long>();
         }
         // one huge slot: spread it over Q co-resident 8-CTA clusters (>= ~8K composites per CTA)

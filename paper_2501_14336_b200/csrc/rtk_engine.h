@@ -204,7 +204,8 @@ private:
     uint32_t next_cap_ = 0;
     uint32_t wgroup_cap_ = 0;
     uint32_t bar_gen_ = 0;        // grid-barrier target of the level-0 MSD (ctl[7], reset per call)
-    int msd_q_max_ = 8;           // clusters per huge slot (RTK_MSD_Q)
+    int msd_q_max_ = 32;          // clusters per huge slot (RTK_MSD_Q)
+    int msd_max_bits_ = kMsdMaxBits;  // RTK_MSD_BITS
 };
 
 }  // namespace rtk_b200

@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
     constexpr int kG = 8;  // per_cta <= 8192 = 8 x 1024 (double-buffered: 2 x 64 KB)
     unsigned long long* cur = smp;
     unsigned long long* alt = smp + kG * 1024;
+    uint32_t* hsub = reinterpret_cast<uint32_t*>(smp + 2 * kG * 1024);  // 4 x kBins sub-histograms
     __shared__ uint32_t s_cnt;
     uint32_t raw[kG];
 #pragma unroll
@@ -310,18 +311,22 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
     const unsigned long long target = sr.target[j];
     unsigned int pos = 53;
     for (;;) {
-        for (int b = tid; b < kBins; b += blockDim.x) { hist[b] = 0; hred[b] = 0; }
+        for (int b = tid; b < 4 * kBins; b += blockDim.x) hsub[b] = 0;
+        for (int b = tid; b < kBins; b += blockDim.x) hred[b] = 0;
         __syncthreads();
         const unsigned int hi = digit_hi(pos);
-        const unsigned long long pm = hi >= 64 ? 0ull : (prefix >> hi);
         const uint32_t dmask = (1u << (hi - pos)) - 1u;
-        // every element left in `cur` matches the prefix (compacted after each pass)
-        (void)pm;
+        // every element left in `cur` matches the prefix (compacted after each pass); four
+        // warp-interleaved sub-histograms: the clustered top digit of real data hits few bins
+        uint32_t* hmine = hsub + (warp & 3) * kBins;
         for (uint32_t i = tid; i < ((local + 31) & ~31u); i += blockDim.x) {
             const bool in_range = i < local;
             const unsigned long long K = in_range ? cur[i] : 0ull;
-            hist_add(hist, static_cast<uint32_t>(K >> pos) & dmask, in_range);
+            if (in_range) atomicAdd(hmine + (static_cast<uint32_t>(K >> pos) & dmask), 1u);
         }
+        __syncthreads();
+        for (int b = tid; b < kBins; b += blockDim.x)
+            hist[b] = hsub[b] + hsub[kBins + b] + hsub[2 * kBins + b] + hsub[3 * kBins + b];
         stamp();
         cluster.sync();
         stamp();
@@ -697,7 +702,8 @@ void launch_init_call(int R, unsigned long long* count, unsigned long long* kmin
 void launch_sample_select(int rows, int cs, uint32_t per_cta, const SampleRows& sr, const InputSrc& in,
                           uint64_t* T, cudaStream_t s) {
     if (rows <= 0) return;
-    const size_t smem = 2 * 8192 * sizeof(unsigned long long);  // double buffer (per_cta <= 8192)
+    // double buffer (per_cta <= 8192) + 4 sub-histograms
+    const size_t smem = 2 * 8192 * sizeof(unsigned long long) + 4 * kBins * sizeof(uint32_t);
     (void)per_cta;
     static bool configured = false;
     if (!configured) {

@@ -20,7 +20,7 @@ __device__ __forceinline__ void plan_row(int j, uint32_t r, const PlanArgs& pa) 
     } else {
         const unsigned long long x = __ldcg(pa.kmin + r) ^ __ldcg(pa.kmax + r);
         const int hb = 63 - __clzll(x ? x : 1ull);
-        const int bits = static_cast<int>(fine_bits(m));  // level 0: fine MSD digit
+        const int bits = static_cast<int>(min(fine_bits(m), pa.max_bits));  // level 0: fine MSD digit
         sl.len = m;
         sl.bits = static_cast<uint32_t>(bits);
         sl.pos = static_cast<uint32_t>(hb >= bits - 1 ? hb - (bits - 1) : 0);

@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* s
     cg::cluster_group cluster = cg::this_cluster();
     // [0,B): counts -> intra-cluster offsets -> cursors; [B, B+slice): slice totals -> starts;
     // [B+slice, B+2 slice): cross-cluster offsets (Q > 1)
-    extern __shared__ uint32_t sm[];
+    extern __shared__ __align__(16) uint32_t sm[];
     __shared__ uint32_t s_ssum[16];
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -691,14 +691,21 @@ __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* s
     msd_plan_slice(sl, tot, slice, off, q == 0, fa);
     cluster.sync();
     if (dbg) fa.dbg[4] = msd_timer();
-    // 5: cursors from the owners' bucket starts (+ cross-cluster offsets), then the scatter
-    for (uint32_t b = threadIdx.x; b < B; b += kMsdThreads) {
-        const uint32_t ow = b / slice, i = b - ow * slice;
-        const uint32_t st = *cluster.map_shared_rank(tot + i, ow);
-        const uint32_t qo = Q > 1 ? *cluster.map_shared_rank(qoff + i, ow) : 0u;
-        h[b] = st == ~0u ? ~0u : st + qo + h[b];
+    // 5: cursors from the owners' bucket starts (+ cross-cluster offsets), 16-byte DSMEM reads
+    for (uint32_t b = threadIdx.x * 4; b < B; b += kMsdThreads * 4) {
+        const uint32_t ow = b / slice, i = b - ow * slice;  // slice is a multiple of 4
+        const uint4 st = *reinterpret_cast<const uint4*>(cluster.map_shared_rank(tot + i, ow));
+        const uint4 qo = Q > 1 ? *reinterpret_cast<const uint4*>(cluster.map_shared_rank(qoff + i, ow))
+                               : make_uint4(0, 0, 0, 0);
+        uint4 c = *reinterpret_cast<uint4*>(h + b);
+        c.x = st.x == ~0u ? ~0u : st.x + qo.x + c.x;
+        c.y = st.y == ~0u ? ~0u : st.y + qo.y + c.y;
+        c.z = st.z == ~0u ? ~0u : st.z + qo.z + c.z;
+        c.w = st.w == ~0u ? ~0u : st.w + qo.w + c.w;
+        *reinterpret_cast<uint4*>(h + b) = c;
     }
     cluster.sync();  // owners' shared memory is read by everyone before anyone exits
+    if (dbg) fa.dbg[5] = msd_timer();
     uint64_t* qd = dst + sl.off;
     msd_stream(p, e0, e1, [&](unsigned long long K, bool valid) {
         const uint32_t d = static_cast<uint32_t>(K >> sl.pos) & dmask;
@@ -714,7 +721,7 @@ __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* s
             if (h[d] != ~0u) qd[atomicAdd(h + d, 1u)] = K;
         }
     });
-    if (dbg) { fa.dbg[5] = msd_timer(); fa.dbg[31] = 6; }
+    if (dbg) { fa.dbg[6] = msd_timer(); fa.dbg[31] = 7; }
 }
 
 // ---- k_seg_scatter ------------------------------------------------------------------------
