@@ -197,15 +197,15 @@ def main():
             b.record(stream)
         torch.cuda.synchronize()
         ms = [a.elapsed_time(b) for a, b in ev]
-        # kernel share (library-internal CUDA events around k_compact), measured on separate
-        # steps so the stats readback never sits inside the timed region
-        comp, launches = [], 0
+        # kernel share: k_compact bracketed by CUDA events on its stream (library timing mode:
+        # no graph replay), on separate steps so no stats readback sits inside the timed region
+        launches = R.last_stats(local).kernel_launches * steps
+        R.set_timing(True, local)
+        comp = []
         for _ in range(min(steps, 10)):
             step(kk)
-            st = R.last_stats(local)
-            comp.append(st.compact_ms)
-            launches = st.kernel_launches
-        launches *= steps
+            comp.append(R.last_stats(local).compact_ms)
+        R.set_timing(False, local)
         if world > 1:
             t = torch.tensor([statistics.mean(ms)], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)

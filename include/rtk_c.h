@@ -106,6 +106,11 @@ const char* rtk_last_error(void);             /* thread-local message of the las
 int rtk_handle_create(rtk_handle* out, int device);
 int rtk_handle_destroy(rtk_handle h);
 int rtk_get_stats(rtk_handle h, rtk_stats* out);
+/* timing mode (on != 0): calls are never replayed from a CUDA graph and k_compact is bracketed
+ * by CUDA events on the call's stream, so rtk_stats.compact_ms is measured for every call. Off
+ * (default): repeated identical calls replay one graph with no events inside (kernel-to-kernel
+ * programmatic launch edges stay intact); compact_ms is then only set for non-replayed calls. */
+int rtk_set_timing(rtk_handle h, int on);
 void rtk_cfg_default(rtk_cfg* cfg);
 int rtk_cfg_validate(const rtk_cfg* cfg);
 

@@ -205,6 +205,13 @@ int rtk_handle_destroy(rtk_handle h) {
     return guarded([&] { delete h; });
 }
 
+int rtk_set_timing(rtk_handle h, int on) {
+    return guarded([&] {
+        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+        h->engine.set_timing(on != 0);
+    });
+}
+
 int rtk_get_stats(rtk_handle h, rtk_stats* out) {
     return guarded([&] {
         if (!h || !out) throw Error{RTK_INVALID_ARGUMENT, "null argument"};

@@ -119,6 +119,12 @@ __device__ __forceinline__ void ldg256_u64(const uint64_t* p, uint64_t (&r)[4]) 
                  : "l"(p));
 }
 
+// Programmatic dependent launch (PDL): a dependent kernel may start while its predecessor
+// runs; it must wait before touching the predecessor's outputs. Both are no-ops when the
+// kernel was launched without the programmatic-serialization attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Launch row owning flat tile t (tile_start is an exclusive prefix, R+1 entries).
 __device__ __forceinline__ int row_of_tile(const Rows& rows, uint64_t t) {
     int lo = 0, hi = rows.R - 1;

@@ -78,6 +78,8 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_GRAPHS")) graphs_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_SELFCLEAN")) self_clean_ok_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_FORCE_INIT")) force_init_ = *g && *g != '0';
+    if (const char* g = std::getenv("RTK_GRAPH_EVENTS")) no_graph_events_ = *g == '0';
+    if (const char* g = std::getenv("RTK_PREFETCH_MB")) prefetch_mb_ = std::max(0, std::atoi(g));
     const char* cs = std::getenv("RTK_COUNT_STATS");
     count_stats_ = profile_ || (cs && *cs && *cs != '0');
 }
@@ -122,7 +124,15 @@ uint8_t* Engine::upload(const Plan& p, cudaStream_t s) {
         uint8_t* h = pin_ + pin_used_;
         pin_used_ += need;
         std::memcpy(h, p.bytes.data(), p.bytes.size());
-        check(cudaMemcpyAsync(d, h, p.bytes.size(), cudaMemcpyHostToDevice, s), "plan upload");
+        if (capturing_) {
+            // not part of the graph: the plan is uploaded now on the caller's stream, and again
+            // before a replay only if another call has overwritten the arena since (arena_tag_)
+            check(cudaMemcpyAsync(d, h, p.bytes.size(), cudaMemcpyHostToDevice, user_s_), "plan upload");
+            cap_uploads_.push_back({d, h, p.bytes.size()});
+        } else {
+            check(cudaMemcpyAsync(d, h, p.bytes.size(), cudaMemcpyHostToDevice, s), "plan upload");
+        }
+        ++arena_tag_;
     }
     return d;
 }
@@ -145,6 +155,7 @@ void Engine::report_marks() {
             const unsigned long long* e = d + 32 * blk;
             std::fprintf(stderr, "[rtk dbg %s phases ns]", blk ? "sample" : "msd/rows");
             for (unsigned long long i = 1; i < e[31] && i < 31; ++i) std::fprintf(stderr, " %llu", e[i] - e[i - 1]);
+            if (!blk && e[12]) std::fprintf(stderr, " | plan: %llu %llu %llu", e[10] - e[3], e[11] - e[10], e[12] - e[11]);
             std::fprintf(stderr, "\n");
         }
         cudaMemset(dbg_.p, 0, sizeof(d));
@@ -231,12 +242,17 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
     key.piv = d_pivots;
     key.s = s;
     key.rows = rows;
-    const bool usable = graphs_ && !profile_ && !count_stats_;
+    const bool usable = graphs_ && !profile_ && !count_stats_ && !timing_;
     const uint64_t gen0 = g_buf_gen.load();
     if (gen0 != last_gen_) needs_init_ = true;  // buffers reallocated: counters are garbage
     if (usable && graph_.valid && graph_.gen == gen0 && graph_.key == key) {
         // replay: restore the plan bytes the captured upload reads, launch, finish on the host
-        if (!graph_.pinned.empty()) std::memcpy(pin_, graph_.pinned.data(), graph_.pinned.size());
+        if (arena_tag_ != graph_.arena_tag) {  // another call reused the arena: re-upload the plan
+            if (!graph_.pinned.empty()) std::memcpy(pin_, graph_.pinned.data(), graph_.pinned.size());
+            for (const auto& u : graph_.uploads)
+                check(cudaMemcpyAsync(u.d, u.h, u.bytes, cudaMemcpyHostToDevice, s), "plan upload");
+            arena_tag_ = graph_.arena_tag;
+        }
         arena_used_ = graph_.arena_used;  // later (host-driven) uploads go after the captured plan
         pin_used_ = graph_.pin_used;
         group_base_ = graph_.group_base;
@@ -250,7 +266,9 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
                              seg_ticket_.as<uint32_t>(), s);
         }
         clean_rows_ = graph_.clean_rows;
+        check(cudaEventRecord(ev_[0], s), "event");
         check(cudaGraphLaunch(graph_.exec, s), "graph launch");
+        check(cudaEventRecord(ev_[3], s), "event");
         expected_seq_ += graph_.seq_incr;
         sig_pending_ = graph_.seq_incr > 0;
         Call c = graph_.call;
@@ -273,6 +291,8 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         cudaGraph_t graph = nullptr;
         bool ok = true;
         capturing_ = true;
+        user_s_ = s;
+        cap_uploads_.clear();
         try {
             enqueue(d_base, dtype, smallest, scaled, a_s, gather, rows, d_vals, d_idx, d_pivots, cap_s_, c);
         } catch (const Error&) {
@@ -297,6 +317,8 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         graph_.key = key;
         graph_.gen = gen0;
         graph_.pinned.assign(pin_, pin_ + pin_used_);
+        graph_.uploads = cap_uploads_;
+        graph_.arena_tag = arena_tag_;
         graph_.call = c;
         graph_.stats = stats;
         graph_.seq_incr = expected_seq_ - seq0;
@@ -307,7 +329,9 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         graph_.wgroup_base = wgroup_base_;
         graph_.clean_rows = clean_rows_;
         graph_.valid = true;
+        check(cudaEventRecord(ev_[0], s), "event");
         check(cudaGraphLaunch(exec, s), "graph launch");
+        check(cudaEventRecord(ev_[3], s), "event");
     } else {
         cudaGetLastError();
         enqueue(d_base, dtype, smallest, scaled, a_s, gather, rows, d_vals, d_idx, d_pivots, s, c);
@@ -641,6 +665,7 @@ PlanArgs Engine::plan_args(const Call& c, const FinishPrep& f) {
     pa.row_fail = row_fail_.as<uint32_t>();
     pa.done = done_.as<uint32_t>();
     pa.max_bits = static_cast<uint32_t>(msd_max_bits_);
+    pa.prefetch_mb = static_cast<uint32_t>(prefetch_mb_);
     return pa;
 }
 
@@ -694,6 +719,8 @@ void Engine::launch_finish(Call& c, const FinishPrep& f) {
 
 // stats events: inside a capture they must be external record nodes to be replayed
 void Engine::record(int i, cudaStream_t s) {
+    if (capturing_ && (i == 0 || i == 3)) return;  // recorded around the graph launch instead
+    if (capturing_ && no_graph_events_) return;     // keep kernel->kernel PDL edges unbroken
     check(capturing_ ? cudaEventRecordWithFlags(ev_[i], s, cudaEventRecordExternal) : cudaEventRecord(ev_[i], s),
           "event");
 }

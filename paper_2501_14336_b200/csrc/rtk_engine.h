@@ -65,6 +65,7 @@ public:
 
     // stats of the last call; total_ms is resolved lazily (waits for the call's last event)
     const rtk_stats& last_stats();
+    void set_timing(bool on) { timing_ = on; }
 
     int device() const { return device_; }
     rtk_stats stats{};
@@ -151,6 +152,14 @@ private:
         std::vector<RowReq> rows;
         bool operator==(const CallKey& o) const;
     };
+    struct Upload {
+        uint8_t* d;
+        const uint8_t* h;
+        size_t bytes;
+    };
+    std::vector<Upload> cap_uploads_;
+    cudaStream_t user_s_ = nullptr;
+    uint64_t arena_tag_ = 0;      // bumped by every plan upload (arena content changed)
     struct GraphCache {
         bool valid = false;
         CallKey key;
@@ -163,6 +172,8 @@ private:
         bool has_init = false;
         int clean_rows = 0;
         size_t arena_used = 0, pin_used = 0;
+        std::vector<Upload> uploads;  // plan uploads done outside the graph at capture time
+        uint64_t arena_tag = 0;
         uint64_t group_base = 0, wgroup_base = 0;
     };
     GraphCache graph_;
@@ -175,7 +186,10 @@ private:
     bool needs_init_ = true;      // per-call counters not known to be clean
     bool self_clean_ = false;     // the next main sort launch resets the counters
     bool self_clean_ok_ = true;   // RTK_SELFCLEAN=0 disables
-    bool force_init_ = false;     // RTK_FORCE_INIT=1: init kernel every call (debug)
+    bool force_init_ = false;
+    bool no_graph_events_ = true;   // no stats events inside graphs (RTK_GRAPH_EVENTS=1 keeps them)
+    bool timing_ = false;           // rtk_set_timing: no graph replay, events around k_compact
+    int prefetch_mb_ = 24;          // L2 prefetch budget of k_compact (RTK_PREFETCH_MB)
     int clean_rows_ = 0;
     int clean_upto_ = 0;          // rows whose counters the last call left clean
     bool did_init_ = false;

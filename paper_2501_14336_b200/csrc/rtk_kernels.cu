@@ -257,6 +257,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc in, uint64_t* T) {
+    pdl_trigger();  // k_compact may launch now (it waits for T in griddepcontrol.wait)
     unsigned long long* dbg = sr.dbg;
     int ndbg = 0;
     auto stamp = [&]() {
@@ -442,6 +443,24 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
     uint64_t off = 0, len = 0, coff = 0, ccap = 0, tile0 = 0, tile1 = 0;
     uint32_t lead = 0, r = 0, mine_tiles = 0;
     int cur_j = -1;
+
+    // PDL: this grid may start while k_sample_select still runs. The input does not depend on
+    // it: each CTA pulls its first tiles into L2 with TMA bulk prefetches (<= ~96 MB in total,
+    // inside the 126 MB L2), then waits for the thresholds.
+    if (threadIdx.x < 8) {
+        const uint64_t budget = (static_cast<uint64_t>(pa.prefetch_mb) << 20) / (static_cast<uint64_t>(gridDim.x) * kTile * 4);
+        const uint64_t t = blockIdx.x + threadIdx.x * static_cast<uint64_t>(gridDim.x);
+        if (threadIdx.x < budget && t < ntiles) {
+            const int j0 = row_of_tile(rows, t);
+            const uint64_t sp0 = (t - rows.tile_start[j0]) * kTile;
+            const uint64_t span_len0 = rows.len[j0] + rows.lead[j0];
+            if (sp0 + kTile <= span_len0) {
+                const uint32_t* tp0 = in.base + rows.off[j0] - rows.lead[j0] + sp0;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(tp0), "r"(kTile * 4) : "memory");
+            }
+        }
+    }
+    pdl_wait();
 
     auto warp_flush = [&]() {  // warp-uniform
         if (wcur == 0) return;
@@ -732,7 +751,16 @@ static void compact_km(uint64_t tiles, const Rows& rows, const InputSrc& in, con
                        unsigned long long* count, unsigned long long* kmin, unsigned long long* kmax,
                        const PlanArgs& pa, cudaStream_t s) {
     const int grid = persistent_grid(k_compact<KM>, kThreads, 0, tiles);
-    k_compact<KM><<<grid, kThreads, 0, s>>>(rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_compact<KM>, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa);
 }
 
 void launch_compact(uint64_t tiles, const Rows& rows, const InputSrc& in, const uint64_t* T,

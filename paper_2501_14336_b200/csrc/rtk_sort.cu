@@ -522,6 +522,8 @@ __device__ void msd_plan_slice(const SegSlot& sl, uint32_t* tot, uint32_t slice,
     __syncthreads();
     uint32_t before = off + inc - sum;
     for (int w = 0; w < warp; ++w) before += s_w[w];
+    const bool dbg = a.dbg && blockIdx.x == 0 && tid == 0;
+    if (dbg) a.dbg[10] = msd_timer();
     // classes of the kept buckets -> list positions
     uint32_t nw = 0, nc = 0, nb = 0;
     if (act) {
@@ -558,6 +560,7 @@ __device__ void msd_plan_slice(const SegSlot& sl, uint32_t* tot, uint32_t slice,
         if (tb) atomicOr(a.flags, kFlagMore);
     }
     __syncthreads();
+    if (dbg) a.dbg[11] = msd_timer();
     uint32_t iw = s_base[0] + static_cast<uint32_t>(cpre & 0x1FFFFF);
     uint32_t ic = s_base[1] + static_cast<uint32_t>((cpre >> 21) & 0x1FFFFF);
     uint32_t ib = s_base[2] + static_cast<uint32_t>(cpre >> 42);
@@ -589,6 +592,7 @@ __device__ void msd_plan_slice(const SegSlot& sl, uint32_t* tot, uint32_t slice,
         }
     }
     if (overflow) atomicOr(a.flags, kFlagOverflow);
+    if (dbg) a.dbg[12] = msd_timer();
     __syncthreads();
 }
 
@@ -612,6 +616,7 @@ __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* s
     const uint32_t cid = blockIdx.x / CS;
     const uint32_t Q = fa.Q;
     const uint32_t j = Q > 1 ? 0 : cid, q = Q > 1 ? cid : 0;
+    pdl_trigger();  // k_sort_groups may launch now (it waits in griddepcontrol.wait)
     const SegSlot sl = slots[j];
     if (sl.len == 0) return;  // uniform over the cluster (and over the grid when Q > 1)
     const uint32_t B = 1u << sl.bits, dmask = B - 1;
@@ -657,15 +662,26 @@ __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* s
         // 3: cross-cluster column scan (redundant per cluster: no second barrier)
         grid_barrier(fa.bar, fa.bar_target);
         if (dbg) fa.dbg[2] = msd_timer();
-        for (uint32_t i = threadIdx.x; i < slice; i += kMsdThreads) {
-            uint32_t pre = 0, all = 0;
-            for (uint32_t q2 = 0; q2 < Q; ++q2) {
-                const uint32_t v = __ldcg(fa.ctot + static_cast<uint64_t>(q2) * B + s0 + i);
-                if (q2 < q) pre += v;
-                all += v;
+        // two consecutive buckets per thread, up to 32 clusters' rows loaded before use
+        for (uint32_t i = threadIdx.x * 2; i < slice; i += kMsdThreads * 2) {
+            uint2 pre = make_uint2(0, 0), all = make_uint2(0, 0);
+            for (uint32_t q0 = 0; q0 < Q; q0 += 16) {
+                uint2 v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u)
+                    v[u] = q0 + u < Q ? __ldcg(reinterpret_cast<const uint2*>(fa.ctot + static_cast<uint64_t>(q0 + u) * B + s0 + i))
+                                      : make_uint2(0, 0);
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    if (q0 + u < q) { pre.x += v[u].x; pre.y += v[u].y; }
+                    all.x += v[u].x;
+                    all.y += v[u].y;
+                }
             }
-            qoff[i] = pre;
-            tot[i] = all;
+            qoff[i] = pre.x;
+            qoff[i + 1] = pre.y;
+            tot[i] = all.x;
+            tot[i + 1] = all.y;
         }
     }
     __syncthreads();
@@ -899,6 +915,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned full = 0xffffffffu;
     const unsigned lt = (1u << lane) - 1u;
+    pdl_wait();  // launched early (PDL) while the MSD kernel finishes
     for (;;) {
         if (tid == 0) s_g = atomicAdd(g.work, 1u);
         __syncthreads();
@@ -1133,7 +1150,17 @@ void launch_sort_groups(uint32_t max_groups, const SortArgs& g, cudaStream_t s) 
         configured = true;
     }
     const int grid = persistent_grid(k_sort_groups, kSortThreads, smem, max_groups);
-    k_sort_groups<<<grid, kSortThreads, smem, s>>>(g);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kSortThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_sort_groups, g);
 }
 
 }  // namespace rtk_b200

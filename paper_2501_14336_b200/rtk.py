@@ -198,6 +198,11 @@ def last_stats(device: int = 0) -> Instrumentation:
                            st.kernel_launches, st.compact_ms, st.total_ms)
 
 
+def set_timing(on: bool, device: int = 0) -> None:
+    """Timing mode (rtk_set_timing): no graph replay, CUDA events around k_compact every call."""
+    _raise(L.load().rtk_set_timing(_handle(device), int(bool(on))))
+
+
 def _is_cuda(x) -> bool:
     return hasattr(x, "is_cuda") and bool(x.is_cuda)
 
