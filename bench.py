@@ -184,7 +184,7 @@ def main():
             r = rtk.merge_shards(vals, idx, [kk] * world, [g * n for g in range(world)], kk)
         return r
 
-    def timed(kk, steps, warmup):
+    def python_loop(kk, steps, warmup):
         for _ in range(warmup):
             step(kk)
         torch.cuda.synchronize()
@@ -196,7 +196,16 @@ def main():
             step(kk)
             b.record(stream)
         torch.cuda.synchronize()
-        ms = [a.elapsed_time(b) for a, b in ev]
+        return [a.elapsed_time(b) for a, b in ev]
+
+    def timed(kk, steps, warmup):
+        if world == 1:
+            # steps issued from C through rtk_topk (the drop-in boundary; the reference's call
+            # sites are C++ loops over rtk::topk), CUDA events per step on the stream
+            torch.cuda.synchronize()
+            _, ms = R.bench_topk(x, kk, steps, warmup)
+        else:
+            ms = python_loop(kk, steps, warmup)
         # kernel share: k_compact bracketed by CUDA events on its stream (library timing mode:
         # no graph replay), on separate steps so no stats readback sits inside the timed region
         launches = R.last_stats(local).kernel_launches * steps
@@ -218,6 +227,7 @@ def main():
     with ClockSampler(local) as clk:
         mean_ms, ms, comp, launches = timed(k, args.steps, args.warmup)
     clocks = clk.summary()
+    py_ms = statistics.mean(python_loop(k, max(5, args.steps // 2), 2)) if world == 1 else None
     total_bytes = world * (4 * n) + 12 * k
     value = total_bytes / (mean_ms * 1e-3) / 1e9
 
@@ -331,6 +341,10 @@ def main():
                             "peak_kind": peak_kind, "kernel_ms": comp_ms,
                             "kernel_share_of_step": comp_ms / mean_ms},
                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+               "timing": "steps issued back-to-back from C through rtk_topk (rtk_bench_topk), CUDA events "
+                         "per step on the launching stream; python_loop_ms = the same call through the "
+                         "Python mirror (rtk.topk) with torch events, harness overhead included",
+               "python_loop_ms": py_ms,
                "k_sweep": sweep,
                "adversarial_c4": {"config": "n=2^26 Uniform[128.6,128.7) fp32, k=2^16, largest, scaled_topk "
                                             "tau=0.5 seed=31 (device-resident)", "results": adversarial},

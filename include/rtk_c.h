@@ -111,6 +111,14 @@ int rtk_get_stats(rtk_handle h, rtk_stats* out);
  * (default): repeated identical calls replay one graph with no events inside (kernel-to-kernel
  * programmatic launch edges stay intact); compact_ms is then only set for non-replayed calls. */
 int rtk_set_timing(rtk_handle h, int on);
+
+/* Benchmark helper: `warmup` untimed then `steps` timed back-to-back rtk_topk calls issued from C
+ * (the reference's own call sites are C++ loops over rtk::topk, rtk_cli.cpp:398). The device time
+ * of every step is measured with CUDA events on `stream`; step_ms (nullable) receives `steps`
+ * values, *mean_ms their mean. Same arguments and errors as rtk_topk. */
+int rtk_bench_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, int order,
+                   void* d_out_vals, uint64_t* d_out_idx, void* d_out_pivot, const rtk_cfg* cfg,
+                   void* stream, int warmup, int steps, float* step_ms, float* mean_ms);
 void rtk_cfg_default(rtk_cfg* cfg);
 int rtk_cfg_validate(const rtk_cfg* cfg);
 

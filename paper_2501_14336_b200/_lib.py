@@ -57,6 +57,8 @@ SIGNATURES = {
     "rtk_handle_destroy": (C.c_int, [vp]),
     "rtk_get_stats": (C.c_int, [vp, C.POINTER(rtk_stats)]),
     "rtk_set_timing": (C.c_int, [vp, C.c_int]),
+    "rtk_bench_topk": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, vp, vp, vp, C.POINTER(rtk_cfg), vp,
+                                 C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "rtk_cfg_default": (None, [C.POINTER(rtk_cfg)]),
     "rtk_cfg_validate": (C.c_int, [C.POINTER(rtk_cfg)]),
     "rtk_topk": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, vp, vp, vp, C.POINTER(rtk_cfg), vp]),

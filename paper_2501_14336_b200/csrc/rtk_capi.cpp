@@ -232,6 +232,38 @@ int rtk_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, 
     });
 }
 
+int rtk_bench_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, int order,
+                   void* d_out_vals, uint64_t* d_out_idx, void* d_out_pivot, const rtk_cfg* cfg,
+                   void* stream, int warmup, int steps, float* step_ms, float* mean_ms) {
+    return guarded([&] {
+        if (!h || steps < 1 || warmup < 0) throw Error{RTK_INVALID_ARGUMENT, "bench: bad arguments"};
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        for (int i = 0; i < warmup; ++i) {
+            const int st = rtk_topk(h, d_in, n, k, dtype, order, d_out_vals, d_out_idx, d_out_pivot, cfg, stream);
+            if (st != RTK_OK) throw Error{st, g_last_error};
+        }
+        std::vector<cudaEvent_t> ev(steps + 1);
+        for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        cuda_check(cudaEventRecord(ev[0], s), "event");
+        for (int i = 0; i < steps; ++i) {
+            const int st = rtk_topk(h, d_in, n, k, dtype, order, d_out_vals, d_out_idx, d_out_pivot, cfg, stream);
+            if (st != RTK_OK) throw Error{st, g_last_error};
+            cuda_check(cudaEventRecord(ev[i + 1], s), "event");
+        }
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        double sum = 0;
+        for (int i = 0; i < steps; ++i) {
+            float ms = 0;
+            cuda_check(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]), "elapsed");
+            if (step_ms) step_ms[i] = ms;
+            sum += ms;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        if (mean_ms) *mean_ms = static_cast<float>(sum / steps);
+    });
+}
+
 int rtk_topk_batched(rtk_handle h, const void* d_data, uint64_t data_len, const uint64_t* offsets,
                      const uint64_t* lengths, const uint64_t* ks, uint64_t B, int dtype, int order,
                      void* d_out_vals, uint64_t* d_out_idx, const uint64_t* out_offsets,

@@ -203,6 +203,29 @@ def set_timing(on: bool, device: int = 0) -> None:
     _raise(L.load().rtk_set_timing(_handle(device), int(bool(on))))
 
 
+def bench_topk(x, k: int, steps: int, warmup: int = 3, order: SelectionOrder = SelectionOrder.Largest,
+               cfg: Optional[EngineConfig] = None):
+    """rtk_bench_topk: `steps` back-to-back rtk_topk calls issued from C on x's current stream;
+    returns (mean_ms, [step_ms]) measured with CUDA events (device-resident input)."""
+    import torch
+    cfg = cfg or EngineConfig()
+    lib = L.load()
+    x = x.contiguous()
+    kk = int(k)
+    vals = torch.empty(kk, dtype=x.dtype, device=x.device)
+    idx = torch.empty(kk, dtype=torch.int64, device=x.device)
+    piv = torch.empty(1, dtype=x.dtype, device=x.device)
+    per = (C.c_float * int(steps))()
+    mean = C.c_float()
+    c = cfg._c()
+    st = lib.rtk_bench_topk(_handle(x.device.index or 0), C.c_void_p(x.data_ptr()), x.numel(), kk,
+                            _dtype_code(x), int(order), C.c_void_p(vals.data_ptr()), C.c_void_p(idx.data_ptr()),
+                            C.c_void_p(piv.data_ptr()), C.byref(c), _stream_ptr(x), int(warmup), int(steps),
+                            per, C.byref(mean))
+    _raise(st, "rtk_bench_topk")
+    return float(mean.value), [float(v) for v in per]
+
+
 def _is_cuda(x) -> bool:
     return hasattr(x, "is_cuda") and bool(x.is_cuda)
 
