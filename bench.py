@@ -274,18 +274,9 @@ def main():
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2: flush between steps
         for kb in [int(v) for v in args.batch_ks.split(",") if v]:
             kb = min(kb, V)
-            for _ in range(3):
-                rtk.batch_topk_dense(logits, kb)
-            times = []
-            for _ in range(max(5, args.steps // 2)):
-                flush.zero_()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                rtk.batch_topk_dense(logits, kb)
-                b.record(stream)
-                torch.cuda.synchronize()
-                times.append(a.elapsed_time(b))
-            ms_b = statistics.mean(times)
+            # steps issued from C (rtk_bench_batched), L2 flushed between steps outside the events
+            torch.cuda.synchronize()
+            ms_b, _ = R.bench_batch_dense(logits, kb, max(5, args.steps // 2), 3, flush)
             if world > 1:
                 t = torch.tensor([ms_b], device=dev)
                 torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)

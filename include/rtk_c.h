@@ -119,6 +119,13 @@ int rtk_set_timing(rtk_handle h, int on);
 int rtk_bench_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, int order,
                    void* d_out_vals, uint64_t* d_out_idx, void* d_out_pivot, const rtk_cfg* cfg,
                    void* stream, int warmup, int steps, float* step_ms, float* mean_ms);
+/* Batched counterpart (rtk_topk_batched per step). When flush_bytes > 0, d_flush is overwritten
+ * before every step OUTSIDE the timed events (evicts the inputs from L2). */
+int rtk_bench_batched(rtk_handle h, const void* d_data, uint64_t data_len, const uint64_t* offsets,
+                      const uint64_t* lengths, const uint64_t* ks, uint64_t B, int dtype, int order,
+                      void* d_out_vals, uint64_t* d_out_idx, const uint64_t* out_offsets,
+                      void* d_out_pivots, const rtk_cfg* cfg, void* stream, void* d_flush,
+                      uint64_t flush_bytes, int warmup, int steps, float* step_ms, float* mean_ms);
 void rtk_cfg_default(rtk_cfg* cfg);
 int rtk_cfg_validate(const rtk_cfg* cfg);
 

@@ -57,6 +57,9 @@ SIGNATURES = {
     "rtk_handle_destroy": (C.c_int, [vp]),
     "rtk_get_stats": (C.c_int, [vp, C.POINTER(rtk_stats)]),
     "rtk_set_timing": (C.c_int, [vp, C.c_int]),
+    "rtk_bench_batched": (C.c_int, [vp, vp, u64, P64, P64, P64, u64, C.c_int, C.c_int, vp, vp, P64, vp,
+                                    C.POINTER(rtk_cfg), vp, vp, u64, C.c_int, C.c_int,
+                                    C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "rtk_bench_topk": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, vp, vp, vp, C.POINTER(rtk_cfg), vp,
                                  C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "rtk_cfg_default": (None, [C.POINTER(rtk_cfg)]),

@@ -264,6 +264,41 @@ int rtk_bench_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int d
     });
 }
 
+int rtk_bench_batched(rtk_handle h, const void* d_data, uint64_t data_len, const uint64_t* offsets,
+                      const uint64_t* lengths, const uint64_t* ks, uint64_t B, int dtype, int order,
+                      void* d_out_vals, uint64_t* d_out_idx, const uint64_t* out_offsets,
+                      void* d_out_pivots, const rtk_cfg* cfg, void* stream, void* d_flush,
+                      uint64_t flush_bytes, int warmup, int steps, float* step_ms, float* mean_ms) {
+    return guarded([&] {
+        if (!h || steps < 1 || warmup < 0) throw Error{RTK_INVALID_ARGUMENT, "bench: bad arguments"};
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto one = [&] {
+            const int st = rtk_topk_batched(h, d_data, data_len, offsets, lengths, ks, B, dtype, order, d_out_vals,
+                                            d_out_idx, out_offsets, d_out_pivots, cfg, nullptr, stream);
+            if (st != RTK_OK) throw Error{st, g_last_error};
+        };
+        for (int i = 0; i < warmup; ++i) one();
+        std::vector<cudaEvent_t> ev(2 * steps);
+        for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
+        for (int i = 0; i < steps; ++i) {
+            if (d_flush && flush_bytes) cuda_check(cudaMemsetAsync(d_flush, i & 0xff, flush_bytes, s), "flush");
+            cuda_check(cudaEventRecord(ev[2 * i], s), "event");
+            one();
+            cuda_check(cudaEventRecord(ev[2 * i + 1], s), "event");
+        }
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        double sum = 0;
+        for (int i = 0; i < steps; ++i) {
+            float ms = 0;
+            cuda_check(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]), "elapsed");
+            if (step_ms) step_ms[i] = ms;
+            sum += ms;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        if (mean_ms) *mean_ms = static_cast<float>(sum / steps);
+    });
+}
+
 int rtk_topk_batched(rtk_handle h, const void* d_data, uint64_t data_len, const uint64_t* offsets,
                      const uint64_t* lengths, const uint64_t* ks, uint64_t B, int dtype, int order,
                      void* d_out_vals, uint64_t* d_out_idx, const uint64_t* out_offsets,

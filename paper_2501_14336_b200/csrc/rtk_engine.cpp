@@ -536,13 +536,26 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
         if (frow[v].empty()) continue;
         RowsFusedArgs fa{at<uint32_t>(D, o_f[v][0]), at<uint64_t>(D, o_f[v][1]), at<uint64_t>(D, o_f[v][2]),
                          at<uint64_t>(D, o_f[v][3]), src, c.d_row_out, d_vals, d_idx, d_pivots,
-                         row_fail_.as<uint32_t>(), ctl_.as<uint32_t>(), nullptr};
+                         row_fail_.as<uint32_t>(), ctl_.as<uint32_t>(), nullptr, CallTail{}};
         if (profile_) {
             dbg_.ensure(4096);
             fa.dbg = dbg_.as<unsigned long long>();
         }
+        // the call's last kernel (no general rows, last fused variant): completion signal + clean
+        const bool last = grow.empty() && (v == 1 || frow[1].empty());
+        if (last && !count_stats_) {
+            fa.tail = tail_args();
+            if (self_clean_) {
+                set_clean(fa.tail, R);
+                clean_rows_ = R;
+            }
+        }
         launch_rows_fused(static_cast<int>(frow[v].size()), fa, v == 1, s);
         ++stats.kernel_launches;
+        if (fa.tail.hflags) {
+            ++expected_seq_;
+            sig_pending_ = true;
+        }
         mark("rows_fused", s);
     }
     record(1, s);
@@ -704,13 +717,7 @@ void Engine::launch_finish(Call& c, const FinishPrep& f) {
     }
     SortArgs sa = sort_args(c, f.gl);
     if (self_clean_) {
-        sa.R_clean = c.R;
-        sa.c_count = count_.as<unsigned long long>();
-        sa.c_kmin = kmin_.as<unsigned long long>();
-        sa.c_kmax = kmax_.as<unsigned long long>();
-        sa.c_T = T_.as<uint64_t>();
-        sa.c_done = done_.as<uint32_t>();
-        sa.c_ticket = seg_ticket_.as<uint32_t>();
+        set_clean(sa.tail, c.R);
         clean_rows_ = c.R;
     }
     launch_sort(static_cast<uint32_t>(f.max_groups + f.max_wgroups / 8 + 1), sa, c.s);
@@ -749,12 +756,28 @@ void Engine::wait_signal(cudaStream_t s) {
     }
 }
 
+CallTail Engine::tail_args() {
+    CallTail t{};
+    t.ctl = ctl_.as<uint32_t>();
+    t.done_ctr = sig_.as<uint32_t>();
+    t.seq_ctr = sig_.as<uint32_t>() + 1;
+    t.hflags = d_hmap_;
+    return t;
+}
+
+void Engine::set_clean(CallTail& t, int R) {
+    t.R_clean = R;
+    t.c_count = count_.as<unsigned long long>();
+    t.c_kmin = kmin_.as<unsigned long long>();
+    t.c_kmax = kmax_.as<unsigned long long>();
+    t.c_T = T_.as<uint64_t>();
+    t.c_done = done_.as<uint32_t>();
+    t.c_ticket = seg_ticket_.as<uint32_t>();
+}
+
 SortArgs Engine::sort_args(const Call& c, const GroupList& gl) {
     SortArgs a{};
-    a.ctl = ctl_.as<uint32_t>();
-    a.done_ctr = sig_.as<uint32_t>();
-    a.seq_ctr = sig_.as<uint32_t>() + 1;
-    a.hflags = d_hmap_;
+    a.tail = tail_args();
     a.groups = gl;
     a.work = ctl_.as<uint32_t>() + 2;
     a.wgroups = GroupList{wgroups_.as<SortGroup>(), ctl_.as<uint32_t>() + 5, wgroup_cap_};

@@ -135,6 +135,8 @@ private:
     void drain(Call& c, uint32_t (&ctl)[8]);
     SortArgs sort_args(const Call& c, const GroupList& gl);
     void launch_sort(uint32_t max_groups, const SortArgs& a, cudaStream_t s);
+    CallTail tail_args();
+    void set_clean(CallTail& t, int R);
     void wait_signal(cudaStream_t s);
     void record(int i, cudaStream_t s);
     void enqueue(const uint32_t* d_base, int dtype, int smallest, bool scaled, float a_s, bool gather,

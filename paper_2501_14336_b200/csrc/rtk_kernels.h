@@ -24,6 +24,59 @@ struct SampleRows {       // rows whose threshold comes from a stratified sample
     unsigned long long* dbg; // optional phase timestamps (RTK_PROFILE)
 };
 
+// End-of-call tail of the LAST kernel of a call (k_sort_groups, or k_rows_fused when a batch
+// has only short rows): the last CTA to finish copies the control words ctl[0..7] to mapped
+// host memory and then writes a per-launch sequence number to hflags[15] (the host spins on it:
+// no memcpy, no stream sync); with R_clean > 0 it also resets the per-call counters of R_clean
+// state rows and the control words, so the next call needs no init kernel.
+struct CallTail {
+    const uint32_t* ctl;
+    uint32_t* done_ctr;
+    uint32_t* seq_ctr;
+    volatile uint32_t* hflags;   // null: no tail
+    int R_clean;
+    unsigned long long* c_count;
+    unsigned long long* c_kmin;
+    unsigned long long* c_kmax;
+    uint64_t* c_T;
+    uint32_t* c_done;
+    uint32_t* c_ticket;
+};
+
+#ifdef __CUDACC__
+// all threads of every CTA call this at the very end; s_flag is one shared word
+__device__ __forceinline__ void call_tail(const CallTail& t, uint32_t* s_flag) {
+    if (!t.hflags) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        *s_flag = 0;
+        if (atomicAdd(t.done_ctr, 1u) == gridDim.x - 1) {
+            __threadfence();
+            *t.done_ctr = 0;
+            const uint32_t seq = atomicAdd(t.seq_ctr, 1u) + 1;
+            const volatile uint32_t* c = t.ctl;
+            for (int i = 0; i < 8; ++i) t.hflags[i] = c[i];
+            __threadfence_system();
+            t.hflags[15] = seq;
+            *s_flag = 1;
+        }
+    }
+    __syncthreads();
+    if (*s_flag && t.R_clean > 0) {
+        for (int r = threadIdx.x; r < t.R_clean; r += blockDim.x) {
+            t.c_count[r] = 0;
+            t.c_kmin[r] = ~0ull;
+            t.c_kmax[r] = 0;
+            t.c_T[r] = 0;
+            t.c_done[r] = 0;
+            t.c_ticket[r] = 0;
+        }
+        if (threadIdx.x < 16) const_cast<uint32_t*>(t.ctl)[threadIdx.x] = 0;
+    }
+}
+#endif
+
 struct RowsFusedArgs {    // K6 fast path: one CTA per short row (rtk_rows.cu)
     const uint32_t* rid;
     const uint64_t* off;
@@ -37,6 +90,7 @@ struct RowsFusedArgs {    // K6 fast path: one CTA per short row (rtk_rows.cu)
     uint32_t* row_fail;
     uint32_t* flags;
     unsigned long long* dbg;      // optional phase timestamps (RTK_PROFILE)
+    CallTail tail;                // set when this is the call's last kernel
 };
 
 struct SortGroup {
@@ -151,21 +205,7 @@ struct SortArgs {
     int gather;
     int dtype;
     int smallest;
-    // completion signal: the last CTA copies ctl[0..7] to mapped host memory and then writes
-    // a per-launch sequence number to hflags[15] (the host spins on it: no memcpy, no sync)
-    const uint32_t* ctl;
-    uint32_t* done_ctr;
-    uint32_t* seq_ctr;
-    volatile uint32_t* hflags;
-    // self-cleaning (R_clean > 0): after publishing, the last CTA resets the per-call counters
-    // of R_clean state rows and the control words, so the next call needs no init kernel
-    int R_clean;
-    unsigned long long* c_count;
-    unsigned long long* c_kmin;
-    unsigned long long* c_kmax;
-    uint64_t* c_T;
-    uint32_t* c_done;
-    uint32_t* c_ticket;
+    CallTail tail;           // completion signal + self-cleaning (see CallTail)
 };
 
 inline int num_sms() {

@@ -169,7 +169,17 @@ __device__ void cta_bitonic_desc(unsigned long long* buf, int n2) {
 }
 
 template <int KM, int CAND, int STAGES, int SAMPLE>
+__device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a);
+
+template <int KM, int CAND, int STAGES, int SAMPLE>
 __global__ void __launch_bounds__(kRowThreads, 2) k_rows_fused(RowsFusedArgs a) {
+    __shared__ uint32_t s_tail;
+    rows_fused_body<KM, CAND, STAGES, SAMPLE>(a);
+    call_tail(a.tail, &s_tail);  // only when this is the call's last kernel
+}
+
+template <int KM, int CAND, int STAGES, int SAMPLE>
+__device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     constexpr int kRowCand = CAND;
     constexpr int kRowStages = STAGES;
     constexpr int kRowSample = SAMPLE;

@@ -1022,36 +1022,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
         else if (grp.len <= 128) warp_sort_group<4>(grp, g, lane);
         else warp_sort_group<8>(grp, g, lane);
     }
-    if (g.hflags) {
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            if (atomicAdd(g.done_ctr, 1u) == gridDim.x - 1) {
-                __threadfence();
-                *g.done_ctr = 0;
-                const uint32_t seq = atomicAdd(g.seq_ctr, 1u) + 1;
-                const volatile uint32_t* c = g.ctl;
-                for (int i = 0; i < 8; ++i) g.hflags[i] = c[i];
-                __threadfence_system();
-                g.hflags[15] = seq;
-                s_g = 1;
-            } else {
-                s_g = 0;
-            }
-        }
-        __syncthreads();
-        if (s_g && g.R_clean > 0) {  // the last CTA: reset the call's counters for the next call
-            for (int r = tid; r < g.R_clean; r += kSortThreads) {
-                g.c_count[r] = 0;
-                g.c_kmin[r] = ~0ull;
-                g.c_kmax[r] = 0;
-                g.c_T[r] = 0;
-                g.c_done[r] = 0;
-                g.c_ticket[r] = 0;
-            }
-            if (tid < 16) const_cast<uint32_t*>(g.ctl)[tid] = 0;
-        }
-    }
+    call_tail(g.tail, &s_g);
 }
 
 // ---- launchers ----------------------------------------------------------------------------

@@ -226,6 +226,36 @@ def bench_topk(x, k: int, steps: int, warmup: int = 3, order: SelectionOrder = S
     return float(mean.value), [float(v) for v in per]
 
 
+def bench_batch_dense(x, k: int, steps: int, warmup: int = 3, flush=None,
+                      order: SelectionOrder = SelectionOrder.Largest, cfg: Optional[EngineConfig] = None):
+    """rtk_bench_batched over a dense [B, V] CUDA tensor: `steps` rtk_topk_batched calls issued
+    from C, CUDA events per step; `flush` (a CUDA byte tensor) is overwritten between steps
+    outside the timed events. Returns (mean_ms, [step_ms])."""
+    import torch
+    cfg = cfg or EngineConfig()
+    lib = L.load()
+    x = x.contiguous()
+    B, V = x.shape
+    offs, p_off = _arr64(np.arange(B, dtype=np.uint64) * V)
+    lens, p_len = _arr64(np.full(B, V, dtype=np.uint64))
+    kks, p_ks = _arr64(np.full(B, k, dtype=np.uint64))
+    oo, p_oo = _arr64(np.arange(B, dtype=np.uint64) * k)
+    vals = torch.empty((B, k), dtype=x.dtype, device=x.device)
+    idx = torch.empty((B, k), dtype=torch.int64, device=x.device)
+    piv = torch.empty(B, dtype=x.dtype, device=x.device)
+    per = (C.c_float * int(steps))()
+    mean = C.c_float()
+    c = cfg._c()
+    st = lib.rtk_bench_batched(_handle(x.device.index or 0), C.c_void_p(x.data_ptr()), x.numel(), p_off, p_len,
+                               p_ks, B, _dtype_code(x), int(order), C.c_void_p(vals.data_ptr()),
+                               C.c_void_p(idx.data_ptr()), p_oo, C.c_void_p(piv.data_ptr()), C.byref(c),
+                               _stream_ptr(x), C.c_void_p(flush.data_ptr() if flush is not None else 0),
+                               int(flush.numel() if flush is not None else 0), int(warmup), int(steps),
+                               per, C.byref(mean))
+    _raise(st, "rtk_bench_batched")
+    return float(mean.value), [float(v) for v in per]
+
+
 def _is_cuda(x) -> bool:
     return hasattr(x, "is_cuda") and bool(x.is_cuda)
 
