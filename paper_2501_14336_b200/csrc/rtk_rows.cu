@@ -107,7 +107,16 @@ __device__ unsigned long long cta_radix_select(const unsigned long long* buf, ui
         for (uint32_t i = tid; i < ((m + 31) & ~31u); i += kRowThreads) {
             const bool in = i < m;
             const unsigned long long K = in ? buf[i] : 0ull;
-            hist_add(hist, static_cast<uint32_t>(K >> pos) & dmask, in && (hi >= 64 || (K >> hi) == pm));
+            // plain shared atomics (+ a whole-warp fast path for tie-heavy rows): __match_any_sync
+            // costs more than the conflicts it saves on these mostly spread digits
+            const bool v = in && (hi >= 64 || (K >> hi) == pm);
+            const uint32_t d = static_cast<uint32_t>(K >> pos) & dmask;
+            const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+            if (__all_sync(0xffffffffu, v && d == d0)) {
+                if ((threadIdx.x & 31) == 0) atomicAdd(&hist[d0], 32u);
+            } else if (v) {
+                atomicAdd(&hist[d], 1u);
+            }
         }
         __syncthreads();
         uint32_t c[per], sum = 0;
