@@ -226,6 +226,18 @@ __device__ __forceinline__ void load_u64_tile(const uint64_t* ptr, uint64_t span
     }
 }
 
+// Lanes of the (full) warp whose 8-bit digit equals this lane's: the ballot multisplit (one
+// ballot per digit bit, AND of the matching masks) — cheaper than __match_any_sync.
+__device__ __forceinline__ unsigned warp_peers8(uint32_t d) {
+    unsigned m = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        m &= ((d >> b) & 1u) ? bal : ~bal;
+    }
+    return m;
+}
+
 // smem histogram increment with a whole-warp fast path: adversarial inputs put every
 // element of a warp into one bin (engine_test.cpp:45-56, C4), which would otherwise
 // serialise 32 same-address shared atomics.

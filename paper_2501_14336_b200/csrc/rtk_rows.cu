@@ -456,7 +456,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
         for (int q = 0; q < IT; ++q) {
             const uint32_t p = warp * 256 + q * 32 + lane;
             dig[q] = p < kk ? 255u - static_cast<uint32_t>((key[q] >> lo) & 0xFFu) : 255u;
-            const unsigned peers = __match_any_sync(full, dig[q]);
+            const unsigned peers = warp_peers8(dig[q]);
             const uint32_t b0 = cnt[warp][dig[q]];
             rk[q] = b0 + __popc(peers & lt);
             __syncwarp();
