@@ -53,6 +53,11 @@ extern "C" {
 /* dtypes (io.hpp:19 codes 0/1) and selection order (keycodec.hpp:19) */
 #define RTK_F32 0
 #define RTK_U32 1
+/* 16-bit floats (io.hpp:3 declares dtype code 2 = f16; the reference build rejects it, io.cpp:71-72).
+ * Order and tie rule as for f32 (the same sign-flip KeyCodec on 16 bits); values come back as
+ * 16-bit words. The result equals rtk::topk on the exactly widened f32 input. */
+#define RTK_F16 2
+#define RTK_BF16 3
 #define RTK_LARGEST 0
 #define RTK_SMALLEST 1
 

@@ -64,6 +64,10 @@ void validate_cfg(const rtk_cfg& c) {
         throw Error{RTK_INVALID_ARGUMENT, "pack_size must be a power of two >= element width"};
 }
 
+bool dtype_ok(int d) { return d == RTK_F32 || d == RTK_U32 || d == RTK_F16 || d == RTK_BF16; }
+int eng_dtype(int d) { return d == RTK_BF16 ? rtk_b200::kF16 : d; }  // f16 and bf16 share the map
+size_t esize(int d) { return (d == RTK_F16 || d == RTK_BF16) ? 2 : 4; }
+
 void check_common(const void* ptr, uint64_t n, uint64_t k, int dtype, int order, const rtk_cfg& cfg,
                   const char* who) {
     // topk: empty -> empty_input_error, k outside [1,n] -> rank_out_of_range (engine.hpp:425-426);
@@ -71,7 +75,7 @@ void check_common(const void* ptr, uint64_t n, uint64_t k, int dtype, int order,
     if (n == 0) throw Error{RTK_EMPTY_INPUT, std::string(who) + ": empty input"};
     if (k == 0 || k > n) throw Error{RTK_RANK_OUT_OF_RANGE, std::string(who) + ": k outside [1, n]"};
     validate_cfg(cfg);
-    if (dtype != RTK_F32 && dtype != RTK_U32) throw Error{RTK_INVALID_ARGUMENT, "dtype must be F32 or U32"};
+    if (!dtype_ok(dtype)) throw Error{RTK_INVALID_ARGUMENT, "dtype must be F32, U32, F16 or BF16"};
     if (order != RTK_LARGEST && order != RTK_SMALLEST) throw Error{RTK_INVALID_ARGUMENT, "bad order"};
     if (n > (uint64_t(1) << 32)) throw Error{RTK_INVALID_ARGUMENT, "n > 2^32 per device row is not supported"};
     if (!ptr) throw Error{RTK_INVALID_ARGUMENT, "null input"};
@@ -226,7 +230,7 @@ int rtk_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, 
         if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
         const rtk_cfg c = cfg ? *cfg : default_cfg();
         check_common(d_in, n, k, dtype, order, c, "topk");
-        h->engine.run(static_cast<const uint32_t*>(d_in), dtype, order, false, 0.0f, false,
+        h->engine.run(static_cast<const uint32_t*>(d_in), eng_dtype(dtype), order, false, 0.0f, false,
                       {RowReq{0, n, k, 0}}, static_cast<uint32_t*>(d_out_vals), d_out_idx,
                       static_cast<uint32_t*>(d_out_pivot), static_cast<cudaStream_t>(stream));
     });
@@ -310,14 +314,14 @@ int rtk_topk_batched(rtk_handle h, const void* d_data, uint64_t data_len, const 
         validate_batch(data_len, offsets, lengths, ks, B);
         const rtk_cfg c = cfg ? *cfg : default_cfg();
         validate_cfg(c);
-        if (dtype != RTK_F32 && dtype != RTK_U32) throw Error{RTK_INVALID_ARGUMENT, "dtype must be F32 or U32"};
+        if (!dtype_ok(dtype)) throw Error{RTK_INVALID_ARGUMENT, "dtype must be F32, U32, F16 or BF16"};
         if (order != RTK_LARGEST && order != RTK_SMALLEST) throw Error{RTK_INVALID_ARGUMENT, "bad order"};
         if (!d_data) throw Error{RTK_INVALID_ARGUMENT, "null input"};
         std::vector<uint64_t> oo = out_offsets ? std::vector<uint64_t>(out_offsets, out_offsets + B)
                                                : packed_out_offsets(ks, B);
         std::vector<RowReq> rows(B);
         for (uint64_t t = 0; t < B; ++t) rows[t] = RowReq{offsets[t], lengths[t], ks[t], oo[t]};
-        h->engine.run(static_cast<const uint32_t*>(d_data), dtype, order, false, 0.0f, false, rows,
+        h->engine.run(static_cast<const uint32_t*>(d_data), eng_dtype(dtype), order, false, 0.0f, false, rows,
                       static_cast<uint32_t*>(d_out_vals), d_out_idx, static_cast<uint32_t*>(d_out_pivots),
                       static_cast<cudaStream_t>(stream));
     });
@@ -347,17 +351,17 @@ int rtk_topk_host(rtk_handle h, const void* in, uint64_t n, uint64_t k, int dtyp
         check_common(in, n, k, dtype, order, c, "topk");
         Engine& e = h->engine;
         cuda_check(cudaSetDevice(e.device()), "cudaSetDevice");
-        e.io_in.ensure(4 * n);
-        e.io_vals.ensure(4 * k);
+        e.io_in.ensure(esize(dtype) * n);
+        e.io_vals.ensure(esize(dtype) * k);
         e.io_idx.ensure(8 * k);
         e.io_piv.ensure(4);
         cudaStream_t s = nullptr;
-        cuda_check(cudaMemcpyAsync(e.io_in.p, in, 4 * n, cudaMemcpyHostToDevice, s), "h2d");
-        e.run(e.io_in.as<uint32_t>(), dtype, order, false, 0.0f, false, {RowReq{0, n, k, 0}},
+        cuda_check(cudaMemcpyAsync(e.io_in.p, in, esize(dtype) * n, cudaMemcpyHostToDevice, s), "h2d");
+        e.run(e.io_in.as<uint32_t>(), eng_dtype(dtype), order, false, 0.0f, false, {RowReq{0, n, k, 0}},
               e.io_vals.as<uint32_t>(), e.io_idx.as<uint64_t>(), e.io_piv.as<uint32_t>(), s);
-        cuda_check(cudaMemcpyAsync(out_vals, e.io_vals.p, 4 * k, cudaMemcpyDeviceToHost, s), "d2h");
+        cuda_check(cudaMemcpyAsync(out_vals, e.io_vals.p, esize(dtype) * k, cudaMemcpyDeviceToHost, s), "d2h");
         cuda_check(cudaMemcpyAsync(out_idx, e.io_idx.p, 8 * k, cudaMemcpyDeviceToHost, s), "d2h");
-        if (out_pivot) cuda_check(cudaMemcpyAsync(out_pivot, e.io_piv.p, 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (out_pivot) cuda_check(cudaMemcpyAsync(out_pivot, e.io_piv.p, esize(dtype), cudaMemcpyDeviceToHost, s), "d2h");
         cuda_check(cudaStreamSynchronize(s), "sync");
     });
 }
@@ -375,12 +379,12 @@ int rtk_topk_batched_host(rtk_handle h, const void* data, uint64_t data_len, con
         for (uint64_t t = 0; t < B; ++t) out_total = std::max(out_total, oo[t] + ks[t]);
         Engine& e = h->engine;
         cuda_check(cudaSetDevice(e.device()), "cudaSetDevice");
-        e.io_in.ensure(4 * std::max<uint64_t>(data_len, 1));
-        e.io_vals.ensure(4 * out_total);
+        e.io_in.ensure(esize(dtype) * std::max<uint64_t>(data_len, 1));
+        e.io_vals.ensure(esize(dtype) * out_total);
         e.io_idx.ensure(8 * out_total);
-        e.io_piv.ensure(4 * B);
+        e.io_piv.ensure(esize(dtype) * B);
         cudaStream_t s = nullptr;
-        cuda_check(cudaMemcpyAsync(e.io_in.p, data, 4 * data_len, cudaMemcpyHostToDevice, s), "h2d");
+        cuda_check(cudaMemcpyAsync(e.io_in.p, data, esize(dtype) * data_len, cudaMemcpyHostToDevice, s), "h2d");
         int st = rtk_topk_batched(h, e.io_in.p, data_len, offsets, lengths, ks, B, dtype, order, e.io_vals.p,
                                   e.io_idx.as<uint64_t>(), oo.data(), e.io_piv.p, cfg, opts, s);
         if (st != RTK_OK) throw Error{st, g_last_error};
@@ -388,19 +392,19 @@ int rtk_topk_batched_host(rtk_handle h, const void* data, uint64_t data_len, con
         bool packed = true;
         for (uint64_t t = 0, acc = 0; t < B; acc += ks[t], ++t) packed &= oo[t] == acc;
         if (packed) {
-            cuda_check(cudaMemcpyAsync(out_vals, e.io_vals.p, 4 * out_total, cudaMemcpyDeviceToHost, s), "d2h");
+            cuda_check(cudaMemcpyAsync(out_vals, e.io_vals.p, esize(dtype) * out_total, cudaMemcpyDeviceToHost, s), "d2h");
             cuda_check(cudaMemcpyAsync(out_idx, e.io_idx.p, 8 * out_total, cudaMemcpyDeviceToHost, s), "d2h");
         } else {
             for (uint64_t t = 0; t < B; ++t) {
-                cuda_check(cudaMemcpyAsync(static_cast<uint32_t*>(out_vals) + oo[t],
-                                           e.io_vals.as<uint32_t>() + oo[t], 4 * ks[t],
+                cuda_check(cudaMemcpyAsync(static_cast<char*>(out_vals) + esize(dtype) * oo[t],
+                                           e.io_vals.as<char>() + esize(dtype) * oo[t], esize(dtype) * ks[t],
                                            cudaMemcpyDeviceToHost, s), "d2h");
                 cuda_check(cudaMemcpyAsync(out_idx + oo[t], e.io_idx.as<uint64_t>() + oo[t], 8 * ks[t],
                                            cudaMemcpyDeviceToHost, s), "d2h");
             }
         }
         if (out_pivots)
-            cuda_check(cudaMemcpyAsync(out_pivots, e.io_piv.p, 4 * B, cudaMemcpyDeviceToHost, s), "d2h");
+            cuda_check(cudaMemcpyAsync(out_pivots, e.io_piv.p, esize(dtype) * B, cudaMemcpyDeviceToHost, s), "d2h");
         cuda_check(cudaStreamSynchronize(s), "sync");
     });
 }
@@ -450,7 +454,7 @@ int rtk_merge_shards(rtk_handle h, const void* d_cand_vals, const uint64_t* d_ca
         // Tie-break surrogate = position in the concatenation: each block is in (key desc,
         // index asc) order and blocks are in ascending index order, so among equal keys
         // position order == global index order.
-        h->engine.run(static_cast<const uint32_t*>(d_cand_vals), dtype, order, false, 0.0f, false,
+        h->engine.run(static_cast<const uint32_t*>(d_cand_vals), eng_dtype(dtype), order, false, 0.0f, false,
                       {RowReq{0, total, k, 0}}, static_cast<uint32_t*>(d_out_vals), d_out_idx,
                       static_cast<uint32_t*>(d_out_pivot), s);
         h->engine.remap(k, d_cand_idx, start, base, d_out_idx, s);

@@ -22,7 +22,12 @@ constexpr int kDigit = 11;             // radix digit width for the 64-bit compo
 constexpr int kBins = 1 << kDigit;
 constexpr int kStageCap = 4096;        // compaction staging buffer (u64), 32 KB smem
 
-enum : int { kF32 = 0, kU32 = 1 };
+// kF16: any 16-bit IEEE-style float (f16 or bf16 — the order-preserving map is the same bit
+// manipulation); its 16-bit key sits in the HIGH half of the 32-bit key, so every selection /
+// ordering stage works on the same 32-bit keys and 64-bit composites as for f32.
+enum : int { kF32 = 0, kU32 = 1, kF16 = 2 };
+
+__host__ __device__ __forceinline__ int elem_bytes(int dtype) { return dtype == kF16 ? 2 : 4; }
 
 // Selection state of one row (one query, one sample, or one MSD segment).
 // Digits are examined MSD-first at bit positions 53, 42, 31, 20, 9, 0 of K.
@@ -69,7 +74,33 @@ __device__ __forceinline__ uint32_t decode_f32_bits(uint32_t bits, bool smallest
     return (bits & 0x80000000u) ? (bits ^ 0x80000000u) : ~bits;
 }
 
+// KeyCodec for 16-bit floats (the f32 map, keycodec.hpp:57-62, on 16 bits), placed in the high half
+__device__ __forceinline__ uint32_t encode_f16_key(uint32_t raw16, bool smallest) {
+    uint32_t bits = (raw16 & 0x8000u) ? (~raw16 & 0xFFFFu) : (raw16 | 0x8000u);
+    if (smallest) bits = ~bits & 0xFFFFu;
+    return bits << 16;
+}
+
+__device__ __forceinline__ uint32_t decode_f16_bits(uint32_t key, bool smallest) {
+    uint32_t bits = key >> 16;
+    if (smallest) bits = ~bits & 0xFFFFu;
+    return (bits & 0x8000u) ? (bits ^ 0x8000u) : (~bits & 0xFFFFu);
+}
+
+// output value (16-bit dtypes write 16-bit words)
+__device__ __forceinline__ void store_val(uint32_t* out, int dtype, uint64_t i, uint32_t v) {
+    if (dtype == kF16) reinterpret_cast<unsigned short*>(out)[i] = static_cast<unsigned short>(v);
+    else out[i] = v;
+}
+
+// element i of an input row (runtime element size; the hot kernels use compile-time paths)
+__device__ __forceinline__ uint32_t load_elem(const InputSrc& s, uint64_t i) {
+    if (s.dtype == kF16) return __ldg(reinterpret_cast<const unsigned short*>(s.base) + i);
+    return __ldg(s.base + i);
+}
+
 __device__ __forceinline__ uint32_t make_key(const InputSrc& s, uint32_t raw) {
+    if (s.dtype == kF16) return encode_f16_key(raw, s.smallest);
     if (s.dtype == kF32) {
         if (s.scaled) {
             // y = x - a_s in IEEE fp32 round-to-nearest, denormals kept (scaling.hpp:69-70);
@@ -82,15 +113,26 @@ __device__ __forceinline__ uint32_t make_key(const InputSrc& s, uint32_t raw) {
 }
 
 // Compile-time key transforms for the streaming kernels (KM = key mode).
-enum : int { kKmF32L = 0, kKmF32S = 1, kKmF32LScaled = 2, kKmF32SScaled = 3, kKmU32L = 4, kKmU32S = 5 };
+enum : int { kKmF32L = 0, kKmF32S = 1, kKmF32LScaled = 2, kKmF32SScaled = 3, kKmU32L = 4, kKmU32S = 5,
+             kKmF16L = 6, kKmF16S = 7 };
 
 inline int key_mode(int dtype, int smallest, int scaled) {
+    if (dtype == kF16) return smallest ? kKmF16S : kKmF16L;
     if (dtype != kF32) return smallest ? kKmU32S : kKmU32L;
     return (scaled ? 2 : 0) + (smallest ? 1 : 0);
 }
 
 template <int KM>
+__host__ __device__ constexpr bool km_is16() { return KM == kKmF16L || KM == kKmF16S; }
+
+template <int KM>
 __device__ __forceinline__ uint32_t key_of(uint32_t raw, float a_s) {
+    if (KM == kKmF16L || KM == kKmF16S) {
+        // raw = zero-extended 16-bit word; sign-flip map as mask arithmetic, key in the high half
+        const uint32_t m = ((raw & 0x8000u) ? 0xFFFFu : 0x8000u);
+        const uint32_t bits = (raw ^ m) << 16;
+        return KM == kKmF16S ? ~bits & 0xFFFF0000u : bits;
+    }
     if (KM == kKmU32L) return raw;
     if (KM == kKmU32S) return ~raw;
     if (KM == kKmF32LScaled || KM == kKmF32SScaled)
@@ -190,6 +232,25 @@ __device__ __forceinline__ void load_input_tile(const uint32_t* row_ptr, uint64_
     }
 }
 
+// load_input_tile for any element size (rare paths: exact radix passes, trigger histogram)
+__device__ __forceinline__ void load_input_tile_any(const InputSrc& in, uint64_t row_off, uint64_t span_len,
+                                                    uint32_t lead, uint64_t span0, uint32_t (&v)[kUnroll][kVec]) {
+    if (in.dtype != kF16) {
+        load_input_tile(in.base + row_off - lead, span_len, lead, span0, v);
+        return;
+    }
+    const unsigned short* rp = reinterpret_cast<const unsigned short*>(in.base) + row_off - lead;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+        const uint64_t p = span0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec;
+#pragma unroll
+        for (int i = 0; i < kVec; ++i) {
+            const uint64_t q = p + i;
+            v[u][i] = (q >= lead && q < span_len) ? static_cast<uint32_t>(__ldg(rp + q)) : 0u;
+        }
+    }
+}
+
 // u64 tiles use the same span convention: ptr is 32-byte aligned, element e of the row sits
 // at span position e + lead (lead = row start's offset inside its 32-byte sector).
 // Same as load_input_tile, but addressed from the tile's own (32-byte aligned) start with the
@@ -205,6 +266,29 @@ __device__ __forceinline__ void load_tile_local(const uint32_t* tile_ptr, uint32
 #pragma unroll
             for (int i = 0; i < kVec; ++i)
                 v[u][i] = (l + i >= vlo && l + i < vhi) ? __ldg(tile_ptr + l + i) : 0u;
+        }
+    }
+}
+
+// 16-bit elements: the same (u, tid, i) layout, 8 halves = one 16-byte load per (u, tid)
+__device__ __forceinline__ void load_tile_local16(const unsigned short* tile_ptr, uint32_t vlo, uint32_t vhi,
+                                                  uint32_t (&v)[kUnroll][kVec]) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t l = (u * kThreads + threadIdx.x) * kVec;
+        if (l >= vlo && l + kVec <= vhi) {
+            uint32_t w0, w1, w2, w3;
+            asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                         : "l"(tile_ptr + l));
+            v[u][0] = w0 & 0xFFFFu; v[u][1] = w0 >> 16;
+            v[u][2] = w1 & 0xFFFFu; v[u][3] = w1 >> 16;
+            v[u][4] = w2 & 0xFFFFu; v[u][5] = w2 >> 16;
+            v[u][6] = w3 & 0xFFFFu; v[u][7] = w3 >> 16;
+        } else {
+#pragma unroll
+            for (int i = 0; i < kVec; ++i)
+                v[u][i] = (l + i >= vlo && l + i < vhi) ? static_cast<uint32_t>(__ldg(tile_ptr + l + i)) : 0u;
         }
     }
 }

@@ -80,6 +80,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_FORCE_INIT")) force_init_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_GRAPH_EVENTS")) no_graph_events_ = *g == '0';
     if (const char* g = std::getenv("RTK_PREFETCH_MB")) prefetch_mb_ = std::max(0, std::atoi(g));
+    if (const char* g = std::getenv("RTK_NO_FUSED")) no_fused_ = *g && *g != '0';
     const char* cs = std::getenv("RTK_COUNT_STATS");
     count_stats_ = profile_ || (cs && *cs && *cs != '0');
 }
@@ -361,7 +362,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     clean_rows_ = 0;
     did_init_ = false;
     InputSrc src{d_base, dtype, smallest, scaled ? 1 : 0, a_s};
-    const uint64_t base_words = reinterpret_cast<uintptr_t>(d_base) / 4;
+    const uint64_t base_words = reinterpret_cast<uintptr_t>(d_base) / elem_bytes(dtype);  // base in elements
 
     // ---- 1. per-row plan: sample size s, sample rank r', candidate capacity -------------
     std::vector<uint32_t> rid(R), lead(R), sampled(R);
@@ -380,6 +381,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     std::vector<uint64_t> f_off[2], f_len[2], f_k[2];
     // returns -1 (general path), 0 (large-buffer fused variant) or 1 (small-buffer variant)
     auto fused_class = [&](const RowReq& q) {
+        if (no_fused_) return -1;
         if (q.k == 0 || q.k > rows_fused_kmax(false)) return -1;
         if (q.n > (uint64_t(1) << 18) && R < 64) return -1;  // long rows want many CTAs
         for (int small = 1; small >= 0; --small) {
@@ -882,7 +884,7 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
                       const std::vector<uint32_t>& fb, Call& c, cudaStream_t s) {
     std::vector<uint64_t>& cand_off = c.cand_off;
     uint64_t& cand_total = c.cand_total;
-    const uint64_t base_words = reinterpret_cast<uintptr_t>(d_base) / 4;
+    const uint64_t base_words = reinterpret_cast<uintptr_t>(d_base) / elem_bytes(src.dtype);
     const int R = static_cast<int>(rows.size());
     std::vector<uint32_t> active = fb;
     {

@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kThreads) k_radix_pass(Rows rows, InputSrc in,
             uint32_t v[kUnroll][kVec];
             const uint64_t span0 = tt * kTile;
             const uint64_t span_len = len + lead;
-            load_input_tile(in.base + off - lead, span_len, lead, span0, v);
+            load_input_tile_any(in, off, span_len, lead, span0, v);
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
                 const uint64_t p = span0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec;
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
         const uint32_t e = q * 1024u + tid;
         if (e < local) {
             const uint64_t sg = s0 + e / 32;
-            raw[q] = __ldg(in.base + off + ((sg * stride_fp) >> 16) + (e & 31));
+            raw[q] = load_elem(in, off + ((sg * stride_fp) >> 16) + (e & 31));
         }
     }
 #pragma unroll
@@ -455,8 +455,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
             const uint64_t sp0 = (t - rows.tile_start[j0]) * kTile;
             const uint64_t span_len0 = rows.len[j0] + rows.lead[j0];
             if (sp0 + kTile <= span_len0) {
-                const uint32_t* tp0 = in.base + rows.off[j0] - rows.lead[j0] + sp0;
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(tp0), "r"(kTile * 4) : "memory");
+                constexpr int EB = km_is16<KM>() ? 2 : 4;
+                const char* tp0 = reinterpret_cast<const char*>(in.base) + (rows.off[j0] - rows.lead[j0] + sp0) * EB;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(tp0), "r"(kTile * EB) : "memory");
             }
         }
     }
@@ -532,7 +533,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         const uint32_t vhi = static_cast<uint32_t>(span_len - span0 < kTile ? span_len - span0 : kTile);
         const uint32_t idx0 = static_cast<uint32_t>(span0 - lead);  // low 32 bits of the row index
         uint32_t v[kUnroll][kVec];
-        load_tile_local(in.base + off - lead + span0, vlo, vhi, v);
+        if constexpr (km_is16<KM>())
+            load_tile_local16(reinterpret_cast<const unsigned short*>(in.base) + off - lead + span0, vlo, vhi, v);
+        else
+            load_tile_local(in.base + off - lead + span0, vlo, vhi, v);
 
         // pass 1: key transform + per-thread hit mask (bit u*8+i)
         uint32_t mask = 0;
@@ -582,14 +586,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         if (wtot <= 96) {
             // sparse hits (the common case): visit only the set bits; the element is re-read
             // from L2 (its tile was just streamed) instead of indexing registers dynamically
-            const uint32_t* tp = in.base + off - lead + span0;
+            const uint64_t tp = off - lead + span0;  // element offset of the tile
             uint32_t o = wcur + incl - c;
             uint32_t m = mask;
             while (m) {
                 const uint32_t b = __ffs(m) - 1;
                 m &= m - 1;
                 const uint32_t l = ((b >> 3) * kThreads + threadIdx.x) * kVec + (b & 7);
-                const uint32_t key = key_of<KM>(__ldg(tp + l), in.a_s);
+                uint32_t raw;
+                if constexpr (km_is16<KM>())
+                    raw = __ldg(reinterpret_cast<const unsigned short*>(in.base) + tp + l);
+                else
+                    raw = __ldg(in.base + tp + l);
+                const uint32_t key = key_of<KM>(raw, in.a_s);
                 stage[o++] = (static_cast<unsigned long long>(key) << 32) | (nidx0 - l);
             }
             wcur += wtot;
@@ -671,7 +680,7 @@ __global__ void __launch_bounds__(kThreads) k_first_digit_hist(Rows rows, InputS
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         uint32_t v[kUnroll][kVec];
         const uint64_t span0 = t * kTile, span_len = len + lead;
-        load_input_tile(in.base + off - lead, span_len, lead, span0, v);
+        load_input_tile_any(in, off, span_len, lead, span0, v);
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
@@ -773,6 +782,8 @@ void launch_compact(uint64_t tiles, const Rows& rows, const InputSrc& in, const 
         case kKmF32LScaled: compact_km<kKmF32LScaled>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
         case kKmF32SScaled: compact_km<kKmF32SScaled>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
         case kKmU32L: compact_km<kKmU32L>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
+        case kKmF16L: compact_km<kKmF16L>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
+        case kKmF16S: compact_km<kKmF16S>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
         default: compact_km<kKmU32S>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
     }
 }

@@ -203,7 +203,13 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     const unsigned full = 0xffffffffu;
     const uint32_t r = a.rid[j];
     const uint64_t n = a.len[j], off = a.off[j], k = a.k[j];
-    const uint32_t* row = a.in.base + off;
+    constexpr int EB = km_is16<KM>() ? 2 : 4;  // input element bytes
+    const char* rowb = reinterpret_cast<const char*>(a.in.base) + off * EB;
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(rowb);  // 32-bit element rows only
+    auto ld = [&](uint64_t i) -> uint32_t {
+        if constexpr (EB == 2) return __ldg(reinterpret_cast<const unsigned short*>(rowb) + i);
+        else return __ldg(row + i);
+    };
     unsigned long long* dbg = a.dbg;
     int ndbg = 0;
     auto stamp = [&]() {
@@ -218,12 +224,13 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     // ---- streaming ring: TMA 1-D bulk copies (cp.async.bulk) of 8 KB chunks into a 4-stage
     // shared-memory ring with mbarrier completion; the first stages are in flight while the
     // threshold is being selected.
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(row);
-    const uint32_t head = static_cast<uint32_t>(((16 - (a0 & 15)) & 15) >> 2);  // to 16-B alignment
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(rowb);
+    const uint32_t head = static_cast<uint32_t>(((16 - (a0 & 15)) & 15) / EB);  // to 16-B alignment
     const uint64_t body = n > head ? n - head : 0;
     const uint64_t nchunks = body / kRowChunk;
-    const uint32_t* bsrc = row + head;
-    uint32_t* ring = reinterpret_cast<uint32_t*>(cand + kRowCand);
+    const char* bsrc = rowb + head * EB;
+    char* ring = reinterpret_cast<char*>(cand + kRowCand);
+    constexpr uint32_t kChunkBytes = kRowChunk * EB;
     if (tid == 0) {
         for (int st = 0; st < kRowStages; ++st) mbar_init(&bar[st], 1);
         fence_mbar_init();
@@ -231,7 +238,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     __syncthreads();
     if (tid == 0) {
         for (uint64_t c = 0; c < nchunks && c < static_cast<uint64_t>(kRowStages); ++c)
-            bulk_g2s(ring + c * kRowChunk, bsrc + c * kRowChunk, kRowChunk * 4, &bar[c]);
+            bulk_g2s(ring + c * kChunkBytes, bsrc + c * kChunkBytes, kChunkBytes, &bar[c]);
     }
 
     // ---- 1. threshold -------------------------------------------------------------------
@@ -242,7 +249,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
         const uint64_t stride_fp = ((n - 32) << 16) / (nseg - 1);
         for (int e = tid; e < kRowSample; e += kRowThreads) {
             const uint64_t idx = ((static_cast<uint64_t>(e / 32) * stride_fp) >> 16) + (e & 31);
-            cand[e] = composite(make_key(a.in, __ldg(row + idx)), idx);
+            cand[e] = composite(make_key(a.in, ld(idx)), idx);
         }
         __syncthreads();
         const double rr = static_cast<double>(k) * kRowSample / static_cast<double>(n);
@@ -305,8 +312,14 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
             if (c >= nchunks) break;
             const int st = static_cast<int>(c % kRowStages);
             mbar_wait(&bar[st], static_cast<uint32_t>((c / kRowStages) & 1));
-            const uint4 q = reinterpret_cast<const uint4*>(ring + st * kRowChunk)[tid];
-            uint32_t key[4] = {q.x, q.y, q.z, q.w};
+            uint32_t key[4];
+            if constexpr (EB == 2) {
+                const uint2 q = reinterpret_cast<const uint2*>(ring + st * kChunkBytes)[tid];
+                key[0] = q.x & 0xFFFFu; key[1] = q.x >> 16; key[2] = q.y & 0xFFFFu; key[3] = q.y >> 16;
+            } else {
+                const uint4 q = reinterpret_cast<const uint4*>(ring + st * kChunkBytes)[tid];
+                key[0] = q.x; key[1] = q.y; key[2] = q.z; key[3] = q.w;
+            }
             const uint32_t ibase = head + static_cast<uint32_t>(c * kRowChunk) + tid * 4;
             const uint32_t mask = test4(key, ibase, 0xFu);
             push4(mask, key, ibase);
@@ -316,8 +329,8 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
             for (int g = 0; g < G; ++g) {
                 const uint64_t c = c0 + g;
                 if (c + kRowStages < nchunks)
-                    bulk_g2s(ring + (c % kRowStages) * kRowChunk, bsrc + (c + kRowStages) * kRowChunk,
-                             kRowChunk * 4, &bar[c % kRowStages]);
+                    bulk_g2s(ring + (c % kRowStages) * kChunkBytes, bsrc + (c + kRowStages) * kChunkBytes,
+                             kChunkBytes, &bar[c % kRowStages]);
             }
         }
     }
@@ -336,7 +349,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
                 const uint64_t g = e + i;
                 uint64_t idx = g < head ? g : t0 + (g - head);
                 const bool ok = g < head ? true : (g - head) < rest;
-                key[i] = ok ? __ldg(row + idx) : 0u;
+                key[i] = ok ? ld(idx) : 0u;
                 valid |= static_cast<uint32_t>(ok) << i;
                 if (i == 0) ib = static_cast<uint32_t>(idx);
             }
@@ -414,10 +427,11 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
             uint32_t val;
             if (a.in.scaled) val = __ldg(row + idx);
             else if (a.in.dtype == kF32) val = decode_f32_bits(kv, a.in.smallest);
+            else if (a.in.dtype == kF16) val = decode_f16_bits(kv, a.in.smallest);
             else val = a.in.smallest ? ~kv : kv;
-            a.out_vals[oo + p] = val;
+            store_val(a.out_vals, a.in.dtype, oo + p, val);
             a.out_idx[oo + p] = idx;
-            if (p == kk - 1 && a.pivots) a.pivots[r] = val;
+            if (p == kk - 1 && a.pivots) store_val(a.pivots, a.in.dtype, r, val);
         }
         stamp();
         return;
@@ -500,10 +514,11 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
         uint32_t val;
         if (a.in.scaled) val = __ldg(row + idx);
         else if (a.in.dtype == kF32) val = decode_f32_bits(kv, a.in.smallest);
+        else if (a.in.dtype == kF16) val = decode_f16_bits(kv, a.in.smallest);
         else val = a.in.smallest ? ~kv : kv;
-        a.out_vals[oo + p] = val;
+        store_val(a.out_vals, a.in.dtype, oo + p, val);
         a.out_idx[oo + p] = idx;
-        if (p == kk - 1 && a.pivots) a.pivots[r] = val;
+        if (p == kk - 1 && a.pivots) store_val(a.pivots, a.in.dtype, r, val);
     }
     stamp();
     if (dbg && blockIdx.x == 0 && threadIdx.x == 0) dbg[31] = ndbg;
@@ -529,6 +544,8 @@ static void rows_variant(int R, const RowsFusedArgs& a, cudaStream_t s) {
         case kKmF32LScaled: rows_km<kKmF32LScaled, CAND, STAGES, SAMPLE>(R, a, s); break;
         case kKmF32SScaled: rows_km<kKmF32SScaled, CAND, STAGES, SAMPLE>(R, a, s); break;
         case kKmU32L: rows_km<kKmU32L, CAND, STAGES, SAMPLE>(R, a, s); break;
+        case kKmF16L: rows_km<kKmF16L, CAND, STAGES, SAMPLE>(R, a, s); break;
+        case kKmF16S: rows_km<kKmF16S, CAND, STAGES, SAMPLE>(R, a, s); break;
         default: rows_km<kKmU32S, CAND, STAGES, SAMPLE>(R, a, s); break;
     }
 }

@@ -840,10 +840,11 @@ __device__ __forceinline__ void emit_rank(const SortArgs& g, uint32_t r, uint64_
     uint32_t val;
     if (g.gather) val = __ldg(g.in_base + g.row_in_off[r] + idx);
     else if (g.dtype == kF32) val = decode_f32_bits(key, g.smallest);
+    else if (g.dtype == kF16) val = decode_f16_bits(key, g.smallest);
     else val = g.smallest ? ~key : key;
-    g.out_vals[oo + rank] = val;
+    store_val(g.out_vals, g.dtype, oo + rank, val);
     g.out_idx[oo + rank] = idx;
-    if (rank == kr - 1 && g.pivots) g.pivots[r] = val;  // engine.hpp:333
+    if (rank == kr - 1 && g.pivots) store_val(g.pivots, g.dtype, r, val);  // engine.hpp:333
 }
 
 // Sort one group of <= 32*IPL composites by one warp and write ranks < k as (value bits, u64
@@ -1000,13 +1001,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
             const unsigned long long K = key[j];
             const uint32_t kk = static_cast<uint32_t>(K >> 32);
             const uint32_t idx = ~static_cast<uint32_t>(K);
-            uint32_t val;
-            if (g.gather) val = __ldg(g.in_base + g.row_in_off[r] + idx);
-            else if (g.dtype == kF32) val = decode_f32_bits(kk, g.smallest);
-            else val = g.smallest ? ~kk : kk;
-            g.out_vals[oo + rank] = val;
-            g.out_idx[oo + rank] = idx;
-            if (rank == kr - 1 && g.pivots) g.pivots[r] = val;  // engine.hpp:333
+            emit_rank(g, r, kr, oo, rank, kk, idx);
         }
         __syncthreads();
     }

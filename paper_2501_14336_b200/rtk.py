@@ -261,18 +261,25 @@ def _is_cuda(x) -> bool:
 
 
 def _dtype_code(x) -> int:
+    """C-ABI dtype code: 0 f32, 1 u32, 2 f16 (io.hpp:3's code), 3 bf16."""
     if _is_cuda(x) or hasattr(x, "dtype") and "torch" in type(x).__module__:
         import torch
         if x.dtype == torch.float32:
             return 0
         if x.dtype in (torch.uint32, torch.int32):
             return 1
+        if x.dtype == torch.float16:
+            return 2
+        if x.dtype == torch.bfloat16:
+            return 3
         raise TypeError(f"unsupported dtype {x.dtype}")
     a = np.asarray(x)
     if a.dtype == np.float32:
         return 0
     if a.dtype == np.uint32:
         return 1
+    if a.dtype == np.float16:
+        return 2
     raise TypeError(f"unsupported dtype {a.dtype}")
 
 
@@ -282,6 +289,8 @@ def _stream_ptr(t) -> C.c_void_p:
 
 
 def _np_scalar(bits: int, dtype_code: int):
+    if dtype_code == 2:
+        return np.array([bits & 0xFFFF], dtype=np.uint16).view(np.float16)[0]
     arr = np.array([bits], dtype=np.uint32)
     return arr.view(np.float32)[0] if dtype_code == 0 else arr[0]
 
@@ -312,7 +321,7 @@ def topk(input, k: int, order: SelectionOrder = SelectionOrder.Largest,
                           int(order), C.c_void_p(vals.data_ptr()), C.c_void_p(idx.data_ptr()),
                           C.c_void_p(piv.data_ptr()), C.byref(c), _stream_ptr(x))
         _raise(st, "rtk_topk")
-        if code == 0:
+        if code in (0, 2, 3):
             return TopKResult(vals, idx, pivot_fn=lambda: piv[0].item())
         return TopKResult(vals, idx, pivot_fn=lambda: int(piv.view(torch.int32)[0].item()) & 0xFFFFFFFF)
     a = np.ascontiguousarray(input.numpy() if hasattr(input, "numpy") else np.asarray(input))

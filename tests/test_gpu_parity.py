@@ -249,3 +249,80 @@ def test_host_entry_points(cuda):
     wv, wi, wp, _ = O.ref_scaled_topk(y, 512, 0, mode=1, seed=2)
     r = rtk.scaled_topk(y, 512, policy=rtk.ScalePolicy(rtk.ScaleMode.Always, 0.5, 2))
     assert_same((r.values, r.indices, r.pivot), (wv, wi, wp), "host scaled")
+
+
+# ---- 16-bit floats ---------------------------------------------------
+# The reference declares f16 (io.hpp:3, dtype code 2) but does not build it (io.cpp:71-72). Both f16
+# and bf16 widen EXACTLY and order-preservingly to f32 (NaN payloads, +-0 and +-inf included), so
+# the reference engine on the widened input is the oracle: identical indices, and the returned
+# 16-bit words must be the inputs at those indices (bit-exact widening: tests/test_oracle.py).
+def _widen16(h, kind):
+    from tests.test_oracle import widen16_exact
+    return widen16_exact(h, kind).view(np.float32)
+
+
+def _gpu_topk16(t16, k, order, cuda):
+    import torch
+    rtk = _rtk()
+    r = rtk.topk(t16.to(cuda), k, rtk.SelectionOrder(order))
+    return r.values.view(torch.int16).cpu().numpy().view(np.uint16), r.indices.cpu().numpy(), r
+
+
+def _check16(h, t16, x32, k, order, cuda, what):
+    gv, gi, r = _gpu_topk16(t16, k, order, cuda)
+    _, wi, _ = O.ref_topk(x32, k, order, grid=4)
+    bad = np.nonzero(gi.astype(np.uint64) != wi.astype(np.uint64))[0]
+    assert bad.size == 0, f"{what}: index mismatch at ranks {bad[:5]}"
+    assert np.array_equal(gv, h[wi.astype(np.int64)]), f"{what}: value bits"
+    # pivot = k-th value (engine.hpp:333): compare through the widened f32 value
+    pv = np.float32(r.pivot)
+    assert pv.view(np.uint32) == x32[wi[-1]].view(np.uint32) or (np.isnan(pv) and np.isnan(x32[wi[-1]])), f"{what}: pivot"
+
+
+@pytest.mark.parametrize("kind", ["bf16", "f16"])
+@pytest.mark.parametrize("n", [1000, 1 << 16, (1 << 20) + 3])
+@pytest.mark.parametrize("order", [0, 1])
+def test_16bit_topk(cuda, kind, n, order):
+    rng = np.random.default_rng(7000 + n + (kind == "f16") * 3 + order)
+    import torch
+    x = torch.from_numpy(rng.standard_normal(n).astype(np.float32))
+    t16 = x.to(torch.bfloat16 if kind == "bf16" else torch.float16)
+    h = t16.view(torch.int16).numpy().view(np.uint16).copy()
+    x32 = _widen16(h, kind)
+    for k in sorted({1, 50, 512, n // 2, n}):
+        _check16(h, t16, x32, k, order, cuda, f"{kind} n={n} order={order} k={k}")
+
+
+@pytest.mark.parametrize("kind", ["bf16", "f16"])
+def test_16bit_special_values_and_ties(cuda, kind):
+    import torch
+    dt = torch.bfloat16 if kind == "bf16" else torch.float16
+    base = torch.tensor([float("nan"), float("inf"), 1.0, 0.0, -0.0, -1.0, float("-inf"), -float("nan"), 1.0, 0.0],
+                        dtype=torch.float32).to(dt)
+    t16 = base.repeat(4000)  # heavy ties: every value 4000 times
+    h = t16.view(torch.int16).numpy().view(np.uint16).copy()
+    h[::997] = 0x7C01 if kind == "f16" else 0x7F81  # signalling-NaN payloads too
+    t16 = torch.from_numpy(h.view(np.int16)).view(dt)
+    x32 = _widen16(h, kind)
+    for order in (0, 1):
+        for k in (1, 7, 3999, 12345, t16.numel()):
+            _check16(h, t16, x32, k, order, cuda, f"{kind} special order={order} k={k}")
+
+
+@pytest.mark.parametrize("k", [50, 4096, 32000])
+def test_16bit_batch_llm_rows(cuda, k):
+    # C3-like bf16 logits: 8 rows of a 32000 vocabulary, batch == per-row topk (batch_test.cpp:90-107)
+    import torch
+    rtk = _rtk()
+    B, V = 8, 32000
+    g = torch.Generator().manual_seed(11)
+    logits = torch.randn(B, V, generator=g).to(torch.bfloat16)
+    r = rtk.batch_topk_dense(logits.to(cuda), k)
+    gv = r.values.view(torch.int16).cpu().numpy().view(np.uint16)
+    gi = r.indices.cpu().numpy()
+    h = logits.view(torch.int16).numpy().view(np.uint16)
+    x32 = _widen16(h.reshape(-1), "bf16").reshape(B, V)
+    for t in range(B):
+        _, wi, _ = O.ref_topk(np.ascontiguousarray(x32[t]), k, 0, grid=4)
+        assert np.array_equal(gi[t].astype(np.uint64), wi.astype(np.uint64)), f"row {t}"
+        assert np.array_equal(gv[t], h[t][wi.astype(np.int64)]), f"row {t} values"
