@@ -264,7 +264,7 @@ def main():
         del xa
 
     # C3: batched LLM sampling top-k, rows sharded across ranks (no collective)
-    batch_llm = {}
+    batch_llm, batch_bf16 = {}, {}
     if args.batch_ks:
         from paper_2501_14336_b200 import sharded as SH
         r0, r1 = SH.row_shard(args.batch_rows, world, rank)
@@ -285,7 +285,18 @@ def main():
             byts = args.batch_rows * (4 * V + 12 * kb)
             batch_llm[str(kb)] = {"ms_per_batch": ms_b, "queries_per_s": q, "effective_GBps": byts / (ms_b * 1e-3) / 1e9,
                                   "fraction_of_hbm_peak": byts / (ms_b * 1e-3) / 1e9 / peak}
-        del logits, flush
+        # the same batches with bf16 logits (16-bit keys): half the bytes per element
+        batch_bf16 = {}
+        lb = logits.to(torch.bfloat16)
+        for kb in [int(v) for v in args.batch_ks.split(",") if v]:
+            kb = min(kb, V)
+            torch.cuda.synchronize()
+            ms_h, _ = R.bench_batch_dense(lb, kb, max(5, args.steps // 2), 3, flush)
+            byts = args.batch_rows * (2 * V + 10 * kb)
+            batch_bf16[str(kb)] = {"ms_per_batch": ms_h, "queries_per_s": args.batch_rows / (ms_h * 1e-3),
+                                   "effective_GBps": byts / (ms_h * 1e-3) / 1e9,
+                                   "fraction_of_hbm_peak": byts / (ms_h * 1e-3) / 1e9 / peak}
+        del logits, flush, lb
 
     # e2e through the host entry point (rank 0 / N=1 semantics: per-GPU query from pinned host)
     e2e = None
@@ -339,6 +350,8 @@ def main():
                "k_sweep": sweep,
                "adversarial_c4": {"config": "n=2^26 Uniform[128.6,128.7) fp32, k=2^16, largest, scaled_topk "
                                             "tau=0.5 seed=31 (device-resident)", "results": adversarial},
+               "batch_llm_bf16": {"config": "the same logits rounded to bf16 (2 B per element; bytes = "
+                                            "rows * (2V + 10k))", "results": batch_bf16},
                "batch_llm": {"config": f"{args.batch_rows} x {args.vocab} fp32 N(0,1) logits, rows sharded over "
                                        f"{world} GPU(s), L2 flushed between batches", "results": batch_llm},
                "step_ms_all": ms}

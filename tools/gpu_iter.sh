@@ -8,5 +8,5 @@ python - <<'PY'
 import json
 d=json.load(open('gpurun_out/bench.json'))
 print('value',round(d['value']),'ms',d['ms_per_step'],'roof',d['roofline']['frac'])
-print('sweep',{k:(round(v['ms_per_step'],4),round(v['GBps'])) for k,v in d['k_sweep'].items()}); print("c4", {k:(round(v["ms"],4), round(v["GBps"])) for k,v in d["adversarial_c4"]["results"].items()}); print('batch',{k:(round(v['ms_per_batch'],4),round(v['queries_per_s'])) for k,v in d['batch_llm']['results'].items()})
+print('sweep',{k:(round(v['ms_per_step'],4),round(v['GBps'])) for k,v in d['k_sweep'].items()}); print("c4", {k:(round(v["ms"],4), round(v["GBps"])) for k,v in d["adversarial_c4"]["results"].items()}); print('batch',{k:(round(v['ms_per_batch'],4),round(v['queries_per_s'])) for k,v in d['batch_llm']['results'].items()}); print('bf16',{k:(round(v['ms_per_batch'],4),round(v['queries_per_s'])) for k,v in d['batch_llm_bf16']['results'].items()})
 PY
