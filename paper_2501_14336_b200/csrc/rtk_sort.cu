@@ -249,194 +249,6 @@ __global__ void __launch_bounds__(kThreads) k_seg_hist(const SegSlot* slots, int
 constexpr int kMsdThreads = 1024;
 constexpr int kMsdWarps = kMsdThreads / 32;
 
-// bucket classes: 0 empty, 1 tiny (packed, quantum 32), 2 mid (packed, quantum 128), 3 solo warp,
-// 4 small (packed, quantum kGroupPack, CTA), 5 solo CTA, 6 big (next level). Classes 1-3 form warp
-// groups (<= kWarpGroupMax), 4-5 CTA groups (<= kSortCap).
-__device__ __forceinline__ uint32_t fine_class(uint32_t c) {
-    return c == 0 ? 0u : c <= kTinyMax ? 1u : c <= kMidMax ? 2u : c <= kWarpGroupMax ? 3u
-         : c <= kGroupPack ? 4u : c <= kSortCap ? 5u : 6u;
-}
-
-// Boundary rule for a kept, non-empty bucket (start s, class cl) after the previous kept
-// bucket `prev` (0: none, else ((start + 1) << 3) | class). Packable buckets join the open group
-// while the class is unchanged and their starts share its quantum (group < 2 x quantum); solo
-// buckets are their own group; big ones are a boundary but no group.
-__device__ __forceinline__ void fine_rule(uint32_t s, uint32_t cl, unsigned long long prev, bool& bnd,
-                                          bool& gst) {
-    if (cl == 6) { bnd = true; gst = false; return; }
-    if (cl == 3 || cl == 5 || prev == 0) { bnd = gst = true; return; }
-    const uint32_t pcl = static_cast<uint32_t>(prev & 7), ps = static_cast<uint32_t>((prev >> 3) - 1);
-    const uint32_t q = cl == 1 ? kTinyMax : cl == 2 ? kMidMax : kGroupPack;
-    gst = pcl != cl || s / q != ps / q;
-    bnd = gst;
-}
-
-// Plan of one slot from its bucket totals cnt[0, B) (shared memory), kMsdThreads threads; cnt
-// is overwritten in place with the bucket starts (~0: dropped, rank >= k).
-// Thread t owns buckets [B - (t+1)*per, B - t*per) walked downward (thread 0: top digits).
-__device__ void msd_plan_block(const SegSlot& sl, uint32_t* cnt, uint32_t B, const FineArgs& a) {
-    constexpr uint32_t INF = 0xffffffffu;
-    __shared__ unsigned long long s_w64[kMsdWarps];
-    __shared__ uint32_t s_w32[kMsdWarps];
-    __shared__ unsigned long long s_cw[kMsdWarps];
-    __shared__ uint32_t s_suf[kMsdWarps], s_ke[kMsdWarps];
-    __shared__ unsigned long long s_base[3];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned full = 0xffffffffu;
-    const uint32_t per = B / kMsdThreads;  // 2, 8 or 16
-    uint32_t* bs = cnt;
-    const uint64_t kr = a.row_k[sl.rid];
-    const uint64_t krel = kr > sl.rank_base ? kr - sl.rank_base : 0;  // kept: start < krel
-    const uint32_t lo = B - (tid + 1) * per;
-
-    // sweep 1: bucket total + last non-empty bucket (local start, class)
-    uint32_t sum = 0, last_ls = 0, last_cl = 0;
-    for (uint32_t i = 0; i < per; ++i) {
-        const uint32_t c = cnt[lo + per - 1 - i];
-        if (c) { last_ls = sum; last_cl = fine_class(c); }
-        sum += c;
-    }
-    // scan 1: exclusive sum (bucket starts) and exclusive max of the last bucket (predecessor)
-    uint32_t inc = sum;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t o = __shfl_up_sync(full, inc, d);
-        if (lane >= d) inc += o;
-    }
-    if (lane == 31) s_w32[warp] = inc;
-    __syncthreads();
-    uint32_t before = inc - sum;
-    for (int w = 0; w < warp; ++w) before += s_w32[w];
-    const unsigned long long L =
-        last_cl ? (static_cast<unsigned long long>(before + last_ls) + 1) << 3 | last_cl : 0ull;
-    unsigned long long prev;
-    {
-        unsigned long long v = L;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const unsigned long long o = __shfl_up_sync(full, v, d);
-            if (lane >= d) v = max(v, o);
-        }
-        const unsigned long long ex = __shfl_up_sync(full, v, 1);
-        if (lane == 31) s_w64[warp] = v;
-        __syncthreads();
-        unsigned long long wpre = 0;
-        for (int w = 0; w < warp; ++w) wpre = max(wpre, s_w64[w]);
-        prev = max(wpre, lane ? ex : 0ull);
-    }
-
-    // sweep 2: count groups / next-level slots, first boundary, kept end
-    uint32_t nw = 0, nc = 0, nb = 0, first_bnd = INF, kept_end = 0;
-    {
-        uint32_t s = before;
-        unsigned long long pv = prev;
-        for (uint32_t i = 0; i < per; ++i) {
-            const uint32_t c = cnt[lo + per - 1 - i];
-            if (c && s < krel) {
-                const uint32_t cl = fine_class(c);
-                bool bnd, gst;
-                fine_rule(s, cl, pv, bnd, gst);
-                if (bnd && first_bnd == INF) first_bnd = s;
-                if (cl == 6) ++nb;
-                else if (gst) { if (cl <= 3) ++nw; else ++nc; }
-                kept_end = s + c;
-                pv = (static_cast<unsigned long long>(s) + 1) << 3 | cl;
-            }
-            s += c;
-        }
-    }
-    // scan 2: packed (nw, nc, nb) exclusive sum; suffix min of first_bnd; max kept_end
-    const unsigned long long cnt3 = static_cast<unsigned long long>(nw) |
-                                    static_cast<unsigned long long>(nc) << 21 |
-                                    static_cast<unsigned long long>(nb) << 42;
-    unsigned long long cinc = cnt3;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned long long o = __shfl_up_sync(full, cinc, d);
-        if (lane >= d) cinc += o;
-    }
-    uint32_t suf = first_bnd, ke = kept_end;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t o = __shfl_down_sync(full, suf, d);
-        if (lane + d < 32) suf = min(suf, o);
-    }
-    const uint32_t suf_after_lane = __shfl_down_sync(full, suf, 1);
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) ke = max(ke, __shfl_xor_sync(full, ke, d));
-    if (lane == 31) s_cw[warp] = cinc;
-    if (lane == 0) { s_suf[warp] = suf; s_ke[warp] = ke; }
-    __syncthreads();
-    unsigned long long cpre = cinc - cnt3, ctot = 0;
-    uint32_t after = lane < 31 ? suf_after_lane : INF, kend = 0;
-    for (int w = 0; w < kMsdWarps; ++w) {
-        if (w < warp) cpre += s_cw[w];
-        ctot += s_cw[w];
-        if (w > warp) after = min(after, s_suf[w]);
-        kend = max(kend, s_ke[w]);
-    }
-    if (tid == 0) {
-        const uint32_t tw = static_cast<uint32_t>(ctot & 0x1FFFFF);
-        const uint32_t tc = static_cast<uint32_t>((ctot >> 21) & 0x1FFFFF);
-        const uint32_t tb = static_cast<uint32_t>(ctot >> 42);
-        s_base[0] = tw ? atomicAdd(a.wgroups.count, tw) : 0;
-        s_base[1] = tc ? atomicAdd(a.groups.count, tc) : 0;
-        s_base[2] = tb ? atomicAdd(a.next.count, tb) : 0;
-        if (tb) atomicOr(a.flags, kFlagMore);
-    }
-    __syncthreads();
-    uint32_t iw = static_cast<uint32_t>(s_base[0] + (cpre & 0x1FFFFF));
-    uint32_t ic = static_cast<uint32_t>(s_base[1] + ((cpre >> 21) & 0x1FFFFF));
-    uint32_t ib = static_cast<uint32_t>(s_base[2] + (cpre >> 42));
-
-    // sweep 3: emit groups / slots and the bucket starts for the scatter
-    bool open = false, overflow = false;
-    uint32_t os = 0, ocl = 0;
-    auto emit = [&](uint32_t end) {
-        const SortGroup gr{sl.off + os, end - os, sl.rid, 1u, 0u, sl.rank_base + os};
-        if (ocl <= 3) {
-            if (iw < a.wgroups.cap) a.wgroups.groups[iw] = gr; else overflow = true;
-            ++iw;
-        } else {
-            if (ic < a.groups.cap) a.groups.groups[ic] = gr; else overflow = true;
-            ++ic;
-        }
-    };
-    {
-        uint32_t s = before;
-        unsigned long long pv = prev;
-        for (uint32_t i = 0; i < per; ++i) {
-            const uint32_t b = lo + per - 1 - i;
-            const uint32_t c = cnt[b];
-            const bool kept = c && s < krel;
-            bs[b] = kept ? s : ~0u;
-            if (kept) {
-                const uint32_t cl = fine_class(c);
-                bool bnd, gst;
-                fine_rule(s, cl, pv, bnd, gst);
-                if (bnd) {
-                    if (open) emit(s);
-                    open = gst;
-                    os = s;
-                    ocl = cl;
-                    if (cl == 6) {
-                        if (ib < a.next.cap)
-                            a.next.slots[ib] = SegSlot{sl.off + s, c, sl.rank_base + s, sl.rid,
-                                                       sl.pos >= kDigit ? sl.pos - kDigit : 0u, kDigit, 0};
-                        else
-                            overflow = true;
-                        ++ib;
-                    }
-                }
-                pv = (static_cast<unsigned long long>(s) + 1) << 3 | cl;
-            }
-            s += c;
-        }
-    }
-    if (open) emit(min(after, kend));
-    if (overflow) atomicOr(a.flags, kFlagOverflow);
-}
-
 // chunk c of G over m elements: [c*ch, min(m, (c+1)*ch)), ch a multiple of 4
 __device__ __forceinline__ void msd_chunk(uint64_t m, uint32_t G, uint32_t c, uint64_t& e0, uint64_t& e1) {
     const uint64_t ch = ((m + G - 1) / G + 3) & ~uint64_t(3);
