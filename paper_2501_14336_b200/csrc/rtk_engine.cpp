@@ -81,6 +81,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_GRAPH_EVENTS")) no_graph_events_ = *g == '0';
     if (const char* g = std::getenv("RTK_PREFETCH_MB")) prefetch_mb_ = std::max(0, std::atoi(g));
     if (const char* g = std::getenv("RTK_NO_FUSED")) no_fused_ = *g && *g != '0';
+    if (const char* g = std::getenv("RTK_NO_DENSE")) no_dense_ = *g && *g != '0';
     const char* cs = std::getenv("RTK_COUNT_STATS");
     count_stats_ = profile_ || (cs && *cs && *cs != '0');
 }
@@ -474,7 +475,21 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     ghist_.ensure(8ull * kBins * R);
     cand_a_.ensure(8 * std::max<uint64_t>(cand_total, 1));
 
+    // Dense mode: every general row is unsampled with k >= n/2 (e.g. k = vocab): all elements are
+    // candidates, so the compaction would only rewrite the rows as composites. The level-0 MSD
+    // reads the input instead (slot.src = 1), its digit the top bits of the key.
+    bool dense = !grow.empty() && no_dense_ == false;
+    std::vector<SegSlot> dslots;
+    for (uint32_t r : grow) {
+        const RowReq& q = rows[r];
+        if (sampled[r] || 2 * q.k < q.n || q.n <= kSortCap) { dense = false; break; }
+        const uint32_t bits = std::min<uint32_t>(fine_bits(q.n), msd_max_bits_);
+        SegSlot sl{cand_off[r], q.n, 0, r, 64u - bits, bits, 1u, q.in_off};
+        dslots.push_back(sl);
+    }
+    if (!dense) dslots.clear();
     Plan P;
+    const size_t o_dslots = P.add(dslots);
     const size_t o_rid = P.add(rid), o_off = P.add(off), o_len = P.add(len), o_lead = P.add(lead),
                  o_tile = P.add(tile_start), o_coff = P.add(cand_off), o_cap = P.add(cap),
                  o_k = P.add(row_k), o_out = P.add(row_out), o_in = P.add(row_in),
@@ -561,7 +576,13 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
         mark("rows_fused", s);
     }
     record(1, s);
-    if (!grow.empty()) {
+    if (!grow.empty() && dense) {
+        FinishPrep fp = prepare_finish(c, grow);
+        fp.slots = at<SegSlot>(D, o_dslots);
+        record(2, s);
+        mark("compact(skipped: dense rows)", s);
+        launch_finish(c, fp);
+    } else if (!grow.empty()) {
         FinishPrep fp = prepare_finish(c, grow);
         Rows all{static_cast<int>(grow.size()), at<uint32_t>(D, o_grow), at<uint64_t>(D, o_goff),
                  at<uint64_t>(D, o_glen), at<uint32_t>(D, o_glead), at<uint64_t>(D, o_gtile)};
@@ -687,7 +708,8 @@ PlanArgs Engine::plan_args(const Call& c, const FinishPrep& f) {
 void Engine::launch_finish(Call& c, const FinishPrep& f) {
     if (f.NR == 0) return;
     if (f.big_rows) {
-        FineArgs fa{c.d_row_k, f.gl, f.wgl, f.nextA, ctl_.as<uint32_t>(), nullptr, 1, nullptr, nullptr, 0};
+        FineArgs fa{c.src, c.d_row_k, f.gl, f.wgl, f.nextA, ctl_.as<uint32_t>(), nullptr, 1, nullptr, nullptr, 0};
+        const SegSlot* slots = f.slots ? f.slots : slots0_.as<SegSlot>();
         if (profile_) {
             dbg_.ensure(4096);
             fa.dbg = dbg_.as<unsigned long long>();
@@ -708,10 +730,10 @@ void Engine::launch_finish(Call& c, const FinishPrep& f) {
                 fa.bar_target = bar_gen_;
             }
         }
-        if (!launch_msd_cluster(f.NR, cs, slots0_.as<SegSlot>(), cand_a_.as<uint64_t>(), cand_b_.as<uint64_t>(), fa, c.s)) {
+        if (!launch_msd_cluster(f.NR, cs, slots, cand_a_.as<uint64_t>(), cand_b_.as<uint64_t>(), fa, c.s)) {
             bar_gen_ -= fa.Q * cs;
             fa.Q = 1;
-            launch_msd_cluster(f.NR, f.cs, slots0_.as<SegSlot>(), cand_a_.as<uint64_t>(), cand_b_.as<uint64_t>(), fa, c.s);
+            launch_msd_cluster(f.NR, f.cs, slots, cand_a_.as<uint64_t>(), cand_b_.as<uint64_t>(), fa, c.s);
         }
         check(cudaGetLastError(), "msd launch");
         stats.kernel_launches += 1;

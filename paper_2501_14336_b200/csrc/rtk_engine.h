@@ -124,6 +124,7 @@ private:
         uint64_t max_wgroups = 0;
         int cs = 2;
         uint64_t max_cap = 0;
+        const SegSlot* slots = nullptr;  // level-0 slots (null: written by k_compact's plan)
         GroupList gl{}, wgl{};
         SlotList nextA{};
     };
@@ -191,7 +192,8 @@ private:
     bool force_init_ = false;
     bool no_graph_events_ = true;   // no stats events inside graphs (RTK_GRAPH_EVENTS=1 keeps them)
     bool timing_ = false;           // rtk_set_timing: no graph replay, events around k_compact
-    bool no_fused_ = false;         // RTK_NO_FUSED=1: short rows take the general path too
+    bool no_fused_ = false;
+    bool no_dense_ = false;         // RTK_NO_DENSE=1: dense rows are compacted too         // RTK_NO_FUSED=1: short rows take the general path too
     int prefetch_mb_ = 24;          // L2 prefetch budget of k_compact (RTK_PREFETCH_MB)
     int clean_rows_ = 0;
     int clean_upto_ = 0;          // rows whose counters the last call left clean

@@ -108,8 +108,9 @@ struct SegSlot {        // one MSD segment; len == 0 means inactive
     uint64_t rank_base;
     uint32_t rid;
     uint32_t pos;        // digit = (K >> pos) & (2^bits - 1)
-    uint32_t bits;       // level 0 (fine MSD): 11..16; deeper levels: kDigit
-    uint32_t pad;
+    uint32_t bits;       // level 0: 11..14; deeper levels: kDigit
+    uint32_t src;        // level 0: 1 = read the INPUT row at in_off (dense row, no compaction)
+    uint64_t in_off;     // input element offset of the row (src == 1)
 };
 
 struct GroupList {
@@ -147,6 +148,7 @@ constexpr uint32_t kMidMax = 128;       // packed by 128-quantum -> warp group <
 constexpr uint32_t kWarpGroupMax = 256; // solo warp group up to this size
 constexpr int kMsdMaxBits = 14;
 struct FineArgs {
+    InputSrc in;             // dense rows (slot.src == 1) are read from the input directly
     const uint64_t* row_k;
     GroupList groups;        // CTA groups
     GroupList wgroups;       // warp groups (<= kWarpGroupMax)

@@ -413,6 +413,27 @@ __device__ void msd_plan_slice(const SegSlot& sl, uint32_t* tot, uint32_t slice,
 //  3 [Q > 1: cluster totals -> global, grid barrier, cross-cluster column scan]
 //  4 each CTA plans its bucket slice (slice offsets exchanged over DSMEM; only cluster 0 emits)
 //  5 cursors = bucket start + cross-cluster + intra-cluster offset; scatter of the chunk
+// Input elements [e0, e1) of a dense row as composites (key transform fused, index = position),
+// 4 loads in flight per thread, block-uniform trip count.
+template <typename F>
+__device__ __forceinline__ void msd_stream_in(const InputSrc& in, uint64_t row_in_off, uint64_t e0, uint64_t e1,
+                                              F f) {
+    for (uint64_t base = e0; base < e1; base += 4ull * kMsdThreads) {
+        uint32_t raw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t e = base + static_cast<uint64_t>(u) * kMsdThreads + threadIdx.x;
+            raw[u] = e < e1 ? load_elem(in, row_in_off + e) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t e = base + static_cast<uint64_t>(u) * kMsdThreads + threadIdx.x;
+            const bool valid = e < e1;
+            f(valid ? composite(make_key(in, raw[u]), e) : 0ull, valid);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* slots, const uint64_t* src,
                                                                 uint64_t* dst, FineArgs fa) {
     namespace cg = cooperative_groups;
@@ -443,7 +464,7 @@ __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* s
     uint64_t e0, e1;
     msd_chunk(sl.len, Q * CS, q * CS + r, e0, e1);
     const uint64_t* p = src + sl.off;
-    msd_stream(p, e0, e1, [&](unsigned long long K, bool valid) {
+    auto hist_one = [&](unsigned long long K, bool valid) {
         const uint32_t d = static_cast<uint32_t>(K >> sl.pos) & dmask;
         const uint32_t d0 = __shfl_sync(full, d, 0);
         if (__all_sync(full, valid && d == d0)) {
@@ -451,7 +472,9 @@ __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* s
         } else if (valid) {
             atomicAdd(h + d, 1u);
         }
-    });
+    };
+    if (sl.src) msd_stream_in(fa.in, sl.in_off, e0, e1, hist_one);  // dense row: no compaction
+    else msd_stream(p, e0, e1, hist_one);
     cluster.sync();
     if (dbg) fa.dbg[1] = msd_timer();
     // 2: intra-cluster column scan of this CTA's slice through DSMEM
@@ -535,7 +558,7 @@ __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* s
     cluster.sync();  // owners' shared memory is read by everyone before anyone exits
     if (dbg) fa.dbg[5] = msd_timer();
     uint64_t* qd = dst + sl.off;
-    msd_stream(p, e0, e1, [&](unsigned long long K, bool valid) {
+    auto scatter_one = [&](unsigned long long K, bool valid) {
         const uint32_t d = static_cast<uint32_t>(K >> sl.pos) & dmask;
         const uint32_t d0 = __shfl_sync(full, d, 0);
         if (__all_sync(full, valid && d == d0)) {  // tie-heavy: one shared atomic per warp
@@ -548,7 +571,9 @@ __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* s
         } else if (valid) {
             if (h[d] != ~0u) qd[atomicAdd(h + d, 1u)] = K;
         }
-    });
+    };
+    if (sl.src) msd_stream_in(fa.in, sl.in_off, e0, e1, scatter_one);
+    else msd_stream(p, e0, e1, scatter_one);
     if (dbg) { fa.dbg[6] = msd_timer(); fa.dbg[31] = 7; }
 }
 
@@ -754,9 +779,9 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
         for (int w = 0; w < kSortThreads / 32; ++w) orv |= s_or[w];
         const int nbits = orv ? 64 - __clzll(orv) : 0;
 
-        for (int lo = 0; lo < nbits; lo += 8) {
-            if (((orv >> lo) & 0xFFull) == 0) continue;  // digit constant across the group
-        if (((orv >> lo) & 0xFFull) == 0) continue;  // digit constant across the group: no-op pass
+        auto lsd = [&](int lo0) {
+        for (int lo = lo0; lo < nbits; lo += 8) {
+            if (((orv >> lo) & 0xFFull) == 0) continue;  // digit constant across the group: no-op pass
             for (int i = tid; i < (kSortThreads / 32) * 256; i += kSortThreads) (&cnt[0][0])[i] = 0;
             __syncthreads();
             uint32_t dig[kSortItems], rk[kSortItems];
@@ -800,6 +825,33 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
 #pragma unroll
             for (int j = 0; j < kSortItems; ++j) key[j] = buf[warp * 256 + j * 32 + lane];
             __syncthreads();
+        }
+        };
+        // Real keys rarely tie: rank by the KEY bits only (3 passes instead of ~5 with the index
+        // bits), then put tied keys back in index order with an odd-even transposition restricted
+        // to runs of equal keys (a run of length L settles in <= L rounds). Long runs (tie-heavy
+        // groups) fall back to the full composite passes.
+        const bool key_only = (orv >> 32) != 0 && (orv & 0xffffffffull) != 0;
+        lsd(key_only ? 32 : 0);
+        if (key_only) {
+            bool prev_sw = true, settled = false;
+            for (int it = 0; it < 64; ++it) {
+                bool sw = false;
+                for (uint32_t q = tid; 2 * q + 1 < len; q += kSortThreads) {
+                    const uint32_t p = 2 * q + (it & 1);
+                    if (p + 1 < len) {
+                        const unsigned long long x = buf[p], y = buf[p + 1];
+                        if ((x >> 32) == (y >> 32) && x < y) { buf[p] = y; buf[p + 1] = x; sw = true; }
+                    }
+                }
+                const bool any = __syncthreads_or(sw);
+                if (!any && !prev_sw) { settled = true; break; }
+                prev_sw = any;
+            }
+#pragma unroll
+            for (int j = 0; j < kSortItems; ++j) key[j] = buf[warp * 256 + j * 32 + lane];
+            __syncthreads();
+            if (!settled) lsd(0);  // tie-heavy group: full composite order
         }
 
         const uint32_t r = grp.rid;
