@@ -82,6 +82,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_PREFETCH_MB")) prefetch_mb_ = std::max(0, std::atoi(g));
     if (const char* g = std::getenv("RTK_NO_FUSED")) no_fused_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_NO_DENSE")) no_dense_ = *g && *g != '0';
+    if (const char* g = std::getenv("RTK_DENSE_BITS")) dense_bits_ = static_cast<uint32_t>(std::atoi(g));
     const char* cs = std::getenv("RTK_COUNT_STATS");
     count_stats_ = profile_ || (cs && *cs && *cs != '0');
 }
@@ -483,7 +484,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     for (uint32_t r : grow) {
         const RowReq& q = rows[r];
         if (sampled[r] || 2 * q.k < q.n || q.n <= kSortCap) { dense = false; break; }
-        const uint32_t bits = std::min<uint32_t>(fine_bits(q.n), msd_max_bits_);
+        const uint32_t bits = std::min<uint32_t>(dense_bits_ ? dense_bits_ : fine_bits(q.n), msd_max_bits_);
         SegSlot sl{cand_off[r], q.n, 0, r, 64u - bits, bits, 1u, q.in_off};
         dslots.push_back(sl);
     }

@@ -193,7 +193,8 @@ private:
     bool no_graph_events_ = true;   // no stats events inside graphs (RTK_GRAPH_EVENTS=1 keeps them)
     bool timing_ = false;           // rtk_set_timing: no graph replay, events around k_compact
     bool no_fused_ = false;
-    bool no_dense_ = false;         // RTK_NO_DENSE=1: dense rows are compacted too         // RTK_NO_FUSED=1: short rows take the general path too
+    bool no_dense_ = false;
+    uint32_t dense_bits_ = 0;       // RTK_DENSE_BITS: level-0 digit of dense rows (0: fine_bits)         // RTK_NO_DENSE=1: dense rows are compacted too         // RTK_NO_FUSED=1: short rows take the general path too
     int prefetch_mb_ = 24;          // L2 prefetch budget of k_compact (RTK_PREFETCH_MB)
     int clean_rows_ = 0;
     int clean_upto_ = 0;          // rows whose counters the last call left clean
