@@ -744,6 +744,123 @@ __device__ __forceinline__ void warp_sort_group(const SortGroup& grp, const Sort
     }
 }
 
+// One CTA group (<= 256 * IT composites): in-smem LSD radix sort (see k_sort_groups), IT items
+// per thread so the work follows the group size (512 / 1024 / 2048 slots).
+template <int IT>
+__device__ __forceinline__ void cta_sort_group(const SortGroup& grp, const SortArgs& g, unsigned long long* buf,
+                                               uint32_t (*cnt)[256], uint32_t* s_scan, unsigned long long* s_or) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned full = 0xffffffffu;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t len = grp.len;
+    const unsigned long long* src = (grp.buf ? g.buf1 : g.buf0) + grp.off;
+    unsigned long long key[IT];
+    const unsigned long long ref = src[0];
+    unsigned long long orv = 0;
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+        const uint32_t p = warp * (32 * IT) + j * 32 + lane;
+        key[j] = p < len ? src[p] : 0ull;
+        if (p < len) orv |= key[j] ^ ref;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) orv |= __shfl_xor_sync(full, orv, d);
+    if (lane == 0) s_or[warp] = orv;
+    __syncthreads();
+    orv = 0;
+    for (int w = 0; w < kSortThreads / 32; ++w) orv |= s_or[w];
+    const int nbits = orv ? 64 - __clzll(orv) : 0;
+
+    auto lsd = [&](int lo0) {
+    for (int lo = lo0; lo < nbits; lo += 8) {
+        if (((orv >> lo) & 0xFFull) == 0) continue;  // digit constant across the group: no-op pass
+        for (int i = tid; i < (kSortThreads / 32) * 256; i += kSortThreads) (&cnt[0][0])[i] = 0;
+        __syncthreads();
+        uint32_t dig[IT], rk[IT];
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
+            const uint32_t p = warp * (32 * IT) + j * 32 + lane;
+            // descending: rank by 255 - digit; padding always takes the last digit
+            dig[j] = p < len ? 255u - static_cast<uint32_t>((key[j] >> lo) & 0xFFu) : 255u;
+            const unsigned peers = __match_any_sync(full, dig[j]);
+            const uint32_t base = cnt[warp][dig[j]];
+            rk[j] = base + __popc(peers & lt);
+            __syncwarp();
+            if ((peers & lt) == 0) cnt[warp][dig[j]] = base + __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        // exclusive scan over counters in (digit, warp) order: thread t -> digit t, all 8 warps
+        {
+            constexpr int NW = kSortThreads / 32;
+            const int d = tid, w0 = 0;
+            uint32_t c[NW], sum = 0;
+#pragma unroll
+            for (int i = 0; i < NW; ++i) { c[i] = cnt[w0 + i][d]; sum += c[i]; }
+            uint32_t inc = sum;
+#pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const uint32_t o = __shfl_up_sync(full, inc, dd);
+                if (lane >= dd) inc += o;
+            }
+            if (lane == 31) s_scan[warp] = inc;
+            __syncthreads();
+            uint32_t pre = inc - sum;
+            for (int w = 0; w < warp; ++w) pre += s_scan[w];
+#pragma unroll
+            for (int i = 0; i < NW; ++i) { cnt[w0 + i][d] = pre; pre += c[i]; }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < IT; ++j) buf[cnt[warp][dig[j]] + rk[j]] = key[j];
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < IT; ++j) key[j] = buf[warp * (32 * IT) + j * 32 + lane];
+        __syncthreads();
+    }
+    };
+    // Real keys rarely tie: rank by the KEY bits only (3 passes instead of ~5 with the index
+    // bits), then put tied keys back in index order with an odd-even transposition restricted
+    // to runs of equal keys (a run of length L settles in <= L rounds). Long runs (tie-heavy
+    // groups) fall back to the full composite passes.
+    const bool key_only = (orv >> 32) != 0 && (orv & 0xffffffffull) != 0;
+    lsd(key_only ? 32 : 0);
+    if (key_only) {
+        bool prev_sw = true, settled = false;
+        for (int it = 0; it < 64; ++it) {
+            bool sw = false;
+            for (uint32_t q = tid; 2 * q + 1 < len; q += kSortThreads) {
+                const uint32_t p = 2 * q + (it & 1);
+                if (p + 1 < len) {
+                    const unsigned long long x = buf[p], y = buf[p + 1];
+                    if ((x >> 32) == (y >> 32) && x < y) { buf[p] = y; buf[p + 1] = x; sw = true; }
+                }
+            }
+            const bool any = __syncthreads_or(sw);
+            if (!any && !prev_sw) { settled = true; break; }
+            prev_sw = any;
+        }
+#pragma unroll
+        for (int j = 0; j < IT; ++j) key[j] = buf[warp * (32 * IT) + j * 32 + lane];
+        __syncthreads();
+        if (!settled) lsd(0);  // tie-heavy group: full composite order
+    }
+
+    const uint32_t r = grp.rid;
+    const uint64_t kr = g.row_k[r];
+    const uint64_t oo = g.row_out_off[r];
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+        const uint32_t p = warp * (32 * IT) + j * 32 + lane;
+        const uint64_t rank = grp.rank_base + p;
+        if (p >= len || rank >= kr) continue;
+        const unsigned long long K = key[j];
+        const uint32_t kk = static_cast<uint32_t>(K >> 32);
+        const uint32_t idx = ~static_cast<uint32_t>(K);
+        emit_rank(g, r, kr, oo, rank, kk, idx);
+    }
+}
+
 __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
     extern __shared__ unsigned long long buf[];  // kSortCap entries (dynamic: > 48 KB static)
     __shared__ uint32_t cnt[kSortThreads / 32][256];
@@ -760,113 +877,9 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
         const uint32_t gi = s_g;
         if (gi >= min(*g.groups.count, g.groups.cap)) break;
         const SortGroup grp = g.groups.groups[gi];
-        const uint32_t len = grp.len;
-        const unsigned long long* src = (grp.buf ? g.buf1 : g.buf0) + grp.off;
-        unsigned long long key[kSortItems];
-        const unsigned long long ref = src[0];
-        unsigned long long orv = 0;
-#pragma unroll
-        for (int j = 0; j < kSortItems; ++j) {
-            const uint32_t p = warp * 256 + j * 32 + lane;
-            key[j] = p < len ? src[p] : 0ull;
-            if (p < len) orv |= key[j] ^ ref;
-        }
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) orv |= __shfl_xor_sync(full, orv, d);
-        if (lane == 0) s_or[warp] = orv;
-        __syncthreads();
-        orv = 0;
-        for (int w = 0; w < kSortThreads / 32; ++w) orv |= s_or[w];
-        const int nbits = orv ? 64 - __clzll(orv) : 0;
-
-        auto lsd = [&](int lo0) {
-        for (int lo = lo0; lo < nbits; lo += 8) {
-            if (((orv >> lo) & 0xFFull) == 0) continue;  // digit constant across the group: no-op pass
-            for (int i = tid; i < (kSortThreads / 32) * 256; i += kSortThreads) (&cnt[0][0])[i] = 0;
-            __syncthreads();
-            uint32_t dig[kSortItems], rk[kSortItems];
-#pragma unroll
-            for (int j = 0; j < kSortItems; ++j) {
-                const uint32_t p = warp * 256 + j * 32 + lane;
-                // descending: rank by 255 - digit; padding always takes the last digit
-                dig[j] = p < len ? 255u - static_cast<uint32_t>((key[j] >> lo) & 0xFFu) : 255u;
-                const unsigned peers = __match_any_sync(full, dig[j]);
-                const uint32_t base = cnt[warp][dig[j]];
-                rk[j] = base + __popc(peers & lt);
-                __syncwarp();
-                if ((peers & lt) == 0) cnt[warp][dig[j]] = base + __popc(peers);
-                __syncwarp();
-            }
-            __syncthreads();
-            // exclusive scan over counters in (digit, warp) order: thread t -> digit t, all 8 warps
-            {
-                constexpr int NW = kSortThreads / 32;
-                const int d = tid, w0 = 0;
-                uint32_t c[NW], sum = 0;
-#pragma unroll
-                for (int i = 0; i < NW; ++i) { c[i] = cnt[w0 + i][d]; sum += c[i]; }
-                uint32_t inc = sum;
-#pragma unroll
-                for (int dd = 1; dd < 32; dd <<= 1) {
-                    const uint32_t o = __shfl_up_sync(full, inc, dd);
-                    if (lane >= dd) inc += o;
-                }
-                if (lane == 31) s_scan[warp] = inc;
-                __syncthreads();
-                uint32_t pre = inc - sum;
-                for (int w = 0; w < warp; ++w) pre += s_scan[w];
-#pragma unroll
-                for (int i = 0; i < NW; ++i) { cnt[w0 + i][d] = pre; pre += c[i]; }
-            }
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < kSortItems; ++j) buf[cnt[warp][dig[j]] + rk[j]] = key[j];
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < kSortItems; ++j) key[j] = buf[warp * 256 + j * 32 + lane];
-            __syncthreads();
-        }
-        };
-        // Real keys rarely tie: rank by the KEY bits only (3 passes instead of ~5 with the index
-        // bits), then put tied keys back in index order with an odd-even transposition restricted
-        // to runs of equal keys (a run of length L settles in <= L rounds). Long runs (tie-heavy
-        // groups) fall back to the full composite passes.
-        const bool key_only = (orv >> 32) != 0 && (orv & 0xffffffffull) != 0;
-        lsd(key_only ? 32 : 0);
-        if (key_only) {
-            bool prev_sw = true, settled = false;
-            for (int it = 0; it < 64; ++it) {
-                bool sw = false;
-                for (uint32_t q = tid; 2 * q + 1 < len; q += kSortThreads) {
-                    const uint32_t p = 2 * q + (it & 1);
-                    if (p + 1 < len) {
-                        const unsigned long long x = buf[p], y = buf[p + 1];
-                        if ((x >> 32) == (y >> 32) && x < y) { buf[p] = y; buf[p + 1] = x; sw = true; }
-                    }
-                }
-                const bool any = __syncthreads_or(sw);
-                if (!any && !prev_sw) { settled = true; break; }
-                prev_sw = any;
-            }
-#pragma unroll
-            for (int j = 0; j < kSortItems; ++j) key[j] = buf[warp * 256 + j * 32 + lane];
-            __syncthreads();
-            if (!settled) lsd(0);  // tie-heavy group: full composite order
-        }
-
-        const uint32_t r = grp.rid;
-        const uint64_t kr = g.row_k[r];
-        const uint64_t oo = g.row_out_off[r];
-#pragma unroll
-        for (int j = 0; j < kSortItems; ++j) {
-            const uint32_t p = warp * 256 + j * 32 + lane;
-            const uint64_t rank = grp.rank_base + p;
-            if (p >= len || rank >= kr) continue;
-            const unsigned long long K = key[j];
-            const uint32_t kk = static_cast<uint32_t>(K >> 32);
-            const uint32_t idx = ~static_cast<uint32_t>(K);
-            emit_rank(g, r, kr, oo, rank, kk, idx);
-        }
+        if (grp.len <= 512) cta_sort_group<2>(grp, g, buf, cnt, s_scan, s_or);
+        else if (grp.len <= 1024) cta_sort_group<4>(grp, g, buf, cnt, s_scan, s_or);
+        else cta_sort_group<8>(grp, g, buf, cnt, s_scan, s_or);
         __syncthreads();
     }
     // warp groups (<= kWarpGroupMax composites): one warp each, bitonic in registers, no shared
