@@ -208,13 +208,20 @@ def main():
             ms = python_loop(kk, steps, warmup)
         # kernel share: k_compact bracketed by CUDA events on its stream (library timing mode:
         # no graph replay), on separate steps so no stats readback sits inside the timed region
-        launches = R.last_stats(local).kernel_launches * steps
+        # (on the local top-k call: with N > 1 the merge that follows is a separate small call)
         R.set_timing(True, local)
         comp = []
+        per_step = 0
         for _ in range(min(steps, 10)):
-            step(kk)
-            comp.append(R.last_stats(local).compact_ms)
+            rtk.topk(x, kk)
+            st = R.last_stats(local)
+            comp.append(st.compact_ms)
+            per_step = st.kernel_launches
         R.set_timing(False, local)
+        if world > 1:  # + the merge of the gathered candidates (rtk_merge_shards)
+            step(kk)
+            per_step += R.last_stats(local).kernel_launches
+        launches = per_step * steps
         if world > 1:
             t = torch.tensor([statistics.mean(ms)], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)

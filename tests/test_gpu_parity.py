@@ -326,3 +326,26 @@ def test_16bit_batch_llm_rows(cuda, k):
         _, wi, _ = O.ref_topk(np.ascontiguousarray(x32[t]), k, 0, grid=4)
         assert np.array_equal(gi[t].astype(np.uint64), wi.astype(np.uint64)), f"row {t}"
         assert np.array_equal(gv[t], h[t][wi.astype(np.int64)]), f"row {t} values"
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+@pytest.mark.parametrize("kind", [UNIFORM, ZIPF])
+def test_sharded_query_merge_on_device(cuda, G, kind):
+    # SURVEY §8e / C5 on one device: per-shard rtk_topk (contiguous index ranges), the shard
+    # blocks concatenated in shard order (the NCCL all-gather's layout), rtk_merge_shards; must
+    # equal rtk::topk on the whole query — ties across shard boundaries included (Zipf).
+    import torch
+    rtk = _rtk()
+    from paper_2501_14336_b200 import sharded as SH
+    n, k = (1 << 20) + 13, 4096
+    x = O.ref_generate(kind, n, 4242 + G, dtype=np.float32, b=1.0)
+    t = torch.from_numpy(x).to(cuda)
+    vals, idx, bases = [], [], []
+    for g in range(G):
+        s0, ln = SH.shard_bounds(n, G, g)
+        r = rtk.topk(t[s0:s0 + ln], k)
+        vals.append(r.values)
+        idx.append(r.indices)
+        bases.append(s0)
+    m = rtk.merge_shards(torch.cat(vals), torch.cat(idx), [k] * G, bases, k)
+    assert_same((m.values, m.indices, m.pivot), O.ref_topk(x, k, 0, grid=4), f"G={G} kind={kind}")
