@@ -267,8 +267,10 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ unsigned long long smp[];
-    __shared__ __align__(16) uint32_t hist[kBins];
-    __shared__ __align__(16) uint32_t hred[kBins];  // this CTA's reduced slice (first SL bins)
+    // double-buffered by pass parity: a pass never rewrites what another CTA may still read from
+    // the previous pass, so each pass needs two cluster barriers instead of three
+    __shared__ __align__(16) uint32_t hist2[2][kBins];
+    __shared__ __align__(16) uint32_t hred2[2][kBins];  // this CTA's reduced slice (first SL bins)
     __shared__ uint32_t s_wsum[32];
     __shared__ unsigned long long s_res[3];
     const unsigned CS = cluster.num_blocks();
@@ -311,7 +313,9 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
     unsigned long long prefix = 0, k_rem = sr.k[j], above = 0;
     const unsigned long long target = sr.target[j];
     unsigned int pos = 53;
-    for (;;) {
+    for (uint32_t ps = 0;; ++ps) {
+        uint32_t* hist = hist2[ps & 1];
+        uint32_t* hred = hred2[ps & 1];
         for (int b = tid; b < 4 * kBins; b += blockDim.x) hsub[b] = 0;
         for (int b = tid; b < kBins; b += blockDim.x) hred[b] = 0;
         __syncthreads();
@@ -375,7 +379,7 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
             else { s_res[0] = b1; s_res[1] = before + c0; s_res[2] = c1; }
         }
         stamp();
-        cluster.sync();  // all DSMEM reads done before anyone rewrites its histogram
+        __syncthreads();  // s_res read by every thread before it changes
         stamp();
         if (s_res[0] == ~0ull) break;  // rank outside sample (cannot happen: k <= sample size)
         prefix |= s_res[0] << pos;
@@ -403,6 +407,7 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
         alt = t;
         pos = pos == 9 ? 0u : pos - 11u;
     }
+    cluster.sync();  // no CTA leaves while another may still read its shared memory
     if (crank == 0 && tid == 0) T[sr.rid[j]] = prefix;
     stamp();
     if (dbg && blockIdx.x == 0 && threadIdx.x == 0) dbg[31] = ndbg;
