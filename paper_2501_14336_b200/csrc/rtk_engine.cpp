@@ -82,6 +82,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_PREFETCH_MB")) prefetch_mb_ = std::max(0, std::atoi(g));
     if (const char* g = std::getenv("RTK_NO_FUSED")) no_fused_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_NO_DENSE")) no_dense_ = *g && *g != '0';
+    if (const char* g = std::getenv("RTK_SPARSE_MAX")) sparse_max_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_DENSE_BITS")) dense_bits_ = static_cast<uint32_t>(std::atoi(g));
     const char* cs = std::getenv("RTK_COUNT_STATS");
     count_stats_ = profile_ || (cs && *cs && *cs != '0');
@@ -703,6 +704,7 @@ PlanArgs Engine::plan_args(const Call& c, const FinishPrep& f) {
     pa.done = done_.as<uint32_t>();
     pa.max_bits = static_cast<uint32_t>(msd_max_bits_);
     pa.prefetch_mb = static_cast<uint32_t>(prefetch_mb_);
+    pa.sparse_max = static_cast<uint32_t>(sparse_max_);
     return pa;
 }
 

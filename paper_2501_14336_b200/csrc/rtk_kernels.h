@@ -188,6 +188,7 @@ struct PlanArgs {         // per-row plan after the compaction (fused into k_com
     uint32_t* done;          // per state row: tiles finished
     uint32_t max_bits;       // cap on the level-0 MSD digit (RTK_MSD_BITS; default kMsdMaxBits)
     uint32_t prefetch_mb;    // L2 prefetch budget of k_compact's prologue (RTK_PREFETCH_MB)
+    uint32_t sparse_max;     // warp-tiles with <= this many hits take the set-bits (L2 re-read) path
 };
 
 struct SortArgs {
