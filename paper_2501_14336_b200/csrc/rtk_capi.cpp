@@ -107,64 +107,47 @@ std::vector<uint64_t> packed_out_offsets(const uint64_t* ks, uint64_t B) {
     return o;
 }
 
-struct ScaleDecision {
-    bool scale = false;
-    float a_s = 0.0f;
-    uint64_t a_index = 0;
-};
-
-// scaled_topk's decision (scaling.hpp:47-67): adaptive trigger on the exact first-window
-// histogram, then a_s = input[mt19937_64(seed)() % n].
-ScaleDecision decide_scale(Engine& e, const float* d_in, uint64_t n, uint64_t k, int order, int mode,
-                           double tau, uint64_t seed, const rtk_cfg& cfg, cudaStream_t s) {
-    ScaleDecision d;
-    if (mode != RTK_SCALE_OFF && mode != RTK_SCALE_ALWAYS && mode != RTK_SCALE_ADAPTIVE)
-        throw Error{RTK_INVALID_ARGUMENT, "bad scale mode"};
-    d.scale = mode == RTK_SCALE_ALWAYS;
-    if (mode == RTK_SCALE_ADAPTIVE) {
-        std::vector<uint64_t> h = e.first_digit_hist(reinterpret_cast<const uint32_t*>(d_in), n, cfg.d,
-                                                     order, s);
-        e.stats.passes += 1;
-        e.stats.elements_scanned += n;
-        // select_bin (engine.hpp:231-241)
-        uint64_t total = 0;
-        for (uint64_t c : h) total += c;
-        if (k == 0 || k > total) throw Error{RTK_RANK_OUT_OF_RANGE, "select_bin: rank outside histogram total"};
-        uint64_t cum = 0;
-        size_t bin = 0;
-        for (size_t b = h.size(); b-- > 0;) {
-            cum += h[b];
-            if (cum >= k) {
-                bin = b;
-                break;
-            }
-        }
-        d.scale = static_cast<double>(h[bin]) > tau * static_cast<double>(n);
-    }
-    if (d.scale) {
-        std::mt19937_64 rng(seed);
-        d.a_index = rng() % n;
-        const uint32_t bits = e.read_word(reinterpret_cast<const uint32_t*>(d_in), d.a_index, s);
-        std::memcpy(&d.a_s, &bits, 4);
-    }
-    return d;
-}
-
+// scaled_topk (scaling.hpp:47-79). The decision is taken on the device: Adaptive runs the
+// exact first-window histogram and a one-CTA select_bin/trigger kernel; Always only fetches
+// a_s. Every pipeline kernel reads {flag, a_s} at its start, so no host round trip separates
+// the trigger pass from the selection. a_index = mt19937_64(seed)() % n (draw_scale) is drawn
+// on the host; values are re-read from the input by index (scaling.hpp:74-75).
 void run_scaled(Engine& e, const float* d_in, uint64_t n, uint64_t k, int order, int mode, double tau,
                 uint64_t seed, float* d_vals, uint64_t* d_idx, float* d_piv, rtk_scale_info* info,
                 const rtk_cfg& cfg, cudaStream_t s) {
-    e.stats = rtk_stats{};  // the trigger pass of this call is added to the run's counters below
-    ScaleDecision d = decide_scale(e, d_in, n, k, order, mode, tau, seed, cfg, s);
-    const rtk_stats pre = e.stats;
-    e.run(reinterpret_cast<const uint32_t*>(d_in), RTK_F32, order, d.scale, d.a_s, /*gather=*/d.scale,
-          {RowReq{0, n, k, 0}}, reinterpret_cast<uint32_t*>(d_vals), d_idx,
-          reinterpret_cast<uint32_t*>(d_piv), s);
-    e.stats.passes += pre.passes;
-    e.stats.elements_scanned += pre.elements_scanned;
+    if (mode != RTK_SCALE_OFF && mode != RTK_SCALE_ALWAYS && mode != RTK_SCALE_ADAPTIVE)
+        throw Error{RTK_INVALID_ARGUMENT, "bad scale mode"};
+    if (mode == RTK_SCALE_OFF) {
+        e.run(reinterpret_cast<const uint32_t*>(d_in), RTK_F32, order, false, 0.0f, false, {RowReq{0, n, k, 0}},
+              reinterpret_cast<uint32_t*>(d_vals), d_idx, reinterpret_cast<uint32_t*>(d_piv), s);
+        if (info) *info = rtk_scale_info{0, 0.0f, 0};
+        return;
+    }
+    std::mt19937_64 rng(seed);
+    const uint64_t a_index = rng() % n;
+    e.enqueue_scale_decide(reinterpret_cast<const uint32_t*>(d_in), n, k, cfg.d, order,
+                           mode == RTK_SCALE_ALWAYS ? 1 : 2, tau, a_index, s);
+    e.set_adapt(e.device_scale());
+    try {
+        e.run(reinterpret_cast<const uint32_t*>(d_in), RTK_F32, order, false, 0.0f, /*gather=*/true,
+              {RowReq{0, n, k, 0}}, reinterpret_cast<uint32_t*>(d_vals), d_idx,
+              reinterpret_cast<uint32_t*>(d_piv), s);
+    } catch (...) {
+        e.set_adapt(nullptr);
+        throw;
+    }
+    e.set_adapt(nullptr);
+    if (mode == RTK_SCALE_ADAPTIVE) {
+        e.stats.passes += 1;
+        e.stats.elements_scanned += n;
+    }
     if (info) {
-        info->scaled = d.scale ? 1 : 0;
-        info->a_s = d.scale ? d.a_s : 0.0f;
-        info->a_index = d.scale ? d.a_index : 0;
+        bool sc = false;
+        float a = 0.0f;
+        e.scale_result(&sc, &a);
+        info->scaled = sc ? 1 : 0;
+        info->a_s = sc ? a : 0.0f;
+        info->a_index = sc ? a_index : 0;
     }
 }
 

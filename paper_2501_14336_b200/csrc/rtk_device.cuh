@@ -60,7 +60,19 @@ struct InputSrc {
     int smallest;
     int scaled;
     float a_s;
+    // scaled_topk decided on the device (ScaleMode::Adaptive / Always): {scale flag, a_s bits},
+    // written by k_scale_decide; every kernel resolves it once at its start (resolve_src)
+    const uint32_t* adapt;
 };
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void resolve_src(InputSrc& s) {
+    if (s.adapt) {
+        s.scaled = static_cast<int>(__ldcg(s.adapt));
+        s.a_s = __uint_as_float(__ldcg(s.adapt + 1));
+    }
+}
+#endif
 
 __device__ __forceinline__ uint32_t encode_f32_bits(uint32_t raw, bool smallest) {
     // KeyCodec<float>::encode, keycodec.hpp:57-62
@@ -114,11 +126,12 @@ __device__ __forceinline__ uint32_t make_key(const InputSrc& s, uint32_t raw) {
 
 // Compile-time key transforms for the streaming kernels (KM = key mode).
 enum : int { kKmF32L = 0, kKmF32S = 1, kKmF32LScaled = 2, kKmF32SScaled = 3, kKmU32L = 4, kKmU32S = 5,
-             kKmF16L = 6, kKmF16S = 7 };
+             kKmF16L = 6, kKmF16S = 7, kKmF32LAdapt = 8, kKmF32SAdapt = 9 };
 
-inline int key_mode(int dtype, int smallest, int scaled) {
+inline int key_mode(int dtype, int smallest, int scaled, const uint32_t* adapt = nullptr) {
     if (dtype == kF16) return smallest ? kKmF16S : kKmF16L;
     if (dtype != kF32) return smallest ? kKmU32S : kKmU32L;
+    if (adapt) return smallest ? kKmF32SAdapt : kKmF32LAdapt;
     return (scaled ? 2 : 0) + (smallest ? 1 : 0);
 }
 
@@ -126,7 +139,14 @@ template <int KM>
 __host__ __device__ constexpr bool km_is16() { return KM == kKmF16L || KM == kKmF16S; }
 
 template <int KM>
-__device__ __forceinline__ uint32_t key_of(uint32_t raw, float a_s) {
+__device__ __forceinline__ uint32_t key_of(uint32_t raw, const InputSrc& in) {
+    const float a_s = in.a_s;
+    if (KM == kKmF32LAdapt || KM == kKmF32SAdapt) {  // decided on the device: kernel-uniform branch
+        if (in.scaled) raw = __float_as_uint(__fsub_rn(__uint_as_float(raw), a_s));
+        const uint32_t m = static_cast<uint32_t>(static_cast<int32_t>(raw) >> 31) | 0x80000000u;
+        const uint32_t bits = raw ^ m;
+        return KM == kKmF32SAdapt ? ~bits : bits;
+    }
     if (KM == kKmF16L || KM == kKmF16S) {
         // raw = zero-extended 16-bit word; sign-flip map as mask arithmetic, key in the high half
         const uint32_t m = ((raw & 0x8000u) ? 0xFFFFu : 0x8000u);

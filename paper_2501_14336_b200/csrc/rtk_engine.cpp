@@ -92,6 +92,7 @@ Engine::~Engine() {
     if (graph_.exec) cudaGraphExecDestroy(graph_.exec);
     if (cap_s_) cudaStreamDestroy(cap_s_);
     if (hmap_) cudaFreeHost(hmap_);
+    if (hscale_) cudaFreeHost(hscale_);
     if (pin_) cudaFreeHost(pin_);
     if (hctl_) cudaFreeHost(hctl_);
     if (hcount_) cudaFreeHost(hcount_);
@@ -99,7 +100,7 @@ Engine::~Engine() {
         if (e) cudaEventDestroy(e);
     for (DevBuf* b : {&arena_, &sel_, &T_, &count_, &kmin_, &kmax_, &ghist_, &samples_, &cand_a_,
                       &cand_b_, &seg_hist_, &gcursor_, &bstart_, &dcap_, &dcoff_, &ctl_, &row_fail_, &groups_, &slots0_, &slotsA_, &slotsB_, &done_, &seg_ticket_, &wgroups_, &ctot_, &sig_, &io_in, &io_vals, &io_idx,
-                      &io_piv, &io_aux})
+                      &io_piv, &io_aux, &adapt_buf_, &scale_hist_, &scale_plan_})
         b->release();
 }
 
@@ -198,6 +199,7 @@ uint32_t Engine::read_word(const uint32_t* d, uint64_t i, cudaStream_t s) {
 // ---------------------------------------------------------------------------------------
 bool Engine::CallKey::operator==(const CallKey& o) const {
     if (base != o.base || dtype != o.dtype || smallest != o.smallest || scaled != o.scaled || gather != o.gather ||
+        adapt != o.adapt ||
         a_s_bits != o.a_s_bits || vals != o.vals || idx != o.idx || piv != o.piv || s != o.s ||
         rows.size() != o.rows.size())
         return false;
@@ -241,6 +243,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
     key.scaled = scaled ? 1 : 0;
     key.gather = gather ? 1 : 0;
     std::memcpy(&key.a_s_bits, &a_s, 4);
+    key.adapt = adapt_;
     key.vals = d_vals;
     key.idx = d_idx;
     key.piv = d_pivots;
@@ -364,7 +367,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     self_clean_ = !count_stats_ && self_clean_ok_;  // the main finish resets counters; fallback/deeper levels never
     clean_rows_ = 0;
     did_init_ = false;
-    InputSrc src{d_base, dtype, smallest, scaled ? 1 : 0, a_s};
+    InputSrc src{d_base, dtype, smallest, scaled ? 1 : 0, a_s, adapt_};
     const uint64_t base_words = reinterpret_cast<uintptr_t>(d_base) / elem_bytes(dtype);  // base in elements
 
     // ---- 1. per-row plan: sample size s, sample rank r', candidate capacity -------------
@@ -1034,13 +1037,58 @@ std::vector<uint64_t> Engine::first_digit_hist(const uint32_t* d_in, uint64_t n,
     uint8_t* D = upload(P, s);
     Rows rr{1, at<uint32_t>(D, o_rid), at<uint64_t>(D, o_off), at<uint64_t>(D, o_len),
             at<uint32_t>(D, o_lead), at<uint64_t>(D, o_tile)};
-    InputSrc src{d_in, kF32, smallest, 0, 0.0f};
+    InputSrc src{d_in, kF32, smallest, 0, 0.0f, nullptr};
     launch_first_digit_hist(tiles.back(), rr, src, d, h.as<unsigned long long>(), s);
     std::vector<uint64_t> out(nb);
     check(cudaMemcpyAsync(out.data(), h.p, 8 * nb, cudaMemcpyDeviceToHost, s), "d2h");
     sync(s, "first digit hist");
     release_retired();
     return out;
+}
+
+void Engine::enqueue_scale_decide(const uint32_t* d_in, uint64_t n, uint64_t k, unsigned d, int smallest,
+                                  int mode, double tau, uint64_t a_index, cudaStream_t s) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    if (!hscale_) {
+        check(cudaHostAlloc(reinterpret_cast<void**>(&hscale_), 16, cudaHostAllocMapped), "cudaHostAlloc");
+        std::memset(hscale_, 0, 16);
+        check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_hscale_), hscale_, 0), "mapped pointer");
+    }
+    adapt_buf_.ensure(16);
+    const uint64_t nb = uint64_t(1) << d;
+    unsigned long long* hist = nullptr;
+    if (mode == 2) {
+        scale_hist_.ensure(8 * nb);
+        hist = scale_hist_.as<unsigned long long>();
+        check(cudaMemsetAsync(hist, 0, 8 * nb, s), "memset");
+        // one-row plan of the trigger pass in its own buffer (not the call arena, whose pinned
+        // staging the next run() may rewrite while this copy is pending); re-sent on change only
+        const uint64_t base_words = reinterpret_cast<uintptr_t>(d_in) / 4;
+        const uint32_t lead = static_cast<uint32_t>(base_words & 7);
+        const uint64_t ntiles = ceil_div(lead + n, kTile);
+        if (d_in != scale_plan_in_ || n != scale_plan_n_ || !scale_plan_.p) {
+            scale_plan_.ensure(64);
+            uint64_t plan[8] = {0, 0, n, lead, 0, ntiles, 0, 0};  // rid | off | len | lead | tiles[2]
+            // pageable source: the copy is staged before cudaMemcpyAsync returns
+            check(cudaMemcpyAsync(scale_plan_.p, plan, sizeof(plan), cudaMemcpyHostToDevice, s), "plan");
+            scale_plan_in_ = d_in;
+            scale_plan_n_ = n;
+        }
+        uint8_t* D = scale_plan_.as<uint8_t>();
+        Rows rr{1, at<uint32_t>(D, 0), at<uint64_t>(D, 8), at<uint64_t>(D, 16), at<uint32_t>(D, 24),
+                at<uint64_t>(D, 32)};
+        InputSrc src{d_in, kF32, smallest, 0, 0.0f, nullptr};
+        launch_first_digit_hist(ntiles, rr, src, d, hist, s);
+    }
+    launch_scale_decide(mode, hist, static_cast<uint32_t>(nb), n, k, tau, d_in, a_index,
+                        adapt_buf_.as<uint32_t>(), d_hscale_, s);
+}
+
+void Engine::scale_result(bool* scaled, float* a_s) const {
+    const volatile uint32_t* h = hscale_;
+    *scaled = h && h[0] != 0;
+    const uint32_t bits = h ? h[1] : 0u;
+    std::memcpy(a_s, &bits, 4);
 }
 
 void Engine::remap(uint64_t k, const uint64_t* d_cand_idx, const std::vector<uint64_t>& block_start,

@@ -63,6 +63,16 @@ public:
 
     uint32_t read_word(const uint32_t* d, uint64_t i, cudaStream_t s);
 
+    // scaled_topk decided on the device (scaling.hpp:47-67): first-window histogram + one-CTA
+    // select_bin / trigger / a_s fetch, stream-ordered, no host round trip. The next run() with
+    // use_device_scale() reads the decision in every kernel. mode: 1 Always, 2 Adaptive.
+    void enqueue_scale_decide(const uint32_t* d_in, uint64_t n, uint64_t k, unsigned d, int smallest,
+                              int mode, double tau, uint64_t a_index, cudaStream_t s);
+    const uint32_t* device_scale() const { return adapt_buf_.as<uint32_t>(); }
+    // {flag, a_s bits} of the last decision (valid once the following run() returned)
+    void scale_result(bool* scaled, float* a_s) const;
+    void set_adapt(const uint32_t* p) { adapt_ = p; }
+
     // stats of the last call; total_ms is resolved lazily (waits for the call's last event)
     const rtk_stats& last_stats();
     void set_timing(bool on) { timing_ = on; }
@@ -150,6 +160,7 @@ private:
         const uint32_t* base = nullptr;
         int dtype = 0, smallest = 0, scaled = 0, gather = 0;
         uint32_t a_s_bits = 0;
+        const uint32_t* adapt = nullptr;
         void *vals = nullptr, *idx = nullptr, *piv = nullptr;
         cudaStream_t s = nullptr;
         std::vector<RowReq> rows;
@@ -227,6 +238,12 @@ private:
     uint32_t bar_gen_ = 0;        // grid-barrier target of the level-0 MSD (ctl[7], reset per call)
     int msd_q_max_ = 32;          // clusters per huge slot (RTK_MSD_Q)
     int msd_max_bits_ = kMsdMaxBits;  // RTK_MSD_BITS
+    const uint32_t* adapt_ = nullptr;  // device scale decision read by the next run() (set_adapt)
+    DevBuf adapt_buf_, scale_hist_, scale_plan_;
+    uint32_t* hscale_ = nullptr;       // mapped {flag, a_s bits} written by k_scale_decide
+    uint32_t* d_hscale_ = nullptr;
+    const uint32_t* scale_plan_in_ = nullptr;  // input the cached first-window plan describes
+    uint64_t scale_plan_n_ = 0;
 };
 
 }  // namespace rtk_b200

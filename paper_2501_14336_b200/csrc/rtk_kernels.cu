@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(kThreads) k_radix_pass(Rows rows, InputSrc in,
                                                          unsigned long long* ghist) {
     __shared__ uint32_t h[kBins];
     __shared__ int s_last;
+    resolve_src(in);
     for (int b = threadIdx.x; b < kBins; b += kThreads) h[b] = 0;
     __syncthreads();
 
@@ -258,6 +259,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc in, uint64_t* T) {
     pdl_trigger();  // k_compact may launch now (it waits for T in griddepcontrol.wait)
+    resolve_src(in);
     unsigned long long* dbg = sr.dbg;
     int ndbg = 0;
     auto stamp = [&]() {
@@ -467,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         }
     }
     pdl_wait();
+    resolve_src(in);  // scaled_topk decided on the device (k_scale_decide)
 
     auto warp_flush = [&]() {  // warp-uniform
         if (wcur == 0) return;
@@ -552,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
             for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
                 for (int i = 0; i < kVec; ++i) {
-                    const uint32_t key = key_of<KM>(v[u][i], in.a_s);
+                    const uint32_t key = key_of<KM>(v[u][i], in);
                     v[u][i] = key;
                     mask |= static_cast<uint32_t>(key >= thi) << (u * kVec + i);
                 }
@@ -561,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
             for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
                 for (int i = 0; i < kVec; ++i) {
-                    const uint32_t key = key_of<KM>(v[u][i], in.a_s);
+                    const uint32_t key = key_of<KM>(v[u][i], in);
                     v[u][i] = key;
                     const uint32_t l = (u * kThreads + threadIdx.x) * kVec + i;
                     mask |= static_cast<uint32_t>(key >= thi && l >= vlo && l < vhi) << (u * kVec + i);
@@ -605,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
                     raw = __ldg(reinterpret_cast<const unsigned short*>(in.base) + tp + l);
                 else
                     raw = __ldg(in.base + tp + l);
-                const uint32_t key = key_of<KM>(raw, in.a_s);
+                const uint32_t key = key_of<KM>(raw, in);
                 stage[o++] = (static_cast<unsigned long long>(key) << 32) | (nidx0 - l);
             }
             wcur += wtot;
@@ -707,6 +710,60 @@ __global__ void __launch_bounds__(kThreads) k_first_digit_hist(Rows rows, InputS
 }
 
 // ----------------------------------------------------------------------------------------
+// k_scale_decide: scaled_topk's decision on the device (scaling.hpp:47-67) — no host round trip.
+// mode 1 (Always): scale. mode 2 (Adaptive): select_bin on the exact first-window histogram
+// (engine.hpp:231-241: first bin from the top whose cumulative count reaches k) and scale iff
+// that bin holds more than tau * n keys. a_s = x[a_index] (the index is drawn on the host with
+// mt19937_64(seed) exactly as draw_scale does). out = {flag, a_s bits}; host_out (mapped, may be
+// null) receives {flag, a_s bits} for ScaleInfo.
+// ----------------------------------------------------------------------------------------
+__global__ void k_scale_decide(int mode, const unsigned long long* hist, uint32_t nbins, uint64_t n, uint64_t k,
+                               double tau, const uint32_t* x, uint64_t a_index, uint32_t* out,
+                               volatile uint32_t* host_out) {
+    __shared__ unsigned long long s_warp[32];
+    __shared__ int s_fat;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_fat = mode == 1;
+    __syncthreads();
+    if (mode == 2) {
+        // descending cumulative scan over nbins (<= 65536) with 1024 threads
+        const uint32_t per = (nbins + blockDim.x - 1) / blockDim.x;
+        unsigned long long sum = 0;
+        for (uint32_t i = 0; i < per; ++i) {
+            const uint32_t b = tid * per + i;  // b-th bin from the top
+            if (b < nbins) sum += hist[nbins - 1 - b];
+        }
+        unsigned long long tot;
+        const unsigned long long before = block_excl_scan(sum, s_warp, &tot);
+        if (before < k && before + sum >= k) {
+            unsigned long long cum = before;
+            for (uint32_t i = 0; i < per; ++i) {
+                const uint32_t b = tid * per + i;
+                if (b >= nbins) break;
+                const unsigned long long c = hist[nbins - 1 - b];
+                if (cum + c >= k) {
+                    s_fat = static_cast<double>(c) > tau * static_cast<double>(n);
+                    break;
+                }
+                cum += c;
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const uint32_t fat = s_fat ? 1u : 0u;
+        const uint32_t a = fat ? __ldg(x + a_index) : 0u;
+        out[0] = fat;
+        out[1] = a;
+        if (host_out) {
+            host_out[0] = fat;
+            host_out[1] = a;
+            __threadfence_system();
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------------------
 // Launchers. Streaming kernels run as persistent grids: resident CTAs per SM (occupancy API)
 // x SM count, capped by the tile count.
 // ----------------------------------------------------------------------------------------
@@ -783,13 +840,15 @@ void launch_compact(uint64_t tiles, const Rows& rows, const InputSrc& in, const 
                     uint64_t* cand, const uint64_t* cand_off, const uint64_t* cap,
                     unsigned long long* count, unsigned long long* kmin, unsigned long long* kmax,
                     const PlanArgs& pa, cudaStream_t s) {
-    switch (key_mode(in.dtype, in.smallest, in.scaled)) {
+    switch (key_mode(in.dtype, in.smallest, in.scaled, in.adapt)) {
         case kKmF32L: compact_km<kKmF32L>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
         case kKmF32S: compact_km<kKmF32S>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
         case kKmF32LScaled: compact_km<kKmF32LScaled>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
         case kKmF32SScaled: compact_km<kKmF32SScaled>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
         case kKmU32L: compact_km<kKmU32L>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
         case kKmF16L: compact_km<kKmF16L>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
+        case kKmF32LAdapt: compact_km<kKmF32LAdapt>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
+        case kKmF32SAdapt: compact_km<kKmF32SAdapt>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
         case kKmF16S: compact_km<kKmF16S>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
         default: compact_km<kKmU32S>(tiles, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa, s); break;
     }
@@ -805,6 +864,12 @@ void launch_first_digit_hist(uint64_t tiles, const Rows& rows, const InputSrc& i
     const size_t smem = d <= 13 ? (static_cast<size_t>(1) << d) * sizeof(uint32_t) : 0;
     const int grid = persistent_grid(k_first_digit_hist, kThreads, smem, tiles);
     k_first_digit_hist<<<grid, kThreads, smem, s>>>(rows, in, d, ghist);
+}
+
+void launch_scale_decide(int mode, const unsigned long long* hist, uint32_t nbins, uint64_t n, uint64_t k,
+                         double tau, const uint32_t* x, uint64_t a_index, uint32_t* out,
+                         volatile uint32_t* host_out, cudaStream_t s) {
+    k_scale_decide<<<1, 1024, 0, s>>>(mode, hist, nbins, n, k, tau, x, a_index, out, host_out);
 }
 
 void launch_remap_idx(uint64_t n, const uint64_t* cand_idx, uint32_t nblocks,

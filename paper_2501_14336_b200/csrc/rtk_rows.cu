@@ -183,6 +183,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a);
 template <int KM, int CAND, int STAGES, int SAMPLE>
 __global__ void __launch_bounds__(kRowThreads, 2) k_rows_fused(RowsFusedArgs a) {
     __shared__ uint32_t s_tail;
+    resolve_src(a.in);
     rows_fused_body<KM, CAND, STAGES, SAMPLE>(a);
     call_tail(a.tail, &s_tail);  // only when this is the call's last kernel
 }
@@ -296,7 +297,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
         uint32_t mask = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            key[i] = key_of<KM>(key[i], a.in.a_s);
+            key[i] = key_of<KM>(key[i], a.in);
             const bool hit = ((valid >> i) & 1u) && (key[i] > thi || (key[i] == thi && ~(ibase + i) >= tlo));
             mask |= static_cast<uint32_t>(hit) << i;
         }
@@ -538,13 +539,15 @@ static void rows_km(int R, const RowsFusedArgs& a, cudaStream_t s) {
 
 template <int CAND, int STAGES, int SAMPLE>
 static void rows_variant(int R, const RowsFusedArgs& a, cudaStream_t s) {
-    switch (key_mode(a.in.dtype, a.in.smallest, a.in.scaled)) {
+    switch (key_mode(a.in.dtype, a.in.smallest, a.in.scaled, a.in.adapt)) {
         case kKmF32L: rows_km<kKmF32L, CAND, STAGES, SAMPLE>(R, a, s); break;
         case kKmF32S: rows_km<kKmF32S, CAND, STAGES, SAMPLE>(R, a, s); break;
         case kKmF32LScaled: rows_km<kKmF32LScaled, CAND, STAGES, SAMPLE>(R, a, s); break;
         case kKmF32SScaled: rows_km<kKmF32SScaled, CAND, STAGES, SAMPLE>(R, a, s); break;
         case kKmU32L: rows_km<kKmU32L, CAND, STAGES, SAMPLE>(R, a, s); break;
         case kKmF16L: rows_km<kKmF16L, CAND, STAGES, SAMPLE>(R, a, s); break;
+        case kKmF32LAdapt: rows_km<kKmF32LAdapt, CAND, STAGES, SAMPLE>(R, a, s); break;
+        case kKmF32SAdapt: rows_km<kKmF32SAdapt, CAND, STAGES, SAMPLE>(R, a, s); break;
         case kKmF16S: rows_km<kKmF16S, CAND, STAGES, SAMPLE>(R, a, s); break;
         default: rows_km<kKmU32S, CAND, STAGES, SAMPLE>(R, a, s); break;
     }

@@ -437,6 +437,7 @@ __device__ __forceinline__ void msd_stream_in(const InputSrc& in, uint64_t row_i
 __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* slots, const uint64_t* src,
                                                                 uint64_t* dst, FineArgs fa) {
     namespace cg = cooperative_groups;
+    resolve_src(fa.in);
     cg::cluster_group cluster = cg::this_cluster();
     // [0,B): counts -> intra-cluster offsets -> cursors; [B, B+slice): slice totals -> starts;
     // [B+slice, B+2 slice): cross-cluster offsets (Q > 1)

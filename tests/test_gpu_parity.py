@@ -221,6 +221,23 @@ def test_scaled_matches_reference(cuda, mode):
         assert_same((r.values, r.indices, r.pivot), (wv, wi, wp), f"scaled mode={mode} n={n}")
 
 
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("n,k", [(3000, 700), (1 << 18, 1 << 17), (1 << 21, 4096)])
+def test_scaled_smallest_and_shapes(cuda, mode, n, k):
+    # the device-decided scale flag must reach every path: fused short rows, dense k >= n/2 rows,
+    # the sampled-threshold pipeline; smallest order subtracts the same a_s (scaling.hpp:70-72)
+    import torch
+    rtk = _rtk()
+    x = O.ref_generate(UNIFORM, n, 77 + n, a=128.6, b=128.7)
+    for order in (0, 1):
+        wv, wi, wp, winfo = O.ref_scaled_topk(x, k, order, mode=mode, seed=5 + k, grid=4)
+        info = rtk.ScaleInfo()
+        r = rtk.scaled_topk(torch.from_numpy(x).to(cuda), k, rtk.SelectionOrder(order),
+                            policy=rtk.ScalePolicy(rtk.ScaleMode(mode), 0.5, 5 + k), info=info)
+        assert info.scaled == winfo["scaled"]
+        assert_same((r.values, r.indices, r.pivot), (wv, wi, wp), f"scaled mode={mode} n={n} order={order}")
+
+
 def test_adaptive_benign_does_not_scale(cuda):
     # scaling_test.cpp:173-196
     import torch

@@ -6,11 +6,8 @@ import torch, paper_2501_14336_b200 as rtk
 from paper_2501_14336_b200 import rtk as R
 g = torch.Generator(device="cuda"); g.manual_seed(1)
 xa = (128.6 + 0.1 * torch.rand(1 << 26, device="cuda", generator=g)).float()
-for mode in (0, 1):
-    pol = R.ScalePolicy(mode=R.ScaleMode(mode), trigger_fraction=0.5, seed=31)
-    for i in range(6):
-        torch.cuda.synchronize(); t = time.perf_counter()
-        rtk.scaled_topk(xa, 1 << 16, policy=pol); torch.cuda.synchronize()
-        print("mode", mode, i, "us", round((time.perf_counter() - t) * 1e6), rtk.last_stats(), flush=True)
+pol = R.ScalePolicy(mode=R.ScaleMode(0), trigger_fraction=0.5, seed=31)
+for i in range(3): rtk.scaled_topk(xa, 1 << 16, policy=pol)
+torch.cuda.synchronize()
 PY
-python /tmp/c4.py 2>&1 | tail -14
+RTK_PROFILE=1 python /tmp/c4.py 2>&1 | grep -E "profile|ctl|dbg" | tail -5 | cut -c1-300
