@@ -83,6 +83,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_NO_FUSED")) no_fused_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_NO_DENSE")) no_dense_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_SPARSE_MAX")) sparse_max_ = std::atoi(g);
+    if (const char* g = std::getenv("RTK_ROWS_PF")) rows_pf_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_DENSE_BITS")) dense_bits_ = static_cast<uint32_t>(std::atoi(g));
     const char* cs = std::getenv("RTK_COUNT_STATS");
     count_stats_ = profile_ || (cs && *cs && *cs != '0');
@@ -558,7 +559,8 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
         if (frow[v].empty()) continue;
         RowsFusedArgs fa{at<uint32_t>(D, o_f[v][0]), at<uint64_t>(D, o_f[v][1]), at<uint64_t>(D, o_f[v][2]),
                          at<uint64_t>(D, o_f[v][3]), src, c.d_row_out, d_vals, d_idx, d_pivots,
-                         row_fail_.as<uint32_t>(), ctl_.as<uint32_t>(), nullptr, CallTail{}};
+                         row_fail_.as<uint32_t>(), ctl_.as<uint32_t>(), nullptr, CallTail{},
+                         static_cast<uint32_t>(rows_pf_)};
         if (profile_) {
             dbg_.ensure(4096);
             fa.dbg = dbg_.as<unsigned long long>();

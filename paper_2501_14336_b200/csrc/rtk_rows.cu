@@ -27,8 +27,18 @@ constexpr int kRowKMaxS = 512;
 constexpr int kRowSampleS = 2048;  // sample size of the small variant (64 segments x 32)
 constexpr int kRowSampleL = 4096;  // large variant
 constexpr int kRowChunk = 2048;   // elements per TMA bulk chunk (8 KB)
-constexpr int kRowStages = 4;     // ring depth of the large-k variant (32 KB in flight per CTA)
-constexpr int kRowStagesS = 8;    // small-k variant (64 KB in flight per CTA)
+#ifndef RTK_ROWS_U
+#define RTK_ROWS_U 4
+#endif
+#ifndef RTK_ROWS_SS
+#define RTK_ROWS_SS 2
+#endif
+#ifndef RTK_ROWS_SL
+#define RTK_ROWS_SL 1
+#endif
+constexpr int kRowU = RTK_ROWS_U;    // 2048-element chunks per ring stage (one TMA copy each)
+constexpr int kRowStU = RTK_ROWS_SS; // stages of the small-k variant
+constexpr int kRowStLU = RTK_ROWS_SL;  // stages of the large-k variant
 
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
@@ -177,18 +187,18 @@ __device__ void cta_bitonic_desc(unsigned long long* buf, int n2) {
     }
 }
 
-template <int KM, int CAND, int STAGES, int SAMPLE>
+template <int KM, int CAND, int STAGES, int SAMPLE, int UU>
 __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a);
 
-template <int KM, int CAND, int STAGES, int SAMPLE>
+template <int KM, int CAND, int STAGES, int SAMPLE, int UU>
 __global__ void __launch_bounds__(kRowThreads, 2) k_rows_fused(RowsFusedArgs a) {
     __shared__ uint32_t s_tail;
     resolve_src(a.in);
-    rows_fused_body<KM, CAND, STAGES, SAMPLE>(a);
+    rows_fused_body<KM, CAND, STAGES, SAMPLE, UU>(a);
     call_tail(a.tail, &s_tail);  // only when this is the call's last kernel
 }
 
-template <int KM, int CAND, int STAGES, int SAMPLE>
+template <int KM, int CAND, int STAGES, int SAMPLE, int UU>
 __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     constexpr int kRowCand = CAND;
     constexpr int kRowStages = STAGES;
@@ -199,6 +209,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     __shared__ unsigned long long s_res[3];
     __shared__ uint32_t s_m;
     __shared__ unsigned long long bar[STAGES];
+    __shared__ uint32_t s_empty[STAGES];
     const int j = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned full = 0xffffffffu;
@@ -228,18 +239,30 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     const uintptr_t a0 = reinterpret_cast<uintptr_t>(rowb);
     const uint32_t head = static_cast<uint32_t>(((16 - (a0 & 15)) & 15) / EB);  // to 16-B alignment
     const uint64_t body = n > head ? n - head : 0;
-    const uint64_t nchunks = body / kRowChunk;
+    constexpr int U = UU;
+    constexpr uint32_t kChunk = static_cast<uint32_t>(U) * kRowChunk;  // elements per ring stage
+    const uint64_t nchunks = body / kChunk;
     const char* bsrc = rowb + head * EB;
     char* ring = reinterpret_cast<char*>(cand + kRowCand);
-    constexpr uint32_t kChunkBytes = kRowChunk * EB;
+    constexpr uint32_t kChunkBytes = kChunk * EB;
     if (tid == 0) {
-        for (int st = 0; st < kRowStages; ++st) mbar_init(&bar[st], 1);
+        for (int st = 0; st < kRowStages; ++st) {
+            mbar_init(&bar[st], 1);
+            s_empty[st] = 0;
+        }
         fence_mbar_init();
     }
     __syncthreads();
+    // L2 prefetch `pf` chunks beyond the ring: bytes in flight per SM without shared memory
+    auto prefetch = [&](uint64_t c) {
+        if (c < nchunks)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(bsrc + c * kChunkBytes),
+                         "r"(kChunkBytes) : "memory");
+    };
     if (tid == 0) {
         for (uint64_t c = 0; c < nchunks && c < static_cast<uint64_t>(kRowStages); ++c)
             bulk_g2s(ring + c * kChunkBytes, bsrc + c * kChunkBytes, kChunkBytes, &bar[c]);
+        for (uint32_t p = 0; p < a.pf; ++p) prefetch(kRowStages + p);
     }
 
     // ---- 1. threshold -------------------------------------------------------------------
@@ -265,7 +288,6 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     stamp();
 
     // ---- 2. one streaming read of the row --------------------------------------------------
-    const uint32_t thi = static_cast<uint32_t>(T >> 32), tlo = static_cast<uint32_t>(T);
     auto append = [&](uint32_t mask, const uint32_t* keys, uint32_t (*idx_of)(uint32_t, const void*),
                       const void* ctx) {};
     (void)append;
@@ -294,50 +316,88 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
             }
     };
     auto test4 = [&](uint32_t (&key)[4], uint32_t ibase, uint32_t valid) {
+        // branch-free 64-bit composite compare (K >= T): two predicated compares per element
         uint32_t mask = 0;
+        const uint32_t nb = ~ibase;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             key[i] = key_of<KM>(key[i], a.in);
-            const bool hit = ((valid >> i) & 1u) && (key[i] > thi || (key[i] == thi && ~(ibase + i) >= tlo));
-            mask |= static_cast<uint32_t>(hit) << i;
+            const unsigned long long K = (static_cast<unsigned long long>(key[i]) << 32) | (nb - i);
+            mask |= static_cast<uint32_t>(K >= T) << i;
         }
-        return mask;
+        return mask & valid;
     };
-    // consume the ring in groups of half its depth: one block barrier per group, then the
-    // group's stages are refilled while the other half is being consumed
-    constexpr int G = kRowStages / 2;
-    for (uint64_t c0 = 0; c0 < nchunks; c0 += G) {
+    // consume the ring without block barriers: a warp that has read its slice of stage st
+    // arrives on the stage's empty counter; the LAST warp to arrive refills the stage (TMA)
+    // and re-arms the counter. Warps drift apart by up to the ring depth instead of meeting
+    // at a __syncthreads per group. A stage holds U chunks of 2048 elements: 4*U independent
+    // elements per thread between two waits (latency hiding with only 16 warps per CTA).
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        const int st = static_cast<int>(c % kRowStages);
+        mbar_wait(&bar[st], static_cast<uint32_t>((c / kRowStages) & 1));
+        uint32_t key[4 * U];
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const uint64_t c = c0 + g;
-            if (c >= nchunks) break;
-            const int st = static_cast<int>(c % kRowStages);
-            mbar_wait(&bar[st], static_cast<uint32_t>((c / kRowStages) & 1));
-            uint32_t key[4];
+        for (int u = 0; u < U; ++u) {
             if constexpr (EB == 2) {
-                const uint2 q = reinterpret_cast<const uint2*>(ring + st * kChunkBytes)[tid];
-                key[0] = q.x & 0xFFFFu; key[1] = q.x >> 16; key[2] = q.y & 0xFFFFu; key[3] = q.y >> 16;
+                const uint2 q = reinterpret_cast<const uint2*>(ring + st * kChunkBytes)[u * kRowThreads + tid];
+                key[4 * u] = q.x & 0xFFFFu; key[4 * u + 1] = q.x >> 16;
+                key[4 * u + 2] = q.y & 0xFFFFu; key[4 * u + 3] = q.y >> 16;
             } else {
-                const uint4 q = reinterpret_cast<const uint4*>(ring + st * kChunkBytes)[tid];
-                key[0] = q.x; key[1] = q.y; key[2] = q.z; key[3] = q.w;
+                const uint4 q = reinterpret_cast<const uint4*>(ring + st * kChunkBytes)[u * kRowThreads + tid];
+                key[4 * u] = q.x; key[4 * u + 1] = q.y; key[4 * u + 2] = q.z; key[4 * u + 3] = q.w;
             }
-            const uint32_t ibase = head + static_cast<uint32_t>(c * kRowChunk) + tid * 4;
-            const uint32_t mask = test4(key, ibase, 0xFu);
-            push4(mask, key, ibase);
         }
-        __syncthreads();  // the group's stages are fully consumed
-        if (tid == 0) {
-            for (int g = 0; g < G; ++g) {
-                const uint64_t c = c0 + g;
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(&s_empty[st], 1u) == kRowWarps - 1) {
+                s_empty[st] = 0;
+                __threadfence_block();
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 if (c + kRowStages < nchunks)
-                    bulk_g2s(ring + (c % kRowStages) * kChunkBytes, bsrc + (c + kRowStages) * kChunkBytes,
-                             kChunkBytes, &bar[c % kRowStages]);
+                    bulk_g2s(ring + st * kChunkBytes, bsrc + (c + kRowStages) * kChunkBytes, kChunkBytes, &bar[st]);
+                if (a.pf) prefetch(c + kRowStages + a.pf);
+            }
+        }
+        uint32_t mask = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t nb = ~(head + static_cast<uint32_t>(c * kChunk + u * 2048) + tid * 4);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                key[4 * u + i] = key_of<KM>(key[4 * u + i], a.in);
+                const unsigned long long K = (static_cast<unsigned long long>(key[4 * u + i]) << 32) | (nb - i);
+                mask |= static_cast<uint32_t>(K >= T) << (4 * u + i);
+            }
+        }
+        if (__any_sync(full, mask)) {
+            const uint32_t cnt = __popc(mask);
+            uint32_t inc = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(full, inc, d);
+                if (lane >= d) inc += o;
+            }
+            const uint32_t wtot = __shfl_sync(full, inc, 31);
+            uint32_t wbase = 0;
+            if (lane == 31) wbase = atomicAdd(&s_m, wtot);
+            wbase = __shfl_sync(full, wbase, 31);
+            uint32_t o = wbase + inc - cnt;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t nb = ~(head + static_cast<uint32_t>(c * kChunk + u * 2048) + tid * 4);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if ((mask >> (4 * u + i)) & 1u) {
+                        if (o < kRowCand) cand[o] = (static_cast<unsigned long long>(key[4 * u + i]) << 32) | (nb - i);
+                        ++o;
+                    }
             }
         }
     }
     // head (< 4 elements before 16-byte alignment) and tail (< one chunk) with plain loads
     {
-        const uint64_t t0 = head + nchunks * kRowChunk;
+        const uint64_t t0 = head + nchunks * kChunk;
         const uint64_t rest = n - t0;  // < kRowChunk + ...
         for (uint64_t b0 = 0; b0 < rest + head; b0 += 4 * kRowThreads) {
             uint32_t key[4];
@@ -435,6 +495,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
             if (p == kk - 1 && a.pivots) store_val(a.pivots, a.in.dtype, r, val);
         }
         stamp();
+        if (dbg && blockIdx.x == 0 && threadIdx.x == 0) dbg[31] = ndbg;
         return;
     }
     // ---- 4. LSD radix sort of the k survivors (descending), 8 items per thread -------------
@@ -525,39 +586,39 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     if (dbg && blockIdx.x == 0 && threadIdx.x == 0) dbg[31] = ndbg;
 }
 
-template <int KM, int CAND, int STAGES, int SAMPLE>
+template <int KM, int CAND, int STAGES, int SAMPLE, int UU>
 static void rows_km(int R, const RowsFusedArgs& a, cudaStream_t s) {
-    constexpr size_t smem = CAND * sizeof(unsigned long long) + STAGES * kRowChunk * sizeof(uint32_t);
+    constexpr size_t smem = CAND * sizeof(unsigned long long) + STAGES * UU * kRowChunk * sizeof(uint32_t);
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_rows_fused<KM, CAND, STAGES, SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_rows_fused<KM, CAND, STAGES, SAMPLE, UU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         configured = true;
     }
-    k_rows_fused<KM, CAND, STAGES, SAMPLE><<<R, kRowThreads, smem, s>>>(a);
+    k_rows_fused<KM, CAND, STAGES, SAMPLE, UU><<<R, kRowThreads, smem, s>>>(a);
 }
 
-template <int CAND, int STAGES, int SAMPLE>
+template <int CAND, int STAGES, int SAMPLE, int UU>
 static void rows_variant(int R, const RowsFusedArgs& a, cudaStream_t s) {
     switch (key_mode(a.in.dtype, a.in.smallest, a.in.scaled, a.in.adapt)) {
-        case kKmF32L: rows_km<kKmF32L, CAND, STAGES, SAMPLE>(R, a, s); break;
-        case kKmF32S: rows_km<kKmF32S, CAND, STAGES, SAMPLE>(R, a, s); break;
-        case kKmF32LScaled: rows_km<kKmF32LScaled, CAND, STAGES, SAMPLE>(R, a, s); break;
-        case kKmF32SScaled: rows_km<kKmF32SScaled, CAND, STAGES, SAMPLE>(R, a, s); break;
-        case kKmU32L: rows_km<kKmU32L, CAND, STAGES, SAMPLE>(R, a, s); break;
-        case kKmF16L: rows_km<kKmF16L, CAND, STAGES, SAMPLE>(R, a, s); break;
-        case kKmF32LAdapt: rows_km<kKmF32LAdapt, CAND, STAGES, SAMPLE>(R, a, s); break;
-        case kKmF32SAdapt: rows_km<kKmF32SAdapt, CAND, STAGES, SAMPLE>(R, a, s); break;
-        case kKmF16S: rows_km<kKmF16S, CAND, STAGES, SAMPLE>(R, a, s); break;
-        default: rows_km<kKmU32S, CAND, STAGES, SAMPLE>(R, a, s); break;
+        case kKmF32L: rows_km<kKmF32L, CAND, STAGES, SAMPLE, UU>(R, a, s); break;
+        case kKmF32S: rows_km<kKmF32S, CAND, STAGES, SAMPLE, UU>(R, a, s); break;
+        case kKmF32LScaled: rows_km<kKmF32LScaled, CAND, STAGES, SAMPLE, UU>(R, a, s); break;
+        case kKmF32SScaled: rows_km<kKmF32SScaled, CAND, STAGES, SAMPLE, UU>(R, a, s); break;
+        case kKmU32L: rows_km<kKmU32L, CAND, STAGES, SAMPLE, UU>(R, a, s); break;
+        case kKmF16L: rows_km<kKmF16L, CAND, STAGES, SAMPLE, UU>(R, a, s); break;
+        case kKmF32LAdapt: rows_km<kKmF32LAdapt, CAND, STAGES, SAMPLE, UU>(R, a, s); break;
+        case kKmF32SAdapt: rows_km<kKmF32SAdapt, CAND, STAGES, SAMPLE, UU>(R, a, s); break;
+        case kKmF16S: rows_km<kKmF16S, CAND, STAGES, SAMPLE, UU>(R, a, s); break;
+        default: rows_km<kKmU32S, CAND, STAGES, SAMPLE, UU>(R, a, s); break;
     }
 }
 
 // small = rows whose k and expected candidate count fit the small-buffer variant
 void launch_rows_fused(int R, const RowsFusedArgs& a, bool small, cudaStream_t s) {
     if (R <= 0) return;
-    if (small) rows_variant<kRowCandS, kRowStagesS, kRowSampleS>(R, a, s);
-    else rows_variant<kRowCand, kRowStages, kRowSampleL>(R, a, s);
+    if (small) rows_variant<kRowCandS, kRowStU, kRowSampleS, kRowU>(R, a, s);
+    else rows_variant<kRowCand, kRowStLU, kRowSampleL, kRowU>(R, a, s);
 }
 
 uint32_t rows_fused_kmax(bool small) { return small ? kRowKMaxS : kRowKMax; }
