@@ -523,7 +523,8 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     // per-warp digit counters live in the (now idle) streaming ring
     uint32_t (*cnt)[256] = reinterpret_cast<uint32_t (*)[256]>(cand + kRowCand);
     const unsigned lt = (1u << lane) - 1u;
-    for (int lo = 0; lo < nbits; lo += 8) {
+    auto lsd = [&](int lo0) {
+    for (int lo = lo0; lo < nbits; lo += 8) {
         if (((orv >> lo) & 0xFFull) == 0) continue;  // digit constant across the group: no-op pass
         for (int i = tid; i < kRowWarps * 256; i += kRowThreads) (&cnt[0][0])[i] = 0;
         __syncthreads();
@@ -561,6 +562,36 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
 #pragma unroll
         for (int q = 0; q < IT; ++q) key[q] = tmp[warp * 256 + q * 32 + lane];
         __syncthreads();
+    }
+
+    };
+    // Real keys rarely tie: rank by the KEY bits only, then restore index order inside runs of
+    // equal keys with an odd-even transposition (a run of length L settles in <= L rounds);
+    // tie-heavy rows fall back to the full composite passes (as cta_sort_group, rtk_sort.cu).
+    const bool key_only = (orv >> 32) != 0 && (orv & 0xffffffffull) != 0;
+    lsd(key_only ? 32 : 0);
+    if (key_only) {
+#pragma unroll
+        for (int q = 0; q < IT; ++q) cand[warp * 256 + q * 32 + lane] = key[q];
+        __syncthreads();
+        bool prev_sw = true, settled = false;
+        for (int it = 0; it < 64; ++it) {
+            bool sw = false;
+            for (uint32_t q = tid; 2 * q + 1 < kk; q += kRowThreads) {
+                const uint32_t p = 2 * q + (it & 1);
+                if (p + 1 < kk) {
+                    const unsigned long long x = cand[p], y = cand[p + 1];
+                    if ((x >> 32) == (y >> 32) && x < y) { cand[p] = y; cand[p + 1] = x; sw = true; }
+                }
+            }
+            const bool any = __syncthreads_or(sw);
+            if (!any && !prev_sw) { settled = true; break; }
+            prev_sw = any;
+        }
+#pragma unroll
+        for (int q = 0; q < IT; ++q) key[q] = cand[warp * 256 + q * 32 + lane];
+        __syncthreads();
+        if (!settled) lsd(0);  // tie-heavy row: full composite order
     }
 
     stamp();
