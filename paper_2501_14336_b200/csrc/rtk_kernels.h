@@ -108,10 +108,13 @@ struct SegSlot {        // one MSD segment; len == 0 means inactive
     uint64_t len;
     uint64_t rank_base;
     uint32_t rid;
-    uint32_t pos;        // digit = (K >> pos) & (2^bits - 1)
+    uint32_t pos;        // digit = ((K - base) >> pos) & (2^bits - 1)
     uint32_t bits;       // level 0: 11..14; deeper levels: kDigit
     uint32_t src;        // level 0: 1 = read the INPUT row at in_off (dense row, no compaction)
     uint64_t in_off;     // input element offset of the row (src == 1)
+    uint64_t base;       // digit = ((K - base) >> pos) & mask: level 0 subtracts the row's kmin so
+                         // the digit spans the candidates' RANGE, not their XOR (tie-heavy rows
+                         // such as C4 split by index bits at level 0); children inherit it
 };
 
 struct GroupList {

@@ -6,8 +6,8 @@
 namespace rtk_b200 {
 
 // m = #{K >= T}: m < k or overflow -> exact path; m <= kSortCap -> one sort group;
-// larger -> an MSD slot whose first (fine, 11..16-bit) digit sits just below the common prefix
-// of kmin..kmax.
+// larger -> an MSD slot whose first (fine, 11..14-bit) digit is the top of K - kmin over the
+// range kmax - kmin.
 __device__ __forceinline__ void plan_row(int j, uint32_t r, const PlanArgs& pa) {
     const uint64_t m = __ldcg(pa.count + r);
     SegSlot sl{pa.cand_off[r], 0, 0, r, 0, 0, 0};
@@ -18,7 +18,9 @@ __device__ __forceinline__ void plan_row(int j, uint32_t r, const PlanArgs& pa) 
         const uint32_t g = atomicAdd(pa.groups.count, 1u);
         pa.groups.groups[g] = SortGroup{pa.cand_off[r], static_cast<uint32_t>(m), r, 0, 0, 0};
     } else {
-        const unsigned long long x = __ldcg(pa.kmin + r) ^ __ldcg(pa.kmax + r);
+        const unsigned long long kmin = __ldcg(pa.kmin + r);
+        const unsigned long long x = __ldcg(pa.kmax + r) - kmin;  // range, not XOR (see SegSlot::base)
+        sl.base = kmin;
         const int hb = 63 - __clzll(x ? x : 1ull);
         const int bits = static_cast<int>(min(fine_bits(m), pa.max_bits));  // level 0: fine MSD digit
         sl.len = m;

@@ -10,4 +10,4 @@ pol = R.ScalePolicy(mode=R.ScaleMode(0), trigger_fraction=0.5, seed=31)
 for i in range(3): rtk.scaled_topk(xa, 1 << 16, policy=pol)
 torch.cuda.synchronize()
 PY
-RTK_PROFILE=1 python /tmp/c4.py 2>&1 | grep -E "profile|ctl|dbg" | tail -5 | cut -c1-300
+RTK_PROFILE=1 python /tmp/c4.py 2>&1 | tee gpurun_out/c4.log | grep -E "profile|ctl|dbg" | tail -8 | cut -c1-300
