@@ -99,7 +99,7 @@ Engine::~Engine() {
     if (hcount_) cudaFreeHost(hcount_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
-    for (DevBuf* b : {&arena_, &sel_, &T_, &count_, &kmin_, &kmax_, &ghist_, &samples_, &cand_a_,
+    for (DevBuf* b : {&arena_, &sel_, &T_, &count_, &kmin_, &kmax_, &kor_, &ghist_, &samples_, &cand_a_,
                       &cand_b_, &seg_hist_, &gcursor_, &bstart_, &dcap_, &dcoff_, &ctl_, &row_fail_, &groups_, &slots0_, &slotsA_, &slotsB_, &done_, &seg_ticket_, &wgroups_, &ctot_, &sig_, &io_in, &io_vals, &io_idx,
                       &io_piv, &io_aux, &adapt_buf_, &scale_hist_, &scale_plan_})
         b->release();
@@ -269,7 +269,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         const int R = static_cast<int>(rows.size());
         if (!graph_.has_init && (needs_init_ || R > clean_upto_)) {
             launch_init_call(R, count_.as<unsigned long long>(), kmin_.as<unsigned long long>(),
-                             kmax_.as<unsigned long long>(), T_.as<uint64_t>(), row_fail_.as<uint32_t>(),
+                             kmax_.as<unsigned long long>(), kor_.as<uint32_t>(), T_.as<uint64_t>(), row_fail_.as<uint32_t>(),
                              ctl_.as<uint32_t>(), seg_hist_.as<uint32_t>(), done_.as<uint32_t>(),
                              seg_ticket_.as<uint32_t>(), s);
         }
@@ -478,6 +478,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     count_.ensure(8 * R);
     kmin_.ensure(8 * R);
     kmax_.ensure(8 * R);
+    kor_.ensure(4 * R);
     ghist_.ensure(8ull * kBins * R);
     cand_a_.ensure(8 * std::max<uint64_t>(cand_total, 1));
 
@@ -531,7 +532,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     needs_init_ = false;
     did_init_ = true;
     launch_init_call(R, count_.as<unsigned long long>(), kmin_.as<unsigned long long>(),
-                     kmax_.as<unsigned long long>(), T_.as<uint64_t>(), row_fail_.as<uint32_t>(),
+                     kmax_.as<unsigned long long>(), kor_.as<uint32_t>(), T_.as<uint64_t>(), row_fail_.as<uint32_t>(),
                      ctl_.as<uint32_t>(), seg_hist_.as<uint32_t>(), done_.as<uint32_t>(),
                      seg_ticket_.as<uint32_t>(), s);
     ++stats.kernel_launches;
@@ -702,6 +703,7 @@ PlanArgs Engine::plan_args(const Call& c, const FinishPrep& f) {
     pa.count = count_.as<unsigned long long>();
     pa.kmin = kmin_.as<unsigned long long>();
     pa.kmax = kmax_.as<unsigned long long>();
+    pa.kor = kor_.as<uint32_t>();
     pa.slots = slots0_.as<SegSlot>();
     pa.groups = f.gl;
     pa.flags = ctl_.as<uint32_t>();
@@ -802,6 +804,7 @@ void Engine::set_clean(CallTail& t, int R) {
     t.c_count = count_.as<unsigned long long>();
     t.c_kmin = kmin_.as<unsigned long long>();
     t.c_kmax = kmax_.as<unsigned long long>();
+    t.c_kor = kor_.as<uint32_t>();
     t.c_T = T_.as<uint64_t>();
     t.c_done = done_.as<uint32_t>();
     t.c_ticket = seg_ticket_.as<uint32_t>();
@@ -996,6 +999,7 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
         check(cudaMemsetAsync(count_.as<uint64_t>() + r, 0, 8, s), "memset");
         check(cudaMemsetAsync(kmin_.as<uint64_t>() + r, 0xFF, 8, s), "memset");
         check(cudaMemsetAsync(kmax_.as<uint64_t>() + r, 0, 8, s), "memset");
+        check(cudaMemsetAsync(kor_.as<uint32_t>() + r, 0, 4, s), "memset");
         check(cudaMemsetAsync(row_fail_.as<uint32_t>() + r, 0, 4, s), "memset");
         check(cudaMemsetAsync(done_.as<uint32_t>() + r, 0, 4, s), "memset");
     }

@@ -230,7 +230,7 @@ private:
     uint64_t* hcount_ = nullptr;   // pinned readback of candidate counts
     size_t hcount_cap_ = 0;
     cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
-    DevBuf sel_, T_, count_, kmin_, kmax_, ghist_, samples_, cand_a_, cand_b_, seg_hist_,
+    DevBuf sel_, T_, count_, kmin_, kmax_, kor_, ghist_, samples_, cand_a_, cand_b_, seg_hist_,
         gcursor_, bstart_, dcap_, dcoff_, ctl_, row_fail_, groups_, slots0_, slotsA_, slotsB_, done_,
         seg_ticket_, dbg_, wgroups_, ctot_, sig_;
     uint64_t group_base_ = 0, wgroup_base_ = 0;

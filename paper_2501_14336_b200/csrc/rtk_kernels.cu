@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kThreads) k_radix_pass(Rows rows, InputSrc in,
 
 // k_init_call: reset every per-call counter in one launch.
 __global__ void k_init_call(int R, unsigned long long* count, unsigned long long* kmin,
-                            unsigned long long* kmax, uint64_t* T, uint32_t* row_fail, uint32_t* ctl,
+                            unsigned long long* kmax, uint32_t* kor, uint64_t* T, uint32_t* row_fail, uint32_t* ctl,
                             uint32_t* seg_hist, uint32_t* done, uint32_t* seg_ticket) {
     const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -232,6 +232,7 @@ __global__ void k_init_call(int R, unsigned long long* count, unsigned long long
         count[i] = 0;
         kmin[i] = ~0ull;
         kmax[i] = 0;
+        kor[i] = 0;
         T[i] = 0;
         row_fail[i] = 0;
         done[i] = 0;
@@ -446,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
 
     int cur = -1;
     unsigned long long thr = 0, mn = ~0ull, mx = 0;
+    uint32_t ko = 0;  // OR of (key ^ T.hi) over this thread's hits of the current row
     uint32_t thi = 0, tlo = 0, wcur = 0;
     uint64_t off = 0, len = 0, coff = 0, ccap = 0, tile0 = 0, tile1 = 0;
     uint32_t lead = 0, r = 0, mine_tiles = 0;
@@ -481,6 +483,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
             const unsigned long long K = stage[i];
             mn = min(mn, K);
             mx = max(mx, K);
+            ko |= static_cast<uint32_t>(K >> 32) ^ thi;
             if (base + i < ccap) cand[coff + base + i] = K;
         }
         __syncwarp();
@@ -489,14 +492,21 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
     auto finish_row = [&]() {
         warp_flush();
         unsigned long long a = mn, b = mx;
+        uint32_t o = ko;
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
             a = min(a, __shfl_xor_sync(full, a, d));
             b = max(b, __shfl_xor_sync(full, b, d));
+            o |= __shfl_xor_sync(full, o, d);
         }
-        if (lane == 0 && a <= b) { atomicMin(kmin + r, a); atomicMax(kmax + r, b); }
+        if (lane == 0 && a <= b) {
+            atomicMin(kmin + r, a);
+            atomicMax(kmax + r, b);
+            if (pa.kor && o) atomicOr(pa.kor + r, o);
+        }
         mn = ~0ull;
         mx = 0;
+        ko = 0;
         // the CTA that finishes the row's last tile plans its ordering (k_plan_rows fused)
         if (pa.done) {
             __threadfence();
@@ -784,11 +794,11 @@ void launch_radix_pass(int src, uint64_t tiles, const Rows& rows, const InputSrc
 }
 
 void launch_init_call(int R, unsigned long long* count, unsigned long long* kmin, unsigned long long* kmax,
-                      uint64_t* T, uint32_t* row_fail, uint32_t* ctl, uint32_t* seg_hist, uint32_t* done,
+                      uint32_t* kor, uint64_t* T, uint32_t* row_fail, uint32_t* ctl, uint32_t* seg_hist, uint32_t* done,
                       uint32_t* seg_ticket, cudaStream_t s) {
     const uint64_t work = static_cast<uint64_t>(R) * kBins;
     const int grid = static_cast<int>(std::min<uint64_t>((work + 255) / 256, 1024));
-    k_init_call<<<grid, 256, 0, s>>>(R, count, kmin, kmax, T, row_fail, ctl, seg_hist, done, seg_ticket);
+    k_init_call<<<grid, 256, 0, s>>>(R, count, kmin, kmax, kor, T, row_fail, ctl, seg_hist, done, seg_ticket);
 }
 
 void launch_sample_select(int rows, int cs, uint32_t per_cta, const SampleRows& sr, const InputSrc& in,

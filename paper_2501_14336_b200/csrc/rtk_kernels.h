@@ -38,6 +38,7 @@ struct CallTail {
     unsigned long long* c_count;
     unsigned long long* c_kmin;
     unsigned long long* c_kmax;
+    uint32_t* c_kor;
     uint64_t* c_T;
     uint32_t* c_done;
     uint32_t* c_ticket;
@@ -68,6 +69,7 @@ __device__ __forceinline__ void call_tail(const CallTail& t, uint32_t* s_flag) {
             t.c_count[r] = 0;
             t.c_kmin[r] = ~0ull;
             t.c_kmax[r] = 0;
+            t.c_kor[r] = 0;
             t.c_T[r] = 0;
             t.c_done[r] = 0;
             t.c_ticket[r] = 0;
@@ -112,10 +114,18 @@ struct SegSlot {        // one MSD segment; len == 0 means inactive
     uint32_t bits;       // level 0: 11..14; deeper levels: kDigit
     uint32_t src;        // level 0: 1 = read the INPUT row at in_off (dense row, no compaction)
     uint64_t in_off;     // input element offset of the row (src == 1)
-    uint64_t base;       // digit = ((K - base) >> pos) & mask: level 0 subtracts the row's kmin so
-                         // the digit spans the candidates' RANGE, not their XOR (tie-heavy rows
-                         // such as C4 split by index bits at level 0); children inherit it
+    uint64_t base;       // digit = (rel(K) >> pos) & mask with rel(K) = ((key - key(base)) >> tz) << 32
+    uint32_t tz;         //   + (lo(K) - lo(base)): the candidates' RANGE, not their XOR, with the
+                         //   key's common trailing zeros squeezed out (order-preserving); tie-heavy
+                         //   rows such as C4 split by index bits at level 0. Children inherit both.
 };
+
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long slot_rel(const SegSlot& sl, unsigned long long K) {
+    const uint32_t kd = (static_cast<uint32_t>(K >> 32) - static_cast<uint32_t>(sl.base >> 32)) >> sl.tz;
+    return (static_cast<unsigned long long>(kd) << 32) + (K & 0xffffffffull) - (sl.base & 0xffffffffull);
+}
+#endif
 
 struct GroupList {
     SortGroup* groups;
@@ -185,6 +195,7 @@ struct PlanArgs {         // per-row plan after the compaction (fused into k_com
     const unsigned long long* count;
     const unsigned long long* kmin;
     const unsigned long long* kmax;
+    uint32_t* kor;           // per state row: OR of (key ^ T.hi) over the candidates (digit stride)
     SegSlot* slots;          // indexed by launch row
     GroupList groups;
     uint32_t* flags;
@@ -240,7 +251,7 @@ void launch_init_sel(int R, const uint32_t* rid, const uint64_t* k, const uint64
 void launch_radix_pass(int src, uint64_t tiles, const Rows& rows, const InputSrc& in,
                        const uint64_t* buf, RowSel* sel, unsigned long long* ghist, cudaStream_t s);
 void launch_init_call(int R, unsigned long long* count, unsigned long long* kmin, unsigned long long* kmax,
-                      uint64_t* T, uint32_t* row_fail, uint32_t* ctl, uint32_t* seg_hist, uint32_t* done,
+                      uint32_t* kor, uint64_t* T, uint32_t* row_fail, uint32_t* ctl, uint32_t* seg_hist, uint32_t* done,
                       uint32_t* seg_ticket, cudaStream_t s);
 void launch_sample_select(int rows, int cs, uint32_t per_cta, const SampleRows& sr, const InputSrc& in,
                           uint64_t* T, cudaStream_t s);

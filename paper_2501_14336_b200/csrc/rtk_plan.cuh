@@ -19,8 +19,11 @@ __device__ __forceinline__ void plan_row(int j, uint32_t r, const PlanArgs& pa) 
         pa.groups.groups[g] = SortGroup{pa.cand_off[r], static_cast<uint32_t>(m), r, 0, 0, 0};
     } else {
         const unsigned long long kmin = __ldcg(pa.kmin + r);
-        const unsigned long long x = __ldcg(pa.kmax + r) - kmin;  // range, not XOR (see SegSlot::base)
         sl.base = kmin;
+        // every candidate key is congruent to T.hi modulo 2^tz: squeeze those zeros out
+        const uint32_t ko = pa.kor ? __ldcg(pa.kor + r) : 0u;
+        sl.tz = ko ? static_cast<uint32_t>(__ffs(ko) - 1) : 0u;
+        const unsigned long long x = slot_rel(sl, __ldcg(pa.kmax + r));  // range, not XOR
         const int hb = 63 - __clzll(x ? x : 1ull);
         const int bits = static_cast<int>(min(fine_bits(m), pa.max_bits));  // level 0: fine MSD digit
         sl.len = m;

@@ -162,7 +162,7 @@ __device__ void seg_plan_block(int j, const SegSlot& sl, const SegPlanArgs& a) {
             const uint32_t q = atomicAdd(next.count, 1u);
             if (q < next.cap)
                 next.slots[q] = SegSlot{sl.off + start[i], c[i], sl.rank_base + start[i], sl.rid,
-                                        sl.pos >= kDigit ? sl.pos - kDigit : 0u, kDigit, 0, 0, sl.base};
+                                        sl.pos >= kDigit ? sl.pos - kDigit : 0u, kDigit, 0, 0, sl.base, sl.tz};
             atomicOr(flags, kFlagMore);
         } else if (gst[i]) {
             uint32_t end = INF;
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kThreads) k_seg_hist(const SegSlot* slots, int
 #pragma unroll
             for (int i = 0; i < kVec64; ++i) {
                 const uint64_t q = e0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec64 + i;
-                hist_add_spread(h, static_cast<uint32_t>((v[u][i] - sl.base) >> sl.pos) & (kBins - 1), q >= lead && q < span_len);
+                hist_add_spread(h, static_cast<uint32_t>(slot_rel(sl, v[u][i]) >> sl.pos) & (kBins - 1), q >= lead && q < span_len);
             }
     }
     if (cur >= 0) finish_slot(cur);
@@ -394,7 +394,7 @@ __device__ void msd_plan_slice(const SegSlot& sl, uint32_t* tot, uint32_t slice,
                 } else {
                     if (ib < a.next.cap)
                         a.next.slots[ib] = SegSlot{sl.off + st, c, sl.rank_base + st, sl.rid,
-                                                   sl.pos >= kDigit ? sl.pos - kDigit : 0u, kDigit, 0, 0, sl.base};
+                                                   sl.pos >= kDigit ? sl.pos - kDigit : 0u, kDigit, 0, 0, sl.base, sl.tz};
                     else
                         overflow = true;
                     ++ib;
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* s
     msd_chunk(sl.len, Q * CS, q * CS + r, e0, e1);
     const uint64_t* p = src + sl.off;
     auto hist_one = [&](unsigned long long K, bool valid) {
-        const uint32_t d = static_cast<uint32_t>((K - sl.base) >> sl.pos) & dmask;
+        const uint32_t d = static_cast<uint32_t>(slot_rel(sl, K) >> sl.pos) & dmask;
         const uint32_t d0 = __shfl_sync(full, d, 0);
         if (__all_sync(full, valid && d == d0)) {
             if (lane == 0) atomicAdd(h + d0, 32u);  // tie-heavy rows: one atomic per warp
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(kMsdThreads, 1) k_msd_cluster(const SegSlot* s
     if (dbg) fa.dbg[5] = msd_timer();
     uint64_t* qd = dst + sl.off;
     auto scatter_one = [&](unsigned long long K, bool valid) {
-        const uint32_t d = static_cast<uint32_t>((K - sl.base) >> sl.pos) & dmask;
+        const uint32_t d = static_cast<uint32_t>(slot_rel(sl, K) >> sl.pos) & dmask;
         const uint32_t d0 = __shfl_sync(full, d, 0);
         if (__all_sync(full, valid && d == d0)) {  // tie-heavy: one shared atomic per warp
             if (h[d0] != ~0u) {                     // warp-uniform (dropped buckets stay ~0)
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(kThreads) k_seg_scatter(const SegSlot* slots, 
 #pragma unroll
             for (int i = 0; i < kVec64; ++i) {
                 const uint64_t q = e0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec64 + i;
-                const uint32_t d = static_cast<uint32_t>((v[u][i] - sl.base) >> sl.pos) & (kBins - 1);
+                const uint32_t d = static_cast<uint32_t>(slot_rel(sl, v[u][i]) >> sl.pos) & (kBins - 1);
                 slot[u][i] = (q >= lead && q < span_len && bs[d] != ~0u) ? atomicAdd(&h[d], 1u) : ~0u;
             }
         __syncthreads();
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(kThreads) k_seg_scatter(const SegSlot* slots, 
 #pragma unroll
             for (int i = 0; i < kVec64; ++i) {
                 if (slot[u][i] != ~0u) {
-                    const uint32_t d = static_cast<uint32_t>((v[u][i] - sl.base) >> sl.pos) & (kBins - 1);
+                    const uint32_t d = static_cast<uint32_t>(slot_rel(sl, v[u][i]) >> sl.pos) & (kBins - 1);
                     dst[sl.off + base[d] + slot[u][i]] = v[u][i];
                 }
             }

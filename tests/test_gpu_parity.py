@@ -104,6 +104,35 @@ def test_adversarial_narrow_band(cuda):
         assert_same(gpu_topk(x, k, 0, cuda), O.ref_topk(x, k, 0, grid=8), f"narrow k={k}")
 
 
+@pytest.mark.parametrize("shift", [0, 7, 12, 20])
+def test_strided_tie_heavy_keys(cuda, shift):
+    # keys that are all congruent modulo 2^shift and heavily tied (the scaled C4 shape: x - a_s
+    # keeps the 2^-16 spacing of x inside much finer floats): the level-0 MSD digit squeezes the
+    # common trailing zeros out of the key range (SegSlot::tz) and must keep the exact order
+    rng = np.random.default_rng(shift)
+    n = 1 << 22
+    x = ((rng.integers(0, 4096, n, dtype=np.uint64) << np.uint64(shift)) + np.uint64(12345)).astype(np.uint32)
+    for order in (0, 1):
+        for k in (700, 1 << 15):
+            assert_same(gpu_topk(x, k, order, cuda), O.ref_topk(x, k, order, grid=8), f"stride {shift} k={k}")
+
+
+def test_scaled_c4_shape(cuda):
+    # C4 at 1/16 size through scaled_topk Always: candidates are 9-ish distinct scaled keys 2^12
+    # float-ulps apart with ~10K copies each
+    import torch
+    rtk = _rtk()
+    n = 1 << 22
+    x = O.ref_generate(UNIFORM, n, 31, a=128.6, b=128.7)
+    for mode in (1, 2):
+        wv, wi, wp, winfo = O.ref_scaled_topk(x, 1 << 12, 0, mode=mode, seed=31, grid=8)
+        info = rtk.ScaleInfo()
+        r = rtk.scaled_topk(torch.from_numpy(x).to(cuda), 1 << 12, policy=rtk.ScalePolicy(rtk.ScaleMode(mode), 0.5, 31),
+                            info=info)
+        assert info.scaled == winfo["scaled"]
+        assert_same((r.values, r.indices, r.pivot), (wv, wi, wp), f"scaled C4 shape mode={mode}")
+
+
 def test_integer_ramp(cuda):
     # engine_test.cpp:292-303
     x = np.arange(1 << 20, dtype=np.uint32)
