@@ -84,6 +84,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_NO_DENSE")) no_dense_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_SPARSE_MAX")) sparse_max_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_ROWS_PF")) rows_pf_ = std::atoi(g);
+    if (const char* g = std::getenv("RTK_MSD_CS")) msd_cs_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_DENSE_BITS")) dense_bits_ = static_cast<uint32_t>(std::atoi(g));
     const char* cs = std::getenv("RTK_COUNT_STATS");
     count_stats_ = profile_ || (cs && *cs && *cs != '0');
@@ -671,6 +672,11 @@ Engine::FinishPrep Engine::prepare_finish(Call& c, const std::vector<uint32_t>& 
         warp_groups += std::min<uint64_t>(bins, cp);
     }
     f.cs = msd_cluster_size(max_cap);
+    // many big rows (batched dense rows, k = vocab): smaller clusters run more rows at once; the
+    // MSD of one slot is latency-bound (cluster barriers), not bandwidth-bound
+    if (msd_cs_) f.cs = msd_cs_;
+    else
+        while (f.cs > 2 && f.big_rows * static_cast<uint64_t>(f.cs) > 2ull * num_sms()) f.cs >>= 1;
     f.max_cap = max_cap;
     f.max_groups = cta_groups;
     f.max_wgroups = warp_groups;
