@@ -684,8 +684,8 @@ __global__ void k_remap_idx(uint64_t n, const uint64_t* cand_idx, uint32_t nbloc
 // (scaled_topk's adaptive trigger, scaling.hpp:50-58). d <= 13 uses smem; wider digits go
 // straight to global u64 atomics.
 // ----------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_first_digit_hist(Rows rows, InputSrc in,
-                                                               unsigned int d,
+template <int KM>
+__global__ void __launch_bounds__(kThreads) k_first_digit_hist(Rows rows, InputSrc in, unsigned int d,
                                                                unsigned long long* ghist) {
     extern __shared__ uint32_t hs[];
     const uint32_t nb = 1u << d;
@@ -697,22 +697,50 @@ __global__ void __launch_bounds__(kThreads) k_first_digit_hist(Rows rows, InputS
     const uint64_t ntiles = rows.tile_start[rows.R];
     const uint64_t off = rows.off[0], len = rows.len[0];
     const uint32_t lead = rows.lead[0];
+    const uint64_t span_len = len + lead;
+    const unsigned full = 0xffffffffu;
+    // warp-uniform tiles (the adversarial inputs this trigger exists for put every key in ONE
+    // bin) accumulate in a register: one shared atomic per run, not one per warp and element
+    uint32_t run_d = 0, run_c = 0;
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t span0 = t * kTile;
+        const uint32_t vlo = span0 >= lead ? 0u : static_cast<uint32_t>(lead - span0);
+        const uint32_t vhi = static_cast<uint32_t>(span_len - span0 < kTile ? span_len - span0 : kTile);
         uint32_t v[kUnroll][kVec];
-        const uint64_t span0 = t * kTile, span_len = len + lead;
-        load_input_tile_any(in, off, span_len, lead, span0, v);
+        load_tile_local(in.base + off - lead + span0, vlo, vhi, v);
+        const bool whole = vlo == 0 && vhi == kTile;
+        uint32_t d0 = 0;
+        bool same = whole;
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
             for (int i = 0; i < kVec; ++i) {
-                const uint64_t q = span0 + static_cast<uint64_t>(u * kThreads + threadIdx.x) * kVec + i;
-                const bool valid = q >= lead && q < span_len;
-                const uint32_t dig = make_key(in, v[u][i]) >> (32 - d);
-                if (use_smem) hist_add(hs, dig, valid);
-                else if (valid) atomicAdd(ghist + dig, 1ull);
+                v[u][i] = key_of<KM>(v[u][i], in) >> (32 - d);
+                if (u == 0 && i == 0) d0 = v[0][0];
+                same &= v[u][i] == d0;
+            }
+        const uint32_t w0 = __shfl_sync(full, d0, 0);
+        if (use_smem && __all_sync(full, same && d0 == w0)) {
+            if (w0 != run_d) {
+                if (run_c && (threadIdx.x & 31) == 0) atomicAdd(&hs[run_d], run_c);
+                run_d = w0;
+                run_c = 0;
+            }
+            run_c += 32 * kUnroll * kVec;
+            continue;
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+            for (int i = 0; i < kVec; ++i) {
+                const uint32_t l = (u * kThreads + threadIdx.x) * kVec + i;
+                const bool valid = l >= vlo && l < vhi;
+                if (use_smem) hist_add(hs, v[u][i], valid);
+                else if (valid) atomicAdd(ghist + v[u][i], 1ull);
             }
     }
     if (use_smem) {
+        if (run_c && (threadIdx.x & 31) == 0) atomicAdd(&hs[run_d], run_c);
         __syncthreads();
         for (uint32_t b = threadIdx.x; b < nb; b += kThreads)
             if (hs[b]) atomicAdd(ghist + b, static_cast<unsigned long long>(hs[b]));
@@ -872,8 +900,14 @@ void launch_pivots(int R, const uint64_t* row_out_off, const uint64_t* row_k, co
 void launch_first_digit_hist(uint64_t tiles, const Rows& rows, const InputSrc& in, unsigned int d,
                              unsigned long long* ghist, cudaStream_t s) {
     const size_t smem = d <= 13 ? (static_cast<size_t>(1) << d) * sizeof(uint32_t) : 0;
-    const int grid = persistent_grid(k_first_digit_hist, kThreads, smem, tiles);
-    k_first_digit_hist<<<grid, kThreads, smem, s>>>(rows, in, d, ghist);
+    // the trigger always histograms the UNSCALED f32 keys (scaling.hpp:50-58)
+    if (in.smallest) {
+        const int grid = persistent_grid(k_first_digit_hist<kKmF32S>, kThreads, smem, tiles);
+        k_first_digit_hist<kKmF32S><<<grid, kThreads, smem, s>>>(rows, in, d, ghist);
+    } else {
+        const int grid = persistent_grid(k_first_digit_hist<kKmF32L>, kThreads, smem, tiles);
+        k_first_digit_hist<kKmF32L><<<grid, kThreads, smem, s>>>(rows, in, d, ghist);
+    }
 }
 
 void launch_scale_decide(int mode, const unsigned long long* hist, uint32_t nbins, uint64_t n, uint64_t k,
