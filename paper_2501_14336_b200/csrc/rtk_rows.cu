@@ -239,7 +239,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     const uintptr_t a0 = reinterpret_cast<uintptr_t>(rowb);
     const uint32_t head = static_cast<uint32_t>(((16 - (a0 & 15)) & 15) / EB);  // to 16-B alignment
     const uint64_t body = n > head ? n - head : 0;
-    constexpr int U = UU;
+    constexpr int U = km_is16<KM>() ? 2 * UU : UU;  // same stage BYTES for 16-bit rows
     constexpr uint32_t kChunk = static_cast<uint32_t>(U) * kRowChunk;  // elements per ring stage
     const uint64_t nchunks = body / kChunk;
     const char* bsrc = rowb + head * EB;
@@ -332,66 +332,74 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     // and re-arms the counter. Warps drift apart by up to the ring depth instead of meeting
     // at a __syncthreads per group. A stage holds U chunks of 2048 elements: 4*U independent
     // elements per thread between two waits (latency hiding with only 16 warps per CTA).
+    constexpr int G = U / UU;  // 16-bit rows: the stage is consumed in G groups of UU sub-chunks
     for (uint64_t c = 0; c < nchunks; ++c) {
         const int st = static_cast<int>(c % kRowStages);
         mbar_wait(&bar[st], static_cast<uint32_t>((c / kRowStages) & 1));
-        uint32_t key[4 * U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if constexpr (EB == 2) {
-                const uint2 q = reinterpret_cast<const uint2*>(ring + st * kChunkBytes)[u * kRowThreads + tid];
-                key[4 * u] = q.x & 0xFFFFu; key[4 * u + 1] = q.x >> 16;
-                key[4 * u + 2] = q.y & 0xFFFFu; key[4 * u + 3] = q.y >> 16;
-            } else {
-                const uint4 q = reinterpret_cast<const uint4*>(ring + st * kChunkBytes)[u * kRowThreads + tid];
-                key[4 * u] = q.x; key[4 * u + 1] = q.y; key[4 * u + 2] = q.z; key[4 * u + 3] = q.w;
+        for (int g = 0; g < G; ++g) {
+            uint32_t key[4 * UU];
+#pragma unroll
+            for (int u = 0; u < UU; ++u) {
+                const int su = g * UU + u;
+                if constexpr (EB == 2) {
+                    const uint2 q = reinterpret_cast<const uint2*>(ring + st * kChunkBytes)[su * kRowThreads + tid];
+                    key[4 * u] = q.x & 0xFFFFu; key[4 * u + 1] = q.x >> 16;
+                    key[4 * u + 2] = q.y & 0xFFFFu; key[4 * u + 3] = q.y >> 16;
+                } else {
+                    const uint4 q = reinterpret_cast<const uint4*>(ring + st * kChunkBytes)[su * kRowThreads + tid];
+                    key[4 * u] = q.x; key[4 * u + 1] = q.y; key[4 * u + 2] = q.z; key[4 * u + 3] = q.w;
+                }
             }
-        }
-        __syncwarp();
-        if (lane == 0) {
-            __threadfence_block();
-            if (atomicAdd(&s_empty[st], 1u) == kRowWarps - 1) {
-                s_empty[st] = 0;
-                __threadfence_block();
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                if (c + kRowStages < nchunks)
-                    bulk_g2s(ring + st * kChunkBytes, bsrc + (c + kRowStages) * kChunkBytes, kChunkBytes, &bar[st]);
-                if (a.pf) prefetch(c + kRowStages + a.pf);
-            }
-        }
-        uint32_t mask = 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t nb = ~(head + static_cast<uint32_t>(c * kChunk + u * 2048) + tid * 4);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                key[4 * u + i] = key_of<KM>(key[4 * u + i], a.in);
-                const unsigned long long K = (static_cast<unsigned long long>(key[4 * u + i]) << 32) | (nb - i);
-                mask |= static_cast<uint32_t>(K >= T) << (4 * u + i);
-            }
-        }
-        if (__any_sync(full, mask)) {
-            const uint32_t cnt = __popc(mask);
-            uint32_t inc = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(full, inc, d);
-                if (lane >= d) inc += o;
-            }
-            const uint32_t wtot = __shfl_sync(full, inc, 31);
-            uint32_t wbase = 0;
-            if (lane == 31) wbase = atomicAdd(&s_m, wtot);
-            wbase = __shfl_sync(full, wbase, 31);
-            uint32_t o = wbase + inc - cnt;
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t nb = ~(head + static_cast<uint32_t>(c * kChunk + u * 2048) + tid * 4);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if ((mask >> (4 * u + i)) & 1u) {
-                        if (o < kRowCand) cand[o] = (static_cast<unsigned long long>(key[4 * u + i]) << 32) | (nb - i);
-                        ++o;
+            if (g == G - 1) {  // this warp is done reading the stage
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_block();
+                    if (atomicAdd(&s_empty[st], 1u) == kRowWarps - 1) {
+                        s_empty[st] = 0;
+                        __threadfence_block();
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        if (c + kRowStages < nchunks)
+                            bulk_g2s(ring + st * kChunkBytes, bsrc + (c + kRowStages) * kChunkBytes, kChunkBytes,
+                                     &bar[st]);
+                        if (a.pf) prefetch(c + kRowStages + a.pf);
                     }
+                }
+            }
+            uint32_t mask = 0;
+#pragma unroll
+            for (int u = 0; u < UU; ++u) {
+                const uint32_t nb = ~(head + static_cast<uint32_t>(c * kChunk + (g * UU + u) * 2048) + tid * 4);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    key[4 * u + i] = key_of<KM>(key[4 * u + i], a.in);
+                    const unsigned long long K = (static_cast<unsigned long long>(key[4 * u + i]) << 32) | (nb - i);
+                    mask |= static_cast<uint32_t>(K >= T) << (4 * u + i);
+                }
+            }
+            if (__any_sync(full, mask)) {
+                const uint32_t cnt = __popc(mask);
+                uint32_t inc = cnt;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(full, inc, d);
+                    if (lane >= d) inc += o;
+                }
+                const uint32_t wtot = __shfl_sync(full, inc, 31);
+                uint32_t wbase = 0;
+                if (lane == 31) wbase = atomicAdd(&s_m, wtot);
+                wbase = __shfl_sync(full, wbase, 31);
+                uint32_t o = wbase + inc - cnt;
+#pragma unroll
+                for (int u = 0; u < UU; ++u) {
+                    const uint32_t nb = ~(head + static_cast<uint32_t>(c * kChunk + (g * UU + u) * 2048) + tid * 4);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if ((mask >> (4 * u + i)) & 1u) {
+                            if (o < kRowCand) cand[o] = (static_cast<unsigned long long>(key[4 * u + i]) << 32) | (nb - i);
+                            ++o;
+                        }
+                }
             }
         }
     }
@@ -568,14 +576,15 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     // Real keys rarely tie: rank by the KEY bits only, then restore index order inside runs of
     // equal keys with an odd-even transposition (a run of length L settles in <= L rounds);
     // tie-heavy rows fall back to the full composite passes (as cta_sort_group, rtk_sort.cu).
-    const bool key_only = (orv >> 32) != 0 && (orv & 0xffffffffull) != 0;
+    // 16-bit keys tie in runs of tens (65536 values over ~10^5 elements): full composite passes
+    const bool key_only = !km_is16<KM>() && (orv >> 32) != 0 && (orv & 0xffffffffull) != 0;
     lsd(key_only ? 32 : 0);
     if (key_only) {
 #pragma unroll
         for (int q = 0; q < IT; ++q) cand[warp * 256 + q * 32 + lane] = key[q];
         __syncthreads();
         bool prev_sw = true, settled = false;
-        for (int it = 0; it < 64; ++it) {
+        for (int it = 0; it < 24; ++it) {
             bool sw = false;
             for (uint32_t q = tid; 2 * q + 1 < kk; q += kRowThreads) {
                 const uint32_t p = 2 * q + (it & 1);

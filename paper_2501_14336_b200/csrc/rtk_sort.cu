@@ -824,11 +824,12 @@ __device__ __forceinline__ void cta_sort_group(const SortGroup& grp, const SortA
     // bits), then put tied keys back in index order with an odd-even transposition restricted
     // to runs of equal keys (a run of length L settles in <= L rounds). Long runs (tie-heavy
     // groups) fall back to the full composite passes.
-    const bool key_only = (orv >> 32) != 0 && (orv & 0xffffffffull) != 0;
+    // 16-bit keys tie in runs of tens (65536 values over ~10^5 elements): full composite passes
+    const bool key_only = g.dtype != kF16 && (orv >> 32) != 0 && (orv & 0xffffffffull) != 0;
     lsd(key_only ? 32 : 0);
     if (key_only) {
         bool prev_sw = true, settled = false;
-        for (int it = 0; it < 64; ++it) {
+        for (int it = 0; it < 24; ++it) {
             bool sw = false;
             for (uint32_t q = tid; 2 * q + 1 < len; q += kSortThreads) {
                 const uint32_t p = 2 * q + (it & 1);
