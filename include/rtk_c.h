@@ -24,9 +24,9 @@
  * Indices are u64 and row-local (engine.hpp:106, batch.hpp:36-38).
  *
  * rtk_topk* take DEVICE pointers and run on `stream` (a cudaStream_t, NULL = legacy
- * default stream). Round-1 implementation note: the call returns after the stream has
- * drained (it reads candidate counts back between stages). rtk_*_host take HOST pointers
- * and include the host<->device copies.
+ * default stream). The call returns once the device has signalled completion through mapped
+ * host memory (no stream synchronisation; rare paths — exact recomputation, deeper MSD
+ * levels — add host round trips). rtk_*_host take HOST pointers and include the copies.
  *
  * Limits: n <= 2^32 elements per row on one device (the composite key carries a 32-bit
  * row-local index); dtype F32 or U32; scaled mode is F32 only (as in the reference).
@@ -49,6 +49,7 @@ extern "C" {
 #define RTK_CUDA_ERROR 5
 #define RTK_OUT_OF_MEMORY 6
 #define RTK_INTERNAL 7
+#define RTK_IO_ERROR 8             /* std::runtime_error from the RTK1/RTKB readers (io.cpp) */
 
 /* dtypes (io.hpp:19 codes 0/1) and selection order (keycodec.hpp:19) */
 #define RTK_F32 0
@@ -104,6 +105,22 @@ typedef struct rtk_stats {
 } rtk_stats;
 
 typedef struct rtk_handle_s* rtk_handle;
+
+/* mirrors rtk::DistributionSpec (datagen.hpp:18-48); kinds in DistKind order */
+#define RTK_DIST_UNIFORM 0
+#define RTK_DIST_NORMAL 1
+#define RTK_DIST_ZIPF 2
+#define RTK_DIST_PEAKED 3
+typedef struct rtk_dist {
+    int32_t kind;
+    double a;          /* Uniform lower / Normal mean       (default 0)   */
+    double b;          /* Uniform upper / Normal stddev     (default 1)   */
+    double s;          /* Zipf skewness                     (default 1.1) */
+    double mass;       /* Peaked: probability mass on modes (default 0.8) */
+    uint32_t modes;    /* Peaked: number of modes           (default 1)   */
+    uint64_t seed;
+    uint64_t n;
+} rtk_dist;
 
 /* library / handle */
 const char* rtk_version(void);
@@ -178,6 +195,24 @@ int rtk_merge_shards(rtk_handle h, const void* d_cand_vals, const uint64_t* d_ca
                      const uint64_t* block_len, const uint64_t* shard_base, uint32_t G,
                      uint64_t k, int dtype, int order, void* d_out_vals, uint64_t* d_out_idx,
                      void* d_out_pivot, void* stream);
+
+/* ---- harness utilities (host only) -----------------------------------
+ * rtk_generate        <- rtk::generate<float|uint32_t>     datagen.hpp:68-140 (same mt19937_64
+ *                        streams and libstdc++ distributions, so inputs are bit-identical)
+ * rtk_result_checksum <- result_checksum                   rtk_cli.cpp:100-115 (FNV-1a over
+ *                        value bits then the u64 index, element by element)
+ * rtk_write_dataset / rtk_read_dataset <- rtk::write_dataset / read_dataset  io.cpp:38-80 (RTK1;
+ *                        dtype codes 0 f32, 1 u32, 2 f16 — accepted here — and 3 bf16)
+ * rtk_write_batch / rtk_read_batch     <- rtk::write_batch / read_batch      io.cpp:82-110 (RTKB)
+ * Readers are two-call: pass NULL outputs to query the sizes first. */
+int rtk_generate(const rtk_dist* spec, int dtype, void* out);
+uint64_t rtk_result_checksum(const void* values, int dtype, const uint64_t* indices, uint64_t k);
+int rtk_write_dataset(const char* path, int dtype, const void* data, uint64_t n);
+int rtk_read_dataset(const char* path, int* dtype, uint64_t* n, void* out, uint64_t capacity);
+int rtk_write_batch(const char* path, const uint64_t* lengths, uint32_t tasks, const void* payload,
+                    uint64_t payload_bytes);
+int rtk_read_batch(const char* path, uint32_t* tasks, uint64_t* payload_bytes, uint64_t* lengths,
+                   void* payload);
 
 #ifdef __cplusplus
 }

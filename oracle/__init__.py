@@ -99,6 +99,11 @@ def ref() -> C.CDLL:
         lib.ref_select_bin.argtypes = [vp, u64, u64, vp, vp]
         lib.ref_encode_f32.argtypes = [C.c_float, C.c_int]
         lib.ref_encode_f32.restype = u32
+        lib.ref_io_error.restype = C.c_char_p
+        lib.ref_write_dataset.argtypes = [C.c_char_p, C.c_int, vp, u64]
+        lib.ref_read_dataset.argtypes = [C.c_char_p, C.POINTER(C.c_int), P64, vp]
+        lib.ref_write_batch.argtypes = [C.c_char_p, P64, u32, vp, u64]
+        lib.ref_read_batch.argtypes = [C.c_char_p, C.POINTER(u32), P64, P64, vp]
         _ref = lib
     return _ref
 
@@ -197,6 +202,39 @@ def ref_generate(kind: int, n: int, seed: int, dtype=np.float32, a: float = 0.0,
     out = np.empty(n, dtype=dtype)
     _ck(ref().ref_generate(kind, a, b, s, mass, modes, seed, n, _dt(out), out.ctypes.data))
     return out
+
+
+def _io_ck(code: int) -> None:
+    if code:
+        raise RuntimeError(ref().ref_io_error().decode())
+
+
+def ref_write_dataset(path: str, x: np.ndarray) -> None:  # rtk::write_dataset (io.cpp:38-44)
+    x = np.ascontiguousarray(x)
+    _io_ck(ref().ref_write_dataset(str(path).encode(), _dt(x), x.ctypes.data, x.size))
+
+
+def ref_read_dataset(path: str):  # rtk::read_dataset (io.cpp:46-80) -> (dtype code, array)
+    dt, n = C.c_int(0), C.c_uint64(0)
+    _io_ck(ref().ref_read_dataset(str(path).encode(), C.byref(dt), C.byref(n), None))
+    out = np.empty(n.value, dtype=np.float32 if dt.value == 0 else np.uint32)
+    _io_ck(ref().ref_read_dataset(str(path).encode(), C.byref(dt), C.byref(n), out.ctypes.data))
+    return dt.value, out
+
+
+def ref_write_batch(path: str, lengths, payload: bytes) -> None:  # io.cpp:82-92
+    ln = np.ascontiguousarray(np.asarray(lengths, dtype=np.uint64))
+    pb = np.frombuffer(payload, dtype=np.uint8)
+    _io_ck(ref().ref_write_batch(str(path).encode(), ln.ctypes.data_as(P64), len(ln), pb.ctypes.data, pb.size))
+
+
+def ref_read_batch(path: str):  # io.cpp:94-110 -> (lengths, payload bytes)
+    t, nb = C.c_uint32(0), C.c_uint64(0)
+    _io_ck(ref().ref_read_batch(str(path).encode(), C.byref(t), C.byref(nb), None, None))
+    ln = np.empty(t.value, dtype=np.uint64)
+    pb = np.empty(nb.value, dtype=np.uint8)
+    _io_ck(ref().ref_read_batch(str(path).encode(), C.byref(t), C.byref(nb), ln.ctypes.data_as(P64), pb.ctypes.data))
+    return [int(v) for v in ln], pb.tobytes()
 
 
 def ref_topk(x: np.ndarray, k: int, order: int = 0, d: int = 12, grid: int = 1) -> Result:

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <string>
 #include <span>
 #include <stdexcept>
 #include <vector>
@@ -15,6 +16,7 @@
 #include "rtk/batch.hpp"
 #include "rtk/datagen.hpp"
 #include "rtk/engine.hpp"
+#include "rtk/io.hpp"
 #include "rtk/oracle.hpp"
 #include "rtk/scaling.hpp"
 
@@ -215,5 +217,63 @@ int ref_select_bin(const std::uint64_t* hist, std::uint64_t nbins, std::uint64_t
 }
 
 std::uint32_t ref_encode_f32(float v, int order) { return rtk::encode_key(v, ord(order)).bits; }
+
+// ---- rtk/io.hpp (io.cpp compiled in place): RTK1 / RTKB containers ------------------------
+static thread_local std::string g_io_msg;
+const char* ref_io_error(void) { return g_io_msg.c_str(); }
+
+int ref_write_dataset(const char* path, int dtype, const void* data, std::uint64_t n) {
+    try {
+        if (dtype == 0) rtk::write_dataset(path, std::span<const float>(static_cast<const float*>(data), n));
+        else rtk::write_dataset(path, std::span<const std::uint32_t>(static_cast<const std::uint32_t*>(data), n));
+        return OK;
+    } catch (const std::exception& e) {
+        g_io_msg = e.what();
+        return OTHER;
+    }
+}
+
+// two-call: out == nullptr returns dtype / count only
+int ref_read_dataset(const char* path, int* dtype, std::uint64_t* n, void* out) {
+    try {
+        rtk::Dataset ds = rtk::read_dataset(path);
+        *dtype = static_cast<int>(ds.dtype);
+        *n = ds.size();
+        if (out) std::memcpy(out, ds.dtype == rtk::DType::F32 ? static_cast<const void*>(ds.f32.data())
+                                                              : static_cast<const void*>(ds.u32.data()),
+                             ds.size() * 4);
+        return OK;
+    } catch (const std::exception& e) {
+        g_io_msg = e.what();
+        return OTHER;
+    }
+}
+
+int ref_write_batch(const char* path, const std::uint64_t* lengths, std::uint32_t tasks, const void* payload,
+                    std::uint64_t bytes) {
+    try {
+        rtk::write_batch(path, std::vector<std::uint64_t>(lengths, lengths + tasks),
+                         std::span<const std::uint8_t>(static_cast<const std::uint8_t*>(payload), bytes));
+        return OK;
+    } catch (const std::exception& e) {
+        g_io_msg = e.what();
+        return OTHER;
+    }
+}
+
+int ref_read_batch(const char* path, std::uint32_t* tasks, std::uint64_t* bytes, std::uint64_t* lengths,
+                   void* payload) {
+    try {
+        rtk::BatchFile b = rtk::read_batch(path);
+        *tasks = static_cast<std::uint32_t>(b.lengths.size());
+        *bytes = b.payload.size();
+        if (lengths) std::memcpy(lengths, b.lengths.data(), b.lengths.size() * 8);
+        if (payload) std::memcpy(payload, b.payload.data(), b.payload.size());
+        return OK;
+    } catch (const std::exception& e) {
+        g_io_msg = e.what();
+        return OTHER;
+    }
+}
 
 }  // extern "C"

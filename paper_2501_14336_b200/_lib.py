@@ -28,6 +28,7 @@ RTK_INVALID_ARGUMENT = 4
 RTK_CUDA_ERROR = 5
 RTK_OUT_OF_MEMORY = 6
 RTK_INTERNAL = 7
+RTK_IO_ERROR = 8
 
 
 class rtk_cfg(C.Structure):
@@ -47,6 +48,11 @@ class rtk_stats(C.Structure):
     _fields_ = [("passes", u64), ("elements_scanned", u64), ("candidates", u64),
                 ("fallback_rows", u64), ("kernel_launches", u64), ("compact_ms", C.c_float),
                 ("total_ms", C.c_float)]
+
+
+class rtk_dist(C.Structure):
+    _fields_ = [("kind", i32), ("a", C.c_double), ("b", C.c_double), ("s", C.c_double),
+                ("mass", C.c_double), ("modes", u32), ("seed", u64), ("n", u64)]
 
 
 # name -> (restype, argtypes); exactly the entry points include/rtk_c.h declares
@@ -75,6 +81,12 @@ SIGNATURES = {
     "rtk_topk_scaled_host": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, C.c_double, u64, vp, vp,
                                        vp, C.POINTER(rtk_scale_info), C.POINTER(rtk_cfg)]),
     "rtk_merge_shards": (C.c_int, [vp, vp, vp, P64, P64, u32, u64, C.c_int, C.c_int, vp, vp, vp, vp]),
+    "rtk_generate": (C.c_int, [C.POINTER(rtk_dist), C.c_int, vp]),
+    "rtk_result_checksum": (u64, [vp, C.c_int, P64, u64]),
+    "rtk_write_dataset": (C.c_int, [C.c_char_p, C.c_int, vp, u64]),
+    "rtk_read_dataset": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), P64, vp, u64]),
+    "rtk_write_batch": (C.c_int, [C.c_char_p, P64, u32, vp, u64]),
+    "rtk_read_batch": (C.c_int, [C.c_char_p, C.POINTER(u32), P64, P64, vp]),
 }
 
 _lib = None

@@ -11,6 +11,7 @@
 
 #include "../../include/rtk_c.h"
 #include "rtk_engine.h"
+#include "rtk_guard.h"
 
 using rtk_b200::Engine;
 using rtk_b200::Error;
@@ -21,29 +22,12 @@ struct rtk_handle_s {
     explicit rtk_handle_s(int dev) : engine(dev) {}
 };
 
+thread_local std::string rtk_b200::g_last_error;
+using rtk_b200::fail;
+using rtk_b200::g_last_error;
+using rtk_b200::guarded;
+
 namespace {
-
-thread_local std::string g_last_error;
-
-int fail(int code, const std::string& msg) {
-    g_last_error = msg;
-    return code;
-}
-
-template <typename F>
-int guarded(F&& f) {
-    try {
-        f();
-        g_last_error.clear();
-        return RTK_OK;
-    } catch (const Error& e) {
-        return fail(e.code, e.msg);
-    } catch (const std::bad_alloc&) {
-        return fail(RTK_OUT_OF_MEMORY, "host allocation failed");
-    } catch (const std::exception& e) {
-        return fail(RTK_INTERNAL, e.what());
-    }
-}
 
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw Error{RTK_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e)};

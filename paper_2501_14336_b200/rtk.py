@@ -67,6 +67,8 @@ def _raise(status: int, where: str = "") -> None:
         raise ValueError(msg)
     if status == L.RTK_OUT_OF_MEMORY:
         raise MemoryError(msg)
+    if status == L.RTK_IO_ERROR:
+        raise RuntimeError(msg)
     raise cuda_error(f"status {status}: {msg}")
 
 

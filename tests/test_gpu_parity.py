@@ -395,3 +395,23 @@ def test_sharded_query_merge_on_device(cuda, G, kind):
         bases.append(s0)
     m = rtk.merge_shards(torch.cat(vals), torch.cat(idx), [k] * G, bases, k)
     assert_same((m.values, m.indices, m.pivot), O.ref_topk(x, k, 0, grid=4), f"G={G} kind={kind}")
+
+
+# ---- bench/report harness ------------------------------------------------
+def test_report_bench_checksum_matches_reference(cuda):
+    # `rtk bench` cell semantics (rtk_cli.cpp:372-420): tasks seeded seed + 100 t + n + k, the first
+    # one n - 1 long, checksum = XOR of per-task FNV-1a; the reference's batch_topk on the same
+    # inputs must give the same checksum
+    from paper_2501_14336_b200 import report
+    n, k, B, seed = 1 << 16, 100, 3, 4
+    rep = report.bench([n], [k], batch=B, repeats=2, seed=seed, verify=True)
+    cell = rep["cells"][0]
+    assert cell["verified"] and "error" not in cell
+    want = 0
+    for t in range(B):
+        x = O.ref_generate(0, n - 1 if t == 0 else n, seed + 100 * t + n + k)
+        v, i, _ = O.ref_topk(x, k, 0, grid=4)
+        want ^= report.result_checksum(v, i)
+    assert cell["checksum"] == want
+    q = report.bench([4096], [], batch=1, repeats=1, quantile=True)
+    assert [c["k"] for c in q["cells"]] == [40, 1024, 2048]
