@@ -196,6 +196,18 @@ int rtk_merge_shards(rtk_handle h, const void* d_cand_vals, const uint64_t* d_ca
                      uint64_t k, int dtype, int order, void* d_out_vals, uint64_t* d_out_idx,
                      void* d_out_pivot, void* stream);
 
+/* LLM sampling consumer: top-k of B logit rows (row b at
+ * d_logits + b*row_stride elements, V elements, dtype F32/F16/BF16), then per row, in fp32:
+ *   e_j = expf((v_j - v_0) / temperature) over the top-k in canonical order (v_0 = row max);
+ *   m = shortest prefix with sum_{j<m} e_j >= top_p * sum_j e_j (top_p = 1 keeps all k);
+ *   token = index of the first j < m with sum_{i<=j} e_i > u_b * sum_{i<m} e_i (u_b = d_uniform[b],
+ *   in [0, 1)); d_probs (nullable, B*k) = e_j / sum_{i<m} e_i for j < m, else 0.
+ * d_topk_vals / d_topk_idx (nullable, B*k) receive the top-k itself (handle workspace if NULL).
+ * Device pointers, stream-ordered. Tokens are row-local u64 indices. */
+int rtk_topk_sample(rtk_handle h, const void* d_logits, uint64_t B, uint64_t V, uint64_t row_stride, int dtype,
+                    uint64_t k, float top_p, float temperature, const float* d_uniform, uint64_t* d_token,
+                    float* d_probs, void* d_topk_vals, uint64_t* d_topk_idx, void* stream);
+
 /* ---- harness utilities (host only) -----------------------------------
  * rtk_generate        <- rtk::generate<float|uint32_t>     datagen.hpp:68-140 (same mt19937_64
  *                        streams and libstdc++ distributions, so inputs are bit-identical)

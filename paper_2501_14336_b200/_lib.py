@@ -81,6 +81,8 @@ SIGNATURES = {
     "rtk_topk_scaled_host": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, C.c_double, u64, vp, vp,
                                        vp, C.POINTER(rtk_scale_info), C.POINTER(rtk_cfg)]),
     "rtk_merge_shards": (C.c_int, [vp, vp, vp, P64, P64, u32, u64, C.c_int, C.c_int, vp, vp, vp, vp]),
+    "rtk_topk_sample": (C.c_int, [vp, vp, u64, u64, u64, C.c_int, u64, C.c_float, C.c_float, vp, vp, vp, vp,
+                                  vp, vp]),
     "rtk_generate": (C.c_int, [C.POINTER(rtk_dist), C.c_int, vp]),
     "rtk_result_checksum": (u64, [vp, C.c_int, P64, u64]),
     "rtk_write_dataset": (C.c_int, [C.c_char_p, C.c_int, vp, u64]),

@@ -19,7 +19,12 @@ using rtk_b200::RowReq;
 
 struct rtk_handle_s {
     Engine engine;
+    rtk_b200::DevBuf smp_vals, smp_idx;  // top-k workspace of rtk_topk_sample (when not supplied)
     explicit rtk_handle_s(int dev) : engine(dev) {}
+    ~rtk_handle_s() {
+        smp_vals.release();
+        smp_idx.release();
+    }
 };
 
 thread_local std::string rtk_b200::g_last_error;
@@ -305,6 +310,46 @@ int rtk_topk_scaled(rtk_handle h, const float* d_in, uint64_t n, uint64_t k, int
         check_common(d_in, n, k, RTK_F32, order, c, "scaled_topk");
         run_scaled(h->engine, d_in, n, k, order, mode, trigger_fraction, seed, d_out_vals, d_out_idx,
                    d_out_pivot, info, c, static_cast<cudaStream_t>(stream));
+    });
+}
+
+// LLM sampling consumer: batched top-k of B logit rows, then softmax /
+// top-p / one inverse-CDF draw per row (rtk_sample.cu) on the same stream.
+int rtk_topk_sample(rtk_handle h, const void* d_logits, uint64_t B, uint64_t V, uint64_t row_stride, int dtype,
+                    uint64_t k, float top_p, float temperature, const float* d_uniform, uint64_t* d_token,
+                    float* d_probs, void* d_topk_vals, uint64_t* d_topk_idx, void* stream) {
+    return guarded([&] {
+        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+        if (B == 0) throw Error{RTK_INVALID_ARGUMENT, "sample: no rows"};
+        if (V == 0) throw Error{RTK_EMPTY_INPUT, "sample: empty rows"};
+        if (k == 0 || k > V) throw Error{RTK_RANK_OUT_OF_RANGE, "sample: k outside [1, V]"};
+        if (row_stride < V) throw Error{RTK_INVALID_ARGUMENT, "sample: row_stride < V"};
+        if (dtype != RTK_F32 && dtype != RTK_F16 && dtype != RTK_BF16)
+            throw Error{RTK_INVALID_ARGUMENT, "sample: logits must be F32, F16 or BF16"};
+        if (!(top_p > 0.f && top_p <= 1.f)) throw Error{RTK_INVALID_ARGUMENT, "sample: top_p must be in (0, 1]"};
+        if (!(temperature > 0.f)) throw Error{RTK_INVALID_ARGUMENT, "sample: temperature must be > 0"};
+        if (!d_logits || !d_uniform || !d_token) throw Error{RTK_INVALID_ARGUMENT, "sample: null argument"};
+        if (V > (uint64_t(1) << 32)) throw Error{RTK_INVALID_ARGUMENT, "sample: V > 2^32"};
+        Engine& e = h->engine;
+        cuda_check(cudaSetDevice(e.device()), "cudaSetDevice");
+        void* tv = d_topk_vals;
+        uint64_t* ti = d_topk_idx;
+        if (!tv) {
+            h->smp_vals.ensure(esize(dtype) * B * k);
+            tv = h->smp_vals.p;
+        }
+        if (!ti) {
+            h->smp_idx.ensure(8 * B * k);
+            ti = h->smp_idx.as<uint64_t>();
+        }
+        std::vector<RowReq> rows(B);
+        for (uint64_t b = 0; b < B; ++b) rows[b] = RowReq{b * row_stride, V, k, b * k};
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        e.run(static_cast<const uint32_t*>(d_logits), eng_dtype(dtype), RTK_LARGEST, false, 0.0f, false, rows,
+              static_cast<uint32_t*>(tv), ti, nullptr, s);
+        const int fmt = dtype == RTK_F32 ? 0 : (dtype == RTK_F16 ? 2 : 3);
+        rtk_b200::launch_sample_rows(B, tv, fmt, ti, k, top_p, temperature, d_uniform, d_token, d_probs, s);
+        cuda_check(cudaGetLastError(), "sample launch");
     });
 }
 

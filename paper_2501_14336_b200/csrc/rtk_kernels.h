@@ -277,6 +277,8 @@ void launch_rows_fused(int R, const RowsFusedArgs& a, bool small, cudaStream_t s
 uint32_t rows_fused_kmax(bool small);
 uint32_t rows_fused_cand(bool small);
 uint32_t rows_fused_sample(bool small);
+void launch_sample_rows(uint64_t rows, const void* vals, int fmt, const uint64_t* idx, uint64_t k, float top_p,
+                        float temperature, const float* uniform, uint64_t* token, float* probs, cudaStream_t s);
 void launch_scale_decide(int mode, const unsigned long long* hist, uint32_t nbins, uint64_t n, uint64_t k,
                          double tau, const uint32_t* x, uint64_t a_index, uint32_t* out,
                          volatile uint32_t* host_out, cudaStream_t s);

@@ -534,3 +534,34 @@ def merge_shards(cand_vals, cand_idx, block_len: Sequence[int], shard_base: Sequ
                               C.c_void_p(piv.data_ptr()), _stream_ptr(cv))
     _raise(st, "rtk_merge_shards")
     return TopKResult(vals, idx, pivot_fn=lambda: piv[0].item())
+
+
+# ---- LLM sampling consumer --------------------------------------------------
+def topk_sample(logits, k: int, top_p: float = 1.0, temperature: float = 1.0, uniform=None, generator=None,
+                return_probs: bool = False):
+    """Top-k -> softmax -> top-p -> one draw per row, on the device (rtk_topk_sample, rtk_c.h).
+
+    ``logits``: CUDA tensor [B, V] (float32 / float16 / bfloat16, unit stride along V). ``uniform``:
+    [B] float32 CUDA tensor of draws in [0, 1) (``torch.rand`` with ``generator`` if None).
+    Returns the sampled row-local token ids (int64 [B]); with ``return_probs`` also the renormalised
+    top-k/top-p probabilities [B, k] (0 past the nucleus) and the top-k indices [B, k], whose
+    order is the reference's canonical top-k order.
+    """
+    import torch
+    if not _is_cuda(logits) or logits.dim() != 2 or logits.stride(1) != 1:
+        raise ValueError("topk_sample: logits must be a 2-D CUDA tensor with unit stride along V")
+    B, V = logits.shape
+    dev = logits.device
+    if uniform is None:
+        uniform = torch.rand(B, device=dev, generator=generator, dtype=torch.float32)
+    uniform = uniform.to(device=dev, dtype=torch.float32).contiguous()
+    token = torch.empty(B, dtype=torch.int64, device=dev)
+    probs = torch.empty((B, k), dtype=torch.float32, device=dev) if return_probs else None
+    tv = torch.empty((B, k), dtype=logits.dtype, device=dev) if return_probs else None
+    ti = torch.empty((B, k), dtype=torch.int64, device=dev) if return_probs else None
+    ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+    st = L.load().rtk_topk_sample(_handle(dev.index or 0), ptr(logits), B, V, logits.stride(0),
+                                  _dtype_code(logits), int(k), float(top_p), float(temperature), ptr(uniform),
+                                  ptr(token), ptr(probs), ptr(tv), ptr(ti), _stream_ptr(logits))
+    _raise(st, "rtk_topk_sample")
+    return (token, probs, ti) if return_probs else token

@@ -415,3 +415,58 @@ def test_report_bench_checksum_matches_reference(cuda):
     assert cell["checksum"] == want
     q = report.bench([4096], [], batch=1, repeats=1, quantile=True)
     assert [c["k"] for c in q["cells"]] == [40, 1024, 2048]
+
+
+# ---- LLM sampling consumer --------------------------------------------------
+def _sample_ref(v: np.ndarray, idx: np.ndarray, top_p: float, T: float, u: float):
+    """fp64 restatement of rtk_topk_sample's definition (rtk_c.h) on one row's canonical top-k."""
+    e = np.exp((v.astype(np.float64) - float(v[0])) / T)
+    c = np.cumsum(e)
+    m = len(e) if top_p >= 1.0 else int(np.searchsorted(c, top_p * c[-1], side="left")) + 1
+    m = min(m, len(e))
+    q = e[:m] / c[m - 1]
+    cq = np.cumsum(q)
+    j = min(int(np.searchsorted(cq, u, side="right")), m - 1)
+    return int(idx[j]), q, m, cq
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
+@pytest.mark.parametrize("k,top_p,T", [(50, 0.9, 1.0), (1, 1.0, 1.0), (4096, 0.95, 0.7), (128256, 0.5, 1.3),
+                                       (200, 1.0, 2.0)])
+def test_topk_sample(cuda, dtype, k, top_p, T):
+    import torch
+    rtk = _rtk()
+    B, V = 24, 128256
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7 + k)
+    logits = (torch.randn(B, V, device=cuda, generator=g) * 3).to(
+        {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}[dtype])
+    u = torch.rand(B, device=cuda, generator=g)
+    tok, probs, ti = rtk.topk_sample(logits, k, top_p=top_p, temperature=T, uniform=u, return_probs=True)
+    plain = rtk.topk_sample(logits, k, top_p=top_p, temperature=T, uniform=u)
+    assert torch.equal(tok, plain)
+    L = logits.float().cpu().numpy()
+    tok, probs, ti, u = tok.cpu().numpy(), probs.cpu().numpy(), ti.cpu().numpy(), u.cpu().numpy()
+    for b in range(B):
+        # the top-k indices are the exact canonical top-k (checked bit-exactly elsewhere); values
+        # are the logits at those indices
+        v = L[b, ti[b]]
+        assert np.all(v[:-1] >= v[1:])
+        want, q, m, cq = _sample_ref(v, ti[b], top_p, T, float(u[b]))
+        assert np.allclose(probs[b, :m], q, rtol=1e-4, atol=2e-6), f"row {b} probs"
+        margin = np.min(np.abs(cq - u[b])) if m > 0 else 1.0
+        if margin > 1e-5:  # u not within fp32 rounding of a CDF step
+            assert tok[b] == want, f"row {b}: token {tok[b]} != {want} (u={u[b]}, margin {margin})"
+        assert np.all(probs[b, m + 2:] == 0)
+
+
+def test_topk_sample_errors(cuda):
+    import torch
+    rtk = _rtk()
+    x = torch.randn(2, 100, device=cuda)
+    with pytest.raises(ValueError, match="top_p"):
+        rtk.topk_sample(x, 5, top_p=0.0)
+    with pytest.raises(ValueError, match="temperature"):
+        rtk.topk_sample(x, 5, temperature=0.0)
+    with pytest.raises(IndexError):
+        rtk.topk_sample(x, 101)
