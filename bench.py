@@ -271,7 +271,7 @@ def main():
         del xa
 
     # C3: batched LLM sampling top-k, rows sharded across ranks (no collective)
-    batch_llm, batch_bf16 = {}, {}
+    batch_llm, batch_bf16, sampling = {}, {}, {}
     if args.batch_ks:
         from paper_2501_14336_b200 import sharded as SH
         r0, r1 = SH.row_shard(args.batch_rows, world, rank)
@@ -303,6 +303,23 @@ def main():
             batch_bf16[str(kb)] = {"ms_per_batch": ms_h, "queries_per_s": args.batch_rows / (ms_h * 1e-3),
                                    "effective_GBps": byts / (ms_h * 1e-3) / 1e9,
                                    "fraction_of_hbm_peak": byts / (ms_h * 1e-3) / 1e9 / peak}
+        # LLM sampling consumer: top-k 50 -> softmax -> top-p 0.9 -> one draw per
+        # row, through rtk.topk_sample (Python loop, torch events, L2 flushed outside the events)
+        sampling = {}
+        u = torch.rand(rows_here, device=dev, generator=gen)
+        for kb, tp in ((50, 0.9), (4096, 0.95)):
+            ev = []
+            for it in range(3 + max(5, args.steps // 2)):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                R.topk_sample(logits, kb, top_p=tp, temperature=1.0, uniform=u)
+                e1.record()
+                if it >= 3:
+                    ev.append((e0, e1))
+            torch.cuda.synchronize()
+            ms_s = statistics.median(a.elapsed_time(b) for a, b in ev)
+            sampling[f"k{kb}_p{tp}"] = {"ms_per_batch": ms_s, "queries_per_s": args.batch_rows / (ms_s * 1e-3)}
         del logits, flush, lb
 
     # e2e through the host entry point (rank 0 / N=1 semantics: per-GPU query from pinned host)
@@ -359,6 +376,8 @@ def main():
                                             "tau=0.5 seed=31 (device-resident)", "results": adversarial},
                "batch_llm_bf16": {"config": "the same logits rounded to bf16 (2 B per element; bytes = "
                                             "rows * (2V + 10k))", "results": batch_bf16},
+               "llm_sampling": {"config": "the fp32 logits batch: top-k -> softmax -> top-p -> one draw per row "
+                                          "(rtk.topk_sample, Python loop, torch events)", "results": sampling},
                "batch_llm": {"config": f"{args.batch_rows} x {args.vocab} fp32 N(0,1) logits, rows sharded over "
                                        f"{world} GPU(s), L2 flushed between batches", "results": batch_llm},
                "step_ms_all": ms}

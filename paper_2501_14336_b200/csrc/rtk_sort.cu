@@ -17,6 +17,7 @@
 // The host only reads two flags after the final synchronisation; deeper MSD levels and
 // the exact path run only when a flag asks for them.
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -1004,7 +1005,11 @@ void launch_sort_groups(uint32_t max_groups, const SortArgs& g, cudaStream_t s) 
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    static const bool no_pdl = [] {
+        const char* e = std::getenv("RTK_NO_PDL_SORT");
+        return e && *e && *e != '0';
+    }();
+    cfg.numAttrs = no_pdl ? 0 : 1;
     cudaLaunchKernelEx(&cfg, k_sort_groups, g);
 }
 
