@@ -85,6 +85,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_SPARSE_MAX")) sparse_max_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_ROWS_PF")) rows_pf_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_MSD_CS")) msd_cs_ = std::atoi(g);
+    if (const char* g = std::getenv("RTK_TILE_CONTIG")) tile_contig_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_DENSE_BITS")) dense_bits_ = static_cast<uint32_t>(std::atoi(g));
     const char* cs = std::getenv("RTK_COUNT_STATS");
     count_stats_ = profile_ || (cs && *cs && *cs != '0');
@@ -710,6 +711,8 @@ PlanArgs Engine::plan_args(const Call& c, const FinishPrep& f) {
     pa.kmin = kmin_.as<unsigned long long>();
     pa.kmax = kmax_.as<unsigned long long>();
     pa.kor = kor_.as<uint32_t>();
+    // interleaved tiles stream ~12% faster for one huge row; many rows prefer contiguous runs
+    pa.contig = tile_contig_ >= 0 ? static_cast<uint32_t>(tile_contig_) : (f.NR > 8 ? 1u : 0u);
     pa.slots = slots0_.as<SegSlot>();
     pa.groups = f.gl;
     pa.flags = ctl_.as<uint32_t>();

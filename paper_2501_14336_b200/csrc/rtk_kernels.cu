@@ -459,7 +459,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
     // inside the 126 MB L2), then waits for the thresholds.
     if (threadIdx.x < 8) {
         const uint64_t budget = (static_cast<uint64_t>(pa.prefetch_mb) << 20) / (static_cast<uint64_t>(gridDim.x) * kTile * 4);
-        const uint64_t t = blockIdx.x + threadIdx.x * static_cast<uint64_t>(gridDim.x);
+        const uint64_t t = pa.contig ? blockIdx.x * ((ntiles + gridDim.x - 1) / gridDim.x) + threadIdx.x
+                                     : blockIdx.x + threadIdx.x * static_cast<uint64_t>(gridDim.x);
         if (threadIdx.x < budget && t < ntiles) {
             const int j0 = row_of_tile(rows, t);
             const uint64_t sp0 = (t - rows.tile_start[j0]) * kTile;
@@ -527,7 +528,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
 
     // interleaved tile order (CTA b: tiles b, b+G, ...): measured ~12% faster streaming on B200
     // than contiguous runs per CTA, at the price of a row switch per tile in many-row batches
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    // many-row batches: contiguous tile runs per CTA (one row switch per run instead of per tile)
+    const uint64_t per = pa.contig ? (ntiles + gridDim.x - 1) / gridDim.x : 1;
+    const uint64_t t_begin = pa.contig ? blockIdx.x * per : blockIdx.x;
+    const uint64_t t_end = pa.contig ? min(ntiles, t_begin + per) : ntiles;
+    const uint64_t t_step = pa.contig ? 1 : gridDim.x;
+    for (uint64_t t = t_begin; t < t_end; t += t_step) {
         if (t >= tile1 || cur < 0) {
             if (cur >= 0) finish_row();
             const int j = row_of_tile(rows, t);
