@@ -325,13 +325,15 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
         __syncthreads();
         const unsigned int hi = digit_hi(pos);
         const uint32_t dmask = (1u << (hi - pos)) - 1u;
-        // every element left in `cur` matches the prefix (compacted after each pass); four
-        // warp-interleaved sub-histograms: the clustered top digit of real data hits few bins
+        // samples outside the selected prefix are skipped in place (no compaction between
+        // passes: <= 8 samples per thread); four warp-interleaved sub-histograms: the clustered
+        // top digit of real data hits few bins
         uint32_t* hmine = hsub + (warp & 3) * kBins;
+        const unsigned long long pm = hi >= 64 ? 0ull : (prefix >> hi);
         for (uint32_t i = tid; i < ((local + 31) & ~31u); i += blockDim.x) {
             const bool in_range = i < local;
             const unsigned long long K = in_range ? cur[i] : 0ull;
-            if (in_range) atomicAdd(hmine + (static_cast<uint32_t>(K >> pos) & dmask), 1u);
+            if (in_range && (hi >= 64 || (K >> hi) == pm)) atomicAdd(hmine + (static_cast<uint32_t>(K >> pos) & dmask), 1u);
         }
         __syncthreads();
         for (int b = tid; b < kBins; b += blockDim.x)
@@ -391,24 +393,7 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
         k_rem -= s_res[1];
         const unsigned long long count_ge = above + s_res[2];
         if (count_ge <= target || pos == 0) break;
-        // keep only the samples inside the selected bin for the next pass
-        if (tid == 0) s_cnt = 0;
-        __syncthreads();
-        const unsigned long long want = prefix >> pos;
-        for (uint32_t i = tid; i < ((local + 31) & ~31u); i += blockDim.x) {
-            const bool keep = i < local && (cur[i] >> pos) == want;
-            const unsigned bal = __ballot_sync(0xffffffffu, keep);
-            uint32_t base = 0;
-            if (lane == 0 && bal) base = atomicAdd(&s_cnt, __popc(bal));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (keep) alt[base + __popc(bal & ((1u << lane) - 1u))] = cur[i];
-        }
-        __syncthreads();
         stamp();
-        local = s_cnt;
-        unsigned long long* t = cur;
-        cur = alt;
-        alt = t;
         pos = pos == 9 ? 0u : pos - 11u;
     }
     cluster.sync();  // no CTA leaves while another may still read its shared memory
