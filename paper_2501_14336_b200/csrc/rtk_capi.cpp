@@ -218,20 +218,22 @@ int rtk_bench_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int d
             const int st = rtk_topk(h, d_in, n, k, dtype, order, d_out_vals, d_out_idx, d_out_pivot, cfg, stream);
             if (st != RTK_OK) throw Error{st, g_last_error};
         }
-        std::vector<cudaEvent_t> ev(steps + 1);
+        // per step: events the engine records right before its first and after its last device
+        // operation of the call (host planning and the host's completion wait excluded)
+        std::vector<cudaEvent_t> ev(2 * steps);
         for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
         cuda_check(cudaStreamSynchronize(s), "sync");
-        cuda_check(cudaEventRecord(ev[0], s), "event");
         for (int i = 0; i < steps; ++i) {
+            h->engine.set_call_events(ev[2 * i], ev[2 * i + 1]);
             const int st = rtk_topk(h, d_in, n, k, dtype, order, d_out_vals, d_out_idx, d_out_pivot, cfg, stream);
+            h->engine.set_call_events(nullptr, nullptr);
             if (st != RTK_OK) throw Error{st, g_last_error};
-            cuda_check(cudaEventRecord(ev[i + 1], s), "event");
         }
         cuda_check(cudaStreamSynchronize(s), "sync");
         double sum = 0;
         for (int i = 0; i < steps; ++i) {
             float ms = 0;
-            cuda_check(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]), "elapsed");
+            cuda_check(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]), "elapsed");
             if (step_ms) step_ms[i] = ms;
             sum += ms;
         }
@@ -258,9 +260,14 @@ int rtk_bench_batched(rtk_handle h, const void* d_data, uint64_t data_len, const
         for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
         for (int i = 0; i < steps; ++i) {
             if (d_flush && flush_bytes) cuda_check(cudaMemsetAsync(d_flush, i & 0xff, flush_bytes, s), "flush");
-            cuda_check(cudaEventRecord(ev[2 * i], s), "event");
-            one();
-            cuda_check(cudaEventRecord(ev[2 * i + 1], s), "event");
+            h->engine.set_call_events(ev[2 * i], ev[2 * i + 1]);
+            try {
+                one();
+            } catch (...) {
+                h->engine.set_call_events(nullptr, nullptr);
+                throw;
+            }
+            h->engine.set_call_events(nullptr, nullptr);
         }
         cuda_check(cudaStreamSynchronize(s), "sync");
         double sum = 0;

@@ -84,6 +84,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_NO_DENSE")) no_dense_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_SPARSE_MAX")) sparse_max_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_ROWS_PF")) rows_pf_ = std::atoi(g);
+    if (const char* g = std::getenv("RTK_ROWS_TRACE")) rows_trace_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_MSD_CS")) msd_cs_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_TILE_CONTIG")) tile_contig_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_DENSE_BITS")) dense_bits_ = static_cast<uint32_t>(std::atoi(g));
@@ -151,6 +152,50 @@ void Engine::mark(const char* name, cudaStream_t s) {
     cudaEventCreate(&e);
     cudaEventRecord(e, s);
     marks_.push_back({name, e, std::chrono::steady_clock::now()});
+}
+
+// RTK_ROWS_TRACE: per-phase end times of every k_rows_fused CTA (ns after the earliest CTA
+// start): percentiles over CTAs, and the spread of CTA finish times by SM load.
+void Engine::report_rows_trace(size_t nrows, cudaStream_t s) {
+    std::vector<unsigned long long> t(nrows * 16);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(t.data(), trace_.p, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, tend = 0;
+    int nph = 0;
+    for (size_t b = 0; b < nrows; ++b) {
+        t0 = std::min(t0, t[b * 16]);
+        int n = 0;
+        while (n < 15 && t[b * 16 + n]) ++n;
+        nph = std::max(nph, n);
+        tend = std::max(tend, t[b * 16 + n - 1]);
+    }
+    std::fprintf(stderr, "[rtk rows trace] rows=%zu span=%.1fus phase end (us after first start) p0/p50/p100:", nrows,
+                 (tend - t0) * 1e-3);
+    for (int ph = 0; ph < nph; ++ph) {
+        std::vector<double> v;
+        for (size_t b = 0; b < nrows; ++b)
+            if (t[b * 16 + ph]) v.push_back((t[b * 16 + ph] - t0) * 1e-3);
+        std::sort(v.begin(), v.end());
+        if (v.empty()) continue;
+        std::fprintf(stderr, " [%d] %.1f/%.1f/%.1f", ph, v.front(), v[v.size() / 2], v.back());
+    }
+    std::vector<int> per_sm(1024, 0);
+    for (size_t b = 0; b < nrows; ++b) ++per_sm[t[b * 16 + 15] & 1023];
+    // phase durations by how many rows share the SM
+    for (int load = 1; load <= 4; ++load) {
+        double dur[15] = {0};
+        int cnt = 0;
+        for (size_t b = 0; b < nrows; ++b) {
+            if (per_sm[t[b * 16 + 15] & 1023] != load) continue;
+            ++cnt;
+            for (int ph = 1; ph < nph; ++ph)
+                if (t[b * 16 + ph]) dur[ph] += (t[b * 16 + ph] - t[b * 16 + ph - 1]) * 1e-3;
+        }
+        if (!cnt) continue;
+        std::fprintf(stderr, "\n  rows on SMs with %d rows: %d, mean phase us:", load, cnt);
+        for (int ph = 1; ph < nph; ++ph) std::fprintf(stderr, " %.1f", dur[ph] / cnt);
+    }
+    std::fprintf(stderr, "\n");
 }
 
 void Engine::report_marks() {
@@ -257,6 +302,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
     if (gen0 != last_gen_) needs_init_ = true;  // buffers reallocated: counters are garbage
     if (usable && graph_.valid && graph_.gen == gen0 && graph_.key == key) {
         // replay: restore the plan bytes the captured upload reads, launch, finish on the host
+        if (call_start_) check(cudaEventRecord(call_start_, s), "event");
         if (arena_tag_ != graph_.arena_tag) {  // another call reused the arena: re-upload the plan
             if (!graph_.pinned.empty()) std::memcpy(pin_, graph_.pinned.data(), graph_.pinned.size());
             for (const auto& u : graph_.uploads)
@@ -278,6 +324,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         clean_rows_ = graph_.clean_rows;
         check(cudaEventRecord(ev_[0], s), "event");
         check(cudaGraphLaunch(graph_.exec, s), "graph launch");
+        if (call_end_) check(cudaEventRecord(call_end_, s), "event");
         check(cudaEventRecord(ev_[3], s), "event");
         expected_seq_ += graph_.seq_incr;
         sig_pending_ = graph_.seq_incr > 0;
@@ -313,6 +360,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         ok = cudaStreamEndCapture(cap_s_, &graph) == cudaSuccess && ok;
         cudaGraphExec_t exec = nullptr;
         ok = ok && g_buf_gen.load() == gen0 && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+        if (graph && std::getenv("RTK_GRAPH_DUMP")) cudaGraphDebugDotPrint(graph, std::getenv("RTK_GRAPH_DUMP"), 0);
         if (graph) cudaGraphDestroy(graph);
         cudaGetLastError();
         if (!ok) {
@@ -340,11 +388,15 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         graph_.clean_rows = clean_rows_;
         graph_.valid = true;
         check(cudaEventRecord(ev_[0], s), "event");
+        if (call_start_) check(cudaEventRecord(call_start_, s), "event");
         check(cudaGraphLaunch(exec, s), "graph launch");
+        if (call_end_) check(cudaEventRecord(call_end_, s), "event");
         check(cudaEventRecord(ev_[3], s), "event");
     } else {
         cudaGetLastError();
+        if (call_start_) check(cudaEventRecord(call_start_, s), "event");
         enqueue(d_base, dtype, smallest, scaled, a_s, gather, rows, d_vals, d_idx, d_pivots, s, c);
+        if (call_end_) check(cudaEventRecord(call_end_, s), "event");
     }
     last_key_ = std::move(key);
     have_last_ = true;
@@ -577,8 +629,15 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
                 clean_rows_ = R;
             }
         }
-        launch_rows_fused(static_cast<int>(frow[v].size()), fa, v == 1, s);
+        const size_t nfr = frow[v].size();
+        if (rows_trace_) {
+            trace_.ensure(nfr * 16 * sizeof(unsigned long long));
+            cudaMemsetAsync(trace_.p, 0, nfr * 16 * sizeof(unsigned long long), s);
+            fa.trace = trace_.as<unsigned long long>();
+        }
+        launch_rows_fused(static_cast<int>(nfr), fa, v == 1, s);
         ++stats.kernel_launches;
+        if (rows_trace_) report_rows_trace(nfr, s);
         if (fa.tail.hflags) {
             ++expected_seq_;
             sig_pending_ = true;
@@ -620,6 +679,8 @@ void Engine::complete(const uint32_t* d_base, const std::vector<RowReq>& rows, C
     const bool cleaned = clean_rows_ >= R && sig_pending_;
     needs_init_ = true;
     drain(c, ctl);
+    // host-driven rare paths enqueue more device work: the call's end moves behind it
+    const bool extra = (first_flags_ & (kFlagMore | kFlagFail)) != 0;
     // first_flags_: the flag word as the main path left it (drain's deeper levels clear kFlagMore)
     if (cleaned && (first_flags_ & (kFlagFail | kFlagMore | kFlagOverflow)) == 0) {
         needs_init_ = false;
@@ -640,7 +701,10 @@ void Engine::complete(const uint32_t* d_base, const std::vector<RowReq>& rows, C
         drain(c, ctl);
         if (ctl[0] & kFlagFail) throw Error{RTK_INVARIANT_VIOLATION, "filter: pivot inconsistent after exact path"};
         record(3, s);
+        if (call_end_) check(cudaEventRecord(call_end_, s), "event");
         sync(s, "finish");
+    } else if (extra && call_end_) {
+        check(cudaEventRecord(call_end_, s), "event");
     }
     if (count_stats_)
         for (int r = 0; r < R; ++r) stats.candidates += hcount_[r];

@@ -76,6 +76,9 @@ public:
     // stats of the last call; total_ms is resolved lazily (waits for the call's last event)
     const rtk_stats& last_stats();
     void set_timing(bool on) { timing_ = on; }
+    // bench: events recorded on the call's stream right before its first and after its last
+    // device operation (host planning and the completion wait stay outside); null = off
+    void set_call_events(cudaEvent_t start, cudaEvent_t end) { call_start_ = start; call_end_ = end; }
 
     int device() const { return device_; }
     rtk_stats stats{};
@@ -97,6 +100,7 @@ private:
     void sync(cudaStream_t s, const char* what);
     void release_retired();
     void mark(const char* name, cudaStream_t s);
+    void report_rows_trace(size_t nrows, cudaStream_t s);
     void report_marks();
     struct Mark {
         const char* name;
@@ -202,6 +206,7 @@ private:
     bool self_clean_ok_ = true;   // RTK_SELFCLEAN=0 disables
     bool force_init_ = false;
     bool no_graph_events_ = true;   // no stats events inside graphs (RTK_GRAPH_EVENTS=1 keeps them)
+    cudaEvent_t call_start_ = nullptr, call_end_ = nullptr;
     bool timing_ = false;           // rtk_set_timing: no graph replay, events around k_compact
     bool no_fused_ = false;
     bool no_dense_ = false;
@@ -210,6 +215,8 @@ private:
     int tile_contig_ = -1;          // RTK_TILE_CONTIG: force k_compact's tile order (-1: by row count)
     int msd_cs_ = 0;                // RTK_MSD_CS: force the level-0 MSD cluster size
     int rows_pf_ = 0;               // L2 prefetch distance of the per-row ring (RTK_ROWS_PF)
+    bool rows_trace_ = false;       // per-CTA phase timestamps of k_rows_fused (RTK_ROWS_TRACE)
+    DevBuf trace_;
     int prefetch_mb_ = 24;          // L2 prefetch budget of k_compact (RTK_PREFETCH_MB)
     int clean_rows_ = 0;
     int clean_upto_ = 0;          // rows whose counters the last call left clean

@@ -94,6 +94,7 @@ struct RowsFusedArgs {    // K6 fast path: one CTA per short row (rtk_rows.cu)
     unsigned long long* dbg;      // optional phase timestamps (RTK_PROFILE)
     CallTail tail;                // set when this is the call's last kernel
     uint32_t pf;                  // L2 prefetch distance of the streaming ring (chunks ahead)
+    unsigned long long* trace;    // optional per-CTA phase timestamps [grid][16] (RTK_ROWS_TRACE)
 };
 
 struct SortGroup {

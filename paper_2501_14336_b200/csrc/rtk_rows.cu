@@ -224,13 +224,20 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     };
     unsigned long long* dbg = a.dbg;
     int ndbg = 0;
+    int ntr = 0;
     auto stamp = [&]() {
-        if (dbg && blockIdx.x == 0 && threadIdx.x == 0 && ndbg < 30) {
+        if ((dbg && blockIdx.x == 0 || a.trace) && threadIdx.x == 0 && ndbg < 30) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-            dbg[ndbg++] = t;
+            if (dbg && blockIdx.x == 0) dbg[ndbg++] = t;
+            if (a.trace && ntr < 15) a.trace[blockIdx.x * 16ull + ntr++] = t;
         }
     };
+    if (a.trace && threadIdx.x == 0) {
+        uint32_t sm;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+        a.trace[blockIdx.x * 16ull + 15] = sm;
+    }
     stamp();
 
     // ---- streaming ring: TMA 1-D bulk copies (cp.async.bulk) of 8 KB chunks into a 4-stage
@@ -286,6 +293,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     if (tid == 0) s_m = 0;
     __syncthreads();
     stamp();
+    const uint32_t Thi = static_cast<uint32_t>(T >> 32);
 
     // ---- 2. one streaming read of the row --------------------------------------------------
     auto append = [&](uint32_t mask, const uint32_t* keys, uint32_t (*idx_of)(uint32_t, const void*),
@@ -366,13 +374,21 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
                     }
                 }
             }
+            // 32-bit pre-filter (key >= T.hi: a superset of K >= T, one compare per element);
+            // the exact composite mask only for warps where some element passes it
+            bool maybe = false;
+#pragma unroll
+            for (int e = 0; e < 4 * UU; ++e) {
+                key[e] = key_of<KM>(key[e], a.in);
+                maybe |= key[e] >= Thi;
+            }
+            if (!__any_sync(full, maybe)) continue;
             uint32_t mask = 0;
 #pragma unroll
             for (int u = 0; u < UU; ++u) {
                 const uint32_t nb = ~(head + static_cast<uint32_t>(c * kChunk + (g * UU + u) * 2048) + tid * 4);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    key[4 * u + i] = key_of<KM>(key[4 * u + i], a.in);
                     const unsigned long long K = (static_cast<unsigned long long>(key[4 * u + i]) << 32) | (nb - i);
                     mask |= static_cast<uint32_t>(K >= T) << (4 * u + i);
                 }
