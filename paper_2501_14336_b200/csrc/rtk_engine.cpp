@@ -83,6 +83,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_NO_FUSED")) no_fused_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_NO_DENSE")) no_dense_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_SPARSE_MAX")) sparse_max_ = std::atoi(g);
+    if (const char* g = std::getenv("RTK_SPARSE_SEL")) sparse_sel_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_ROWS_PF")) rows_pf_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_ROWS_TRACE")) rows_trace_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_MSD_CS")) msd_cs_ = std::atoi(g);
@@ -785,6 +786,7 @@ PlanArgs Engine::plan_args(const Call& c, const FinishPrep& f) {
     pa.max_bits = static_cast<uint32_t>(msd_max_bits_);
     pa.prefetch_mb = static_cast<uint32_t>(prefetch_mb_);
     pa.sparse_max = static_cast<uint32_t>(sparse_max_);
+    pa.sparse_sel = static_cast<uint32_t>(sparse_sel_);
     return pa;
 }
 

@@ -211,6 +211,7 @@ private:
     bool no_fused_ = false;
     bool no_dense_ = false;
     int sparse_max_ = 96;            // RTK_SPARSE_MAX (k_compact sparse-hit path threshold)
+    int sparse_sel_ = 1;             // RTK_SPARSE_SEL (sparse hits from registers, no L2 re-read)
     uint32_t dense_bits_ = 0;       // RTK_DENSE_BITS: level-0 digit of dense rows (0: fine_bits)         // RTK_NO_DENSE=1: dense rows are compacted too         // RTK_NO_FUSED=1: short rows take the general path too
     int tile_contig_ = -1;          // RTK_TILE_CONTIG: force k_compact's tile order (-1: by row count)
     int msd_cs_ = 0;                // RTK_MSD_CS: force the level-0 MSD cluster size

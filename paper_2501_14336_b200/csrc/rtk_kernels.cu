@@ -518,6 +518,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
     const uint64_t t_begin = pa.contig ? blockIdx.x * per : blockIdx.x;
     const uint64_t t_end = pa.contig ? min(ntiles, t_begin + per) : ntiles;
     const uint64_t t_step = pa.contig ? 1 : gridDim.x;
+    uint32_t v[kUnroll][kVec];
+    auto load_tile = [&](uint64_t tt) {
+        const uint64_t sp = (tt - tile0) * kTile;
+        const uint32_t lo = sp >= lead ? 0u : static_cast<uint32_t>(lead - sp);
+        const uint32_t hi = static_cast<uint32_t>(len + lead - sp < kTile ? len + lead - sp : kTile);
+        if constexpr (km_is16<KM>())
+            load_tile_local16(reinterpret_cast<const unsigned short*>(in.base) + off - lead + sp, lo, hi, v);
+        else
+            load_tile_local(in.base + off - lead + sp, lo, hi, v);
+    };
     for (uint64_t t = t_begin; t < t_end; t += t_step) {
         if (t >= tile1 || cur < 0) {
             if (cur >= 0) finish_row();
@@ -544,11 +554,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         const uint32_t vlo = span0 >= lead ? 0u : static_cast<uint32_t>(lead - span0);
         const uint32_t vhi = static_cast<uint32_t>(span_len - span0 < kTile ? span_len - span0 : kTile);
         const uint32_t idx0 = static_cast<uint32_t>(span0 - lead);  // low 32 bits of the row index
-        uint32_t v[kUnroll][kVec];
-        if constexpr (km_is16<KM>())
-            load_tile_local16(reinterpret_cast<const unsigned short*>(in.base) + off - lead + span0, vlo, vhi, v);
-        else
-            load_tile_local(in.base + off - lead + span0, vlo, vhi, v);
+        load_tile(t);
 
         // pass 1: key transform + per-thread hit mask (bit u*8+i)
         uint32_t mask = 0;
@@ -601,6 +607,26 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
             const uint64_t tp = off - lead + span0;  // element offset of the tile
             uint32_t o = wcur + incl - c;
             uint32_t m = mask;
+            if (pa.sparse_sel) {
+                // the hit's key from registers through a 31-SEL tree (static register indices;
+                // no L2 re-read stalling the warp before its next tile's loads)
+                while (m) {
+                    const uint32_t b = __ffs(m) - 1;
+                    m &= m - 1;
+                    uint32_t t[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) t[j] = (b & 1) ? v[(2 * j + 1) >> 3][(2 * j + 1) & 7] : v[(2 * j) >> 3][(2 * j) & 7];
+#pragma unroll
+                    for (int w = 8; w >= 1; w >>= 1) {
+                        const uint32_t bit = 16u / w;  // 2, 4, 8, 16
+#pragma unroll
+                        for (int j = 0; j < w; ++j) t[j] = (b & bit) ? t[2 * j + 1] : t[2 * j];
+                    }
+                    const uint32_t l = ((b >> 3) * kThreads + threadIdx.x) * kVec + (b & 7);
+                    stage[o++] = (static_cast<unsigned long long>(t[0]) << 32) | (nidx0 - l);
+                }
+                m = 0;
+            }
             while (m) {
                 const uint32_t b = __ffs(m) - 1;
                 m &= m - 1;

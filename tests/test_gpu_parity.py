@@ -6,6 +6,8 @@ generators (datagen.hpp:71-141) through oracle/_ref; expected outputs from rtk::
 rtk::batch_topk / rtk::scaled_topk compiled from the reference headers (oracle/_ref) — the
 configurations follow the reference tests cited on each case.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -14,6 +16,7 @@ import oracle as O
 pytestmark = pytest.mark.gpu
 
 UNIFORM, NORMAL, ZIPF, PEAKED = 0, 1, 2, 3
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _rtk():
@@ -470,3 +473,12 @@ def test_topk_sample_errors(cuda):
         rtk.topk_sample(x, 5, temperature=0.0)
     with pytest.raises(IndexError):
         rtk.topk_sample(x, 101)
+
+
+@pytest.mark.parametrize("k", [256, 1])
+def test_c2_full_size_small_k(cuda, k):
+    # BASELINE C2 at full size, n = 2^28 U[0,1), small k (C2's k = 2^8 and the extreme k = 1),
+    # bit-exact against the reference engine compiled in place (oracle/_ref)
+    x = O.ref_generate(UNIFORM, 1 << 28, 1)
+    assert_same(gpu_topk(x, k, 0, cuda), O.ref_topk(x, k, 0, grid=8), f"C2 k={k}")
+
