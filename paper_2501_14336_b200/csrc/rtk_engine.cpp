@@ -84,6 +84,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_NO_DENSE")) no_dense_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_SPARSE_MAX")) sparse_max_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_SPARSE_SEL")) sparse_sel_ = std::atoi(g);
+    if (const char* g = std::getenv("RTK_LSD")) lsd_mode_ = std::strcmp(g, "all") == 0 ? 2 : std::strcmp(g, "off") == 0 ? 0 : 1;
     if (const char* g = std::getenv("RTK_ROWS_PF")) rows_pf_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_ROWS_TRACE")) rows_trace_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_MSD_CS")) msd_cs_ = std::atoi(g);
@@ -550,8 +551,27 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
         dslots.push_back(sl);
     }
     if (!dense) dslots.clear();
+    // dense rows of >= 2 tiles each: the segmented one-sweep LSD sort (rtk_lsd.cu)
+    // (16-bit keys by default: 2 passes; RTK_LSD=all also for 32-bit keys, RTK_LSD=off never)
+    const bool lsd = dense && (lsd_mode_ == 2 || (lsd_mode_ == 1 && dtype == kF16));
+    std::vector<uint64_t> l_tile{0}, l_len, l_in, l_buf, l_k, l_out;
+    uint64_t l_total = 0;
+    if (lsd) {
+        for (uint32_t r : grow) {
+            const RowReq& q = rows[r];
+            l_tile.push_back(l_tile.back() + ceil_div(q.n, lsd_tile()));
+            l_len.push_back(q.n);
+            l_in.push_back(q.in_off);
+            l_buf.push_back(l_total);
+            l_total += (q.n + 3) & ~uint64_t(3);
+            l_k.push_back(q.k);
+            l_out.push_back(q.out_off);
+        }
+    }
     Plan P;
     const size_t o_dslots = P.add(dslots);
+    const size_t o_ltile = P.add(l_tile), o_llen = P.add(l_len), o_lin = P.add(l_in), o_lbuf = P.add(l_buf),
+                 o_lk = P.add(l_k), o_lout = P.add(l_out);
     const size_t o_rid = P.add(rid), o_off = P.add(off), o_len = P.add(len), o_lead = P.add(lead),
                  o_tile = P.add(tile_start), o_coff = P.add(cand_off), o_cap = P.add(cap),
                  o_k = P.add(row_k), o_out = P.add(row_out), o_in = P.add(row_in),
@@ -646,7 +666,58 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
         mark("rows_fused", s);
     }
     record(1, s);
-    if (!grow.empty() && dense) {
+    if (!grow.empty() && lsd) {
+        record(2, s);
+        mark("compact(skipped: dense rows)", s);
+        const int NR = static_cast<int>(grow.size());
+        const uint64_t tiles = l_tile.back();
+        lsd_a_.ensure(8 * std::max<uint64_t>(l_total, 1));
+        lsd_b_.ensure(8 * std::max<uint64_t>(l_total, 1));
+        // look-back words carry a device epoch (ctr[4]); both are zeroed together whenever either
+        // buffer is (re)allocated, so a stale word can never match a later call's epoch
+        if (lsd_status_.cap < 8 * 256 * tiles || lsd_hist_cap_ < static_cast<size_t>(NR)) {
+            lsd_status_.ensure(std::max<size_t>(lsd_status_.cap, 8 * 256 * tiles));
+            lsd_hist_cap_ = std::max<size_t>(lsd_hist_cap_, NR);
+            lsd_meta_.ensure(4ull * (1024ull * lsd_hist_cap_ + 8));
+            check(cudaMemsetAsync(lsd_status_.p, 0, lsd_status_.cap, s), "memset");
+            check(cudaMemsetAsync(lsd_meta_.p, 0, 4ull * (1024ull * lsd_hist_cap_ + 8), s), "memset");
+        }
+        uint32_t* hist = lsd_meta_.as<uint32_t>();
+        uint32_t* ctr = hist + 1024ull * lsd_hist_cap_;
+        check(cudaMemsetAsync(hist, 0, 4ull * 1024 * NR, s), "memset");
+        check(cudaMemsetAsync(ctr, 0, 16, s), "memset");  // tile counters; ctr[4] (epoch) persists
+        LsdArgs la{};
+        la.R = NR;
+        la.tile_start = at<uint64_t>(D, o_ltile);
+        la.len = at<uint64_t>(D, o_llen);
+        la.in_off = at<uint64_t>(D, o_lin);
+        la.buf_off = at<uint64_t>(D, o_lbuf);
+        la.k = at<uint64_t>(D, o_lk);
+        la.out_off = at<uint64_t>(D, o_lout);
+        la.rid = at<uint32_t>(D, o_grow);
+        la.hist = hist;
+        la.status = lsd_status_.as<unsigned long long>();
+        la.ctr = ctr;
+        la.src = lsd_b_.as<unsigned long long>();
+        la.dst = lsd_a_.as<unsigned long long>();
+        la.in = src;
+        la.out_vals = d_vals;
+        la.out_idx = d_idx;
+        la.pivots = d_pivots;
+        la.npass = dtype == kF16 ? 2u : 4u;
+        la.shift0 = dtype == kF16 ? 16u : 0u;
+        la.tail = tail_args();
+        if (self_clean_) {
+            set_clean(la.tail, R);
+            clean_rows_ = R;
+        }
+        launch_lsd(tiles, la, s);
+        check(cudaGetLastError(), "lsd launch");
+        stats.kernel_launches += 1 + la.npass;
+        ++expected_seq_;
+        sig_pending_ = true;
+        mark("lsd sort", s);
+    } else if (!grow.empty() && dense) {
         FinishPrep fp = prepare_finish(c, grow);
         fp.slots = at<SegSlot>(D, o_dslots);
         record(2, s);

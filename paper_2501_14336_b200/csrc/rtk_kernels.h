@@ -276,6 +276,30 @@ void launch_pivots(int R, const uint64_t* row_out_off, const uint64_t* row_k, co
                    uint32_t* pivots, cudaStream_t s);
 void launch_first_digit_hist(uint64_t tiles, const Rows& rows, const InputSrc& in, unsigned int d,
                              unsigned long long* ghist, cudaStream_t s);
+struct LsdArgs {  // dense rows: segmented one-sweep LSD radix sort (rtk_lsd.cu)
+    int R;                        // rows of this launch
+    const uint64_t* tile_start;   // [R + 1] 4096-element tiles per row, prefix
+    const uint64_t* len;          // elements per row
+    const uint64_t* in_off;       // row start in the input (elements)
+    const uint64_t* buf_off;      // row start in the ping-pong buffers
+    const uint64_t* k;
+    const uint64_t* out_off;
+    const uint32_t* rid;          // state row (pivots)
+    uint32_t* hist;               // [R][4][256] digit counts (zeroed per call)
+    unsigned long long* status;   // [tiles][256] look-back words (epoch-tagged, never reset)
+    uint32_t* ctr;                // [0..3] tile counters (zeroed per call), [4] epoch
+    unsigned long long* src;      // pass p > 0 input (swapped per pass by the launcher)
+    unsigned long long* dst;
+    InputSrc in;
+    uint32_t* out_vals;
+    uint64_t* out_idx;
+    uint32_t* pivots;
+    CallTail tail;                // last pass only
+    uint32_t npass;               // 4 (32-bit keys) or 2 (16-bit keys: low half constant)
+    uint32_t shift0;              // 0 or 16
+};
+uint32_t lsd_tile();
+void launch_lsd(uint64_t tiles, const LsdArgs& a, cudaStream_t s);
 void launch_rows_fused(int R, const RowsFusedArgs& a, bool small, cudaStream_t s);
 uint32_t rows_fused_kmax(bool small);
 uint32_t rows_fused_cand(bool small);

@@ -482,3 +482,42 @@ def test_c2_full_size_small_k(cuda, k):
     x = O.ref_generate(UNIFORM, 1 << 28, 1)
     assert_same(gpu_topk(x, k, 0, cuda), O.ref_topk(x, k, 0, grid=8), f"C2 k={k}")
 
+
+
+@pytest.mark.parametrize("mode", ["all", "off"])
+def test_dense_rows_lsd_forced(cuda, mode):
+    # dense rows (k >= n/2): the segmented one-sweep LSD sort is forced for 32-bit keys too
+    # (RTK_LSD=all) or disabled (off) in a fresh process; both must equal the reference per row,
+    # ragged rows, both orders, u32 ties and heavy f32 ties included
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle as O, paper_2501_14336_b200 as rtk
+rng = np.random.default_rng(3)
+lens = [5000, 4096, 12289, 70001]
+offs = [0]
+for n in lens[:-1]: offs.append(offs[-1] + n + 3)
+data = rng.standard_normal(offs[-1] + lens[-1]).astype(np.float32)
+data[offs[2]:offs[2] + lens[2]:3] = 0.5
+ks = [5000, 2048, 12289, 40000]
+for order in (0, 1):
+    b = rtk.BatchInput(torch.from_numpy(data).cuda(), offs, lens, ks)
+    got = rtk.batch_topk(b, rtk.SelectionOrder(order))
+    for t in range(4):
+        x = data[offs[t]:offs[t] + lens[t]]
+        wv, wi, _ = O.port_topk(x, ks[t], order)
+        assert np.array_equal(got[t].values.cpu().numpy().view(np.uint32), wv.view(np.uint32)), (order, t)
+        assert np.array_equal(got[t].indices.cpu().numpy().astype(np.uint64), wi), (order, t)
+u = rng.integers(0, 50, 3 * 9000, dtype=np.uint32)
+b = rtk.BatchInput(torch.from_numpy(u.view(np.int32)).cuda().view(torch.uint32), [0, 9000, 18000], [9000] * 3, [9000, 6000, 4500])
+got = rtk.batch_topk(b)
+for t in range(3):
+    wv, wi, _ = O.port_topk(u[9000 * t:9000 * (t + 1)], [9000, 6000, 4500][t], 0)
+    assert np.array_equal(got[t].indices.cpu().numpy().astype(np.uint64), wi), ("u32", t)
+print("ok")
+''' % ROOT
+    env = dict(os.environ, RTK_LSD=mode)
+    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr

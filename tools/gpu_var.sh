@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+cp paper_2501_14336_b200/librtk_b200.so /tmp/lib_cur.so
+for v in ${VARS:-A B C D}; do
+  cp paper_2501_14336_b200/build/var/lib_$v.so paper_2501_14336_b200/librtk_b200.so
+  echo "== $v"; KS=${KS:-128256} DT=${DT:-f32,bf16} timeout 300 python tools/c3_ab.py ""
+done > gpurun_out/var.log 2>&1
+cp /tmp/lib_cur.so paper_2501_14336_b200/librtk_b200.so
+cat gpurun_out/var.log

@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    --log-file gpurun_out/prof_launches.csv python tools/prof_topk.py 28 1048576 3 > /dev/null 2>&1; echo "launches rc=$?"
+    --log-file gpurun_out/prof_launches.csv env RTK_MSD_Q=1 python tools/prof_topk.py 28 1048576 3 > /dev/null 2>&1; echo "launches rc=$?"
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/prof_batch_launches.csv python -c "
 import torch, paper_2501_14336_b200 as rtk
@@ -30,7 +30,7 @@ MODE=2 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_wri
 ncu --set full --clock-control none --import-source on -k regex:"k_compact" -s 2 -c 1 \
     -o gpurun_out/prof_compact -f python tools/prof_topk.py 28 1048576 3 > gpurun_out/prof_compact.log 2>&1; echo "compact rc=$?"
 ncu --set full --clock-control none --import-source on -k regex:"k_msd_cluster|k_sort_groups|k_sample_select" -s 3 -c 3 \
-    -o gpurun_out/prof_finish -f python tools/prof_topk.py 28 1048576 3 > gpurun_out/prof_finish.log 2>&1; echo "finish rc=$?"
+    -o gpurun_out/prof_finish -f env RTK_MSD_Q=1 python tools/prof_topk.py 28 1048576 3 > gpurun_out/prof_finish.log 2>&1; echo "finish rc=$?"
 ncu --set full --clock-control none --import-source on -k regex:"k_rows_fused" -s 1 -c 2 \
     -o gpurun_out/prof_rows -f python -c "
 import torch, paper_2501_14336_b200 as rtk
