@@ -114,6 +114,9 @@ __global__ void __launch_bounds__(kLsdHistThreads) k_lsd_hist(LsdArgs a, uint32_
 }
 
 // ---- k_lsd_pass -----------------------------------------------------------------------------
+// SH: the digit's shift in the sort key (compile-time: one byte extract per item); FIRST:
+// pass 0 (reads the input); LAST: writes the output
+template <int SH, bool FIRST, bool LAST>
 __global__ void __launch_bounds__(kLsdThreads, 3) k_lsd_pass(LsdArgs a, uint32_t pass) {
     __shared__ unsigned long long s_tile[kLsdTile];
     __shared__ uint32_t s_cnt[kLsdWarps][256];
@@ -135,12 +138,13 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_lsd_pass(LsdArgs a, uint32_t
     const uint64_t e0 = (t - t0) * kLsdTile;
     const uint32_t cnt = static_cast<uint32_t>(n - e0 < kLsdTile ? n - e0 : kLsdTile);
     const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(a.ctr + 4) * 4u + pass + 1u;
-    const uint32_t sh = a.shift0 + 8 * pass;
-    const bool last = pass + 1 == a.npass;
+    const uint32_t hrow = __ldcg(a.hist + j * 1024 + pass * 256 + tid);  // consumed after the look-back
+    const bool full_tile = cnt == kLsdTile;
+    auto digit = [](unsigned long long K) { return (static_cast<uint32_t>(K >> 32) >> SH) & 255u; };
 
     // load: warp w owns tile elements [512w, 512w + 512), round i covers 32 consecutive ones
     unsigned long long c[kLsdItems];
-    if (pass == 0) {
+    if (FIRST) {
         uint32_t raw[kLsdItems];
 #pragma unroll
         for (int i = 0; i < kLsdItems; ++i) {
@@ -167,9 +171,10 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_lsd_pass(LsdArgs a, uint32_t
     for (int i = 0; i < kLsdItems; ++i) {
         const uint32_t e = warp * (kLsdItems * 32) + i * 32 + lane;
         const bool valid = e < cnt;
-        const uint32_t d = static_cast<uint32_t>(c[i] >> (32 + sh)) & 255u;
+        const uint32_t d = digit(c[i]);
         // ballot multisplit (8 ballots) measured faster here than __match_any_sync
-        const unsigned peers = warp_peers8(d) & __ballot_sync(full, valid);
+        unsigned peers = warp_peers8(d);
+        if (!full_tile) peers &= __ballot_sync(full, valid);
         const uint32_t b0 = s_cnt[warp][d];
         rk[i] = b0 + __popc(peers & lt);
         __syncwarp();
@@ -219,7 +224,7 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_lsd_pass(LsdArgs a, uint32_t
         __stcg(st, ep | kLsdPrefix | (excl + tc));
     }
     uint32_t tot;
-    const uint32_t rowbase = lsd_block_scan(a.hist[j * 1024 + pass * 256 + d], s_w, &tot);
+    const uint32_t rowbase = lsd_block_scan(hrow, s_w, &tot);
     const uint32_t dstart = lsd_block_scan(tc, s_w, &tot);
     s_dstart[d] = dstart;
     s_gbase[d] = rowbase + excl;
@@ -229,24 +234,24 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_lsd_pass(LsdArgs a, uint32_t
     for (int i = 0; i < kLsdItems; ++i) {
         const uint32_t e = warp * (kLsdItems * 32) + i * 32 + lane;
         if (e < cnt) {
-            const uint32_t dd = static_cast<uint32_t>(c[i] >> (32 + sh)) & 255u;
+            const uint32_t dd = digit(c[i]);
             s_tile[s_dstart[dd] + s_cnt[warp][dd] + rk[i]] = c[i];
         }
     }
     __syncthreads();
     // coalesced runs: tile-sorted position q -> row position gbase[d] + (q - dstart[d])
-    if (!last) {
+    if (!LAST) {
         unsigned long long* dst = a.dst + a.buf_off[j];
         for (uint32_t q = tid; q < cnt; q += kLsdThreads) {
             const unsigned long long K = s_tile[q];
-            const uint32_t dd = static_cast<uint32_t>(K >> (32 + sh)) & 255u;
+            const uint32_t dd = digit(K);
             __stcs(dst + s_gbase[dd] + (q - s_dstart[dd]), K);
         }
     } else {
         const uint64_t k = a.k[j], oo = a.out_off[j];
         for (uint32_t q = tid; q < cnt; q += kLsdThreads) {
             const unsigned long long K = s_tile[q];
-            const uint32_t dd = static_cast<uint32_t>(K >> (32 + sh)) & 255u;
+            const uint32_t dd = digit(K);
             const uint64_t rank = s_gbase[dd] + (q - s_dstart[dd]);
             if (rank >= k) continue;
             const uint32_t kv = ~static_cast<uint32_t>(K >> 32);
@@ -272,7 +277,15 @@ void launch_lsd(uint64_t tiles, const LsdArgs& a, cudaStream_t s) {
         LsdArgs b = a;
         if (p % 2 == 1) std::swap(b.src, b.dst);  // pass p reads what pass p-1 wrote
         if (p + 1 < a.npass) b.tail = CallTail{};
-        k_lsd_pass<<<static_cast<unsigned>(tiles), kLsdThreads, 0, s>>>(b, p);
+        const dim3 g(static_cast<unsigned>(tiles));
+        const uint32_t sh = a.shift0 + 8 * p;
+        const bool first = p == 0, last = p + 1 == a.npass;
+        if (sh == 0) k_lsd_pass<0, true, false><<<g, kLsdThreads, 0, s>>>(b, p);
+        else if (sh == 8) k_lsd_pass<8, false, false><<<g, kLsdThreads, 0, s>>>(b, p);
+        else if (sh == 16 && first) k_lsd_pass<16, true, false><<<g, kLsdThreads, 0, s>>>(b, p);
+        else if (sh == 16) k_lsd_pass<16, false, false><<<g, kLsdThreads, 0, s>>>(b, p);
+        else if (last) k_lsd_pass<24, false, true><<<g, kLsdThreads, 0, s>>>(b, p);
+        else k_lsd_pass<24, false, false><<<g, kLsdThreads, 0, s>>>(b, p);
     }
 }
 
