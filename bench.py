@@ -367,9 +367,12 @@ def main():
                             "peak_kind": peak_kind, "kernel_ms": comp_ms,
                             "kernel_share_of_step": comp_ms / mean_ms},
                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-               "timing": "steps issued back-to-back from C through rtk_topk (rtk_bench_topk), CUDA events "
-                         "per step on the launching stream; python_loop_ms = the same call through the "
-                         "Python mirror (rtk.topk) with torch events, harness overhead included",
+               "timing": "steps issued back-to-back from C through rtk_topk (rtk_bench_topk); per step two "
+                         "CUDA events the engine records on the launching stream right before its first and "
+                         "after its last device operation of the call (host planning and the host's wait for "
+                         "the completion signal are outside; they are inside e2e and python_loop_ms); "
+                         "python_loop_ms = the same call through the Python mirror (rtk.topk) with torch "
+                         "events around the whole call",
                "python_loop_ms": py_ms,
                "k_sweep": sweep,
                "adversarial_c4": {"config": "n=2^26 Uniform[128.6,128.7) fp32, k=2^16, largest, scaled_topk "

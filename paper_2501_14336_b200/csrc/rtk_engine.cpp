@@ -84,6 +84,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_NO_DENSE")) no_dense_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_SPARSE_MAX")) sparse_max_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_SPARSE_SEL")) sparse_sel_ = std::atoi(g);
+    if (const char* g = std::getenv("RTK_DYN")) dyn_per_cta_ = std::max(0, std::atoi(g));
     if (const char* g = std::getenv("RTK_LSD")) lsd_mode_ = std::strcmp(g, "all") == 0 ? 2 : std::strcmp(g, "off") == 0 ? 0 : 1;
     if (const char* g = std::getenv("RTK_ROWS_PF")) rows_pf_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_ROWS_TRACE")) rows_trace_ = *g && *g != '0';
@@ -858,6 +859,8 @@ PlanArgs Engine::plan_args(const Call& c, const FinishPrep& f) {
     pa.prefetch_mb = static_cast<uint32_t>(prefetch_mb_);
     pa.sparse_max = static_cast<uint32_t>(sparse_max_);
     pa.sparse_sel = static_cast<uint32_t>(sparse_sel_);
+    pa.dyn_ctr = dyn_per_cta_ > 0 ? ctl_.as<uint32_t>() + 8 : nullptr;  // ctl[8..9]: zeroed by init / self-clean
+    pa.dyn_per_cta = static_cast<uint32_t>(dyn_per_cta_);
     return pa;
 }
 

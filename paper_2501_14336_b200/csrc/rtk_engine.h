@@ -214,7 +214,8 @@ private:
     int lsd_mode_ = 1;               // RTK_LSD: dense rows' LSD sort: 0 off, 1 16-bit keys, 2 all
     size_t lsd_hist_cap_ = 0;
     DevBuf lsd_a_, lsd_b_, lsd_status_, lsd_meta_;
-    int sparse_sel_ = 1;             // RTK_SPARSE_SEL (sparse hits from registers, no L2 re-read)
+    int sparse_sel_ = 1;
+    int dyn_per_cta_ = 12;            // RTK_DYN: k_compact dynamic-tail tiles per CTA (0: static split)             // RTK_SPARSE_SEL (sparse hits from registers, no L2 re-read)
     uint32_t dense_bits_ = 0;       // RTK_DENSE_BITS: level-0 digit of dense rows (0: fine_bits)         // RTK_NO_DENSE=1: dense rows are compacted too         // RTK_NO_FUSED=1: short rows take the general path too
     int tile_contig_ = -1;          // RTK_TILE_CONTIG: force k_compact's tile order (-1: by row count)
     int msd_cs_ = 0;                // RTK_MSD_CS: force the level-0 MSD cluster size

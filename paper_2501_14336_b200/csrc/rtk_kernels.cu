@@ -528,7 +528,24 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         else
             load_tile_local(in.base + off - lead + sp, lo, hi, v);
     };
-    for (uint64_t t = t_begin; t < t_end; t += t_step) {
+    // interleaved mode: the last `dyn` tiles are handed out from a counter, so CTAs that start
+    // late (PDL launch next to the sample kernel's cluster) do not leave a tail
+    __shared__ uint64_t s_next;
+    const uint64_t dyn_want = static_cast<uint64_t>(gridDim.x) * pa.dyn_per_cta;
+    const uint64_t dyn = (!pa.contig && pa.dyn_ctr) ? (dyn_want < ntiles ? dyn_want : ntiles) : 0;
+    const uint64_t ns = ntiles - dyn;
+    auto grab = [&]() -> uint64_t {  // block-collective
+        __syncthreads();
+        if (threadIdx.x == 0) s_next = ns + atomicAdd(pa.dyn_ctr, 1u);
+        __syncthreads();
+        return s_next;
+    };
+    auto next_tile = [&](uint64_t tt) -> uint64_t {
+        if (dyn == 0 || tt + t_step < ns) return tt + t_step;
+        return grab();
+    };
+    const uint64_t t_first = (dyn != 0 && t_begin >= ns) ? grab() : t_begin;
+    for (uint64_t t = t_first; t < t_end; t = next_tile(t)) {
         if (t >= tile1 || cur < 0) {
             if (cur >= 0) finish_row();
             const int j = row_of_tile(rows, t);
@@ -672,6 +689,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         }
     }
     if (cur >= 0) finish_row();
+    if (dyn) {  // the last CTA out resets the tile counters for the next launch
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(pa.dyn_ctr + 1, 1u) == gridDim.x - 1) {
+                pa.dyn_ctr[0] = 0;
+                pa.dyn_ctr[1] = 0;
+            }
+        }
+    }
 }
 
 // pivot[r] = values[k-1] of each row (engine.hpp:333 / scaling.hpp:76).
@@ -888,13 +915,16 @@ static void compact_km(uint64_t tiles, const Rows& rows, const InputSrc& in, con
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    // PDL off by default: early-launched compaction CTAs that cannot fit next to the sample
-    // kernel start late, and the static interleaved tile split then ends on a tail (measured
-    // +14 us at k = 256, no gain at k = 2^20, with or without the L2 prefetch prologue)
-    static const bool no_pdl = [] {
+    // PDL (RTK_PDL_COMPACT=1): compaction CTAs launch while the sample kernel runs (L2 prefetch
+    // prologue, then griddepcontrol.wait); those that cannot fit next to the sample's cluster
+    // start late. Off by default: with the static split it measured +14 us at k = 256 (tail);
+    // with the dynamic tail (pa.dyn_ctr, 12 tiles per CTA) it is neutral at k = 256 and +5 us at
+    // k = 2^20, while the dynamic tail alone gains 4 / 7 us (C2 k = 256 / 2^20).
+    static const bool env_off = [] {
         const char* e = std::getenv("RTK_PDL_COMPACT");
         return !(e && *e && *e != '0');
     }();
+    const bool no_pdl = env_off || pa.dyn_ctr == nullptr || pa.contig;
     cfg.numAttrs = no_pdl ? 0 : 1;
     cudaLaunchKernelEx(&cfg, k_compact<KM>, rows, in, T, cand, cand_off, cap, count, kmin, kmax, pa);
 }

@@ -206,6 +206,8 @@ struct PlanArgs {         // per-row plan after the compaction (fused into k_com
     uint32_t prefetch_mb;    // L2 prefetch budget of k_compact's prologue (RTK_PREFETCH_MB)
     uint32_t sparse_max;     // warp-tiles with <= this many hits take the set-bits (L2 re-read) path
     uint32_t sparse_sel;     // set-bits path takes the key from registers (select tree), no re-read
+    uint32_t* dyn_ctr;       // [2] dynamic-tail tile counter + CTAs done (self-resetting); null = static
+    uint32_t dyn_per_cta;    // dynamic-tail tiles per CTA of the grid
     uint32_t contig;         // 1: contiguous tile runs per CTA (many-row batches), 0: interleaved
 };
 
