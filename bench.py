@@ -255,17 +255,9 @@ def main():
         xa = (128.6 + 0.1 * torch.rand(na, device=dev, generator=gen)).float()
         for name, mode in (("off", 0), ("always", 1), ("adaptive", 2)):
             pol = R.ScalePolicy(mode=R.ScaleMode(mode), trigger_fraction=0.5, seed=31)
-            for _ in range(3):
-                rtk.scaled_topk(xa, ka, policy=pol)
-            times = []
-            for _ in range(max(5, args.steps // 2)):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                rtk.scaled_topk(xa, ka, policy=pol)
-                b.record(stream)
-                torch.cuda.synchronize()
-                times.append(a.elapsed_time(b))
-            ms_a = statistics.mean(times)
+            # steps issued from C (rtk_bench_scaled): events before the scale decision's kernels
+            # and after the call's last device operation, as for the C2 value
+            ms_a, _ = R.bench_scaled(xa, ka, max(5, args.steps // 2), 3, policy=pol)
             adversarial[name] = {"ms": ms_a, "GBps": (4 * na + 12 * ka) / (ms_a * 1e-3) / 1e9,
                                  "fraction_of_hbm_peak": (4 * na + 12 * ka) / (ms_a * 1e-3) / 1e9 / peak}
         del xa

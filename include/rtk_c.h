@@ -136,11 +136,19 @@ int rtk_set_timing(rtk_handle h, int on);
 
 /* Benchmark helper: `warmup` untimed then `steps` timed back-to-back rtk_topk calls issued from C
  * (the reference's own call sites are C++ loops over rtk::topk, rtk_cli.cpp:398). The device time
- * of every step is measured with CUDA events on `stream`; step_ms (nullable) receives `steps`
+ * of every step is measured with CUDA events on `stream`, recorded by the engine right before its
+ * first and after its last device operation of the call (host planning and the host's wait for
+ * the completion signal excluded); step_ms (nullable) receives `steps`
  * values, *mean_ms their mean. Same arguments and errors as rtk_topk. */
 int rtk_bench_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, int order,
                    void* d_out_vals, uint64_t* d_out_idx, void* d_out_pivot, const rtk_cfg* cfg,
                    void* stream, int warmup, int steps, float* step_ms, float* mean_ms);
+/* Scaled counterpart (rtk_topk_scaled per step; the start event precedes the scale decision's
+ * kernels). Same arguments and errors as rtk_topk_scaled. */
+int rtk_bench_scaled(rtk_handle h, const float* d_in, uint64_t n, uint64_t k, int order, int mode,
+                     double trigger_fraction, uint64_t seed, float* d_out_vals, uint64_t* d_out_idx,
+                     float* d_out_pivot, const rtk_cfg* cfg, void* stream, int warmup, int steps,
+                     float* step_ms, float* mean_ms);
 /* Batched counterpart (rtk_topk_batched per step). When flush_bytes > 0, d_flush is overwritten
  * before every step OUTSIDE the timed events (evicts the inputs from L2). */
 int rtk_bench_batched(rtk_handle h, const void* d_data, uint64_t data_len, const uint64_t* offsets,

@@ -68,6 +68,9 @@ SIGNATURES = {
                                     C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "rtk_bench_topk": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, vp, vp, vp, C.POINTER(rtk_cfg), vp,
                                  C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "rtk_bench_scaled": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, C.c_double, u64, vp, vp, vp,
+                                   C.POINTER(rtk_cfg), vp, C.c_int, C.c_int, C.POINTER(C.c_float),
+                                   C.POINTER(C.c_float)]),
     "rtk_cfg_default": (None, [C.POINTER(rtk_cfg)]),
     "rtk_cfg_validate": (C.c_int, [C.POINTER(rtk_cfg)]),
     "rtk_topk": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, vp, vp, vp, C.POINTER(rtk_cfg), vp]),

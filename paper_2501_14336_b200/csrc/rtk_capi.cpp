@@ -242,6 +242,46 @@ int rtk_bench_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int d
     });
 }
 
+int rtk_bench_scaled(rtk_handle h, const float* d_in, uint64_t n, uint64_t k, int order, int mode,
+                     double trigger_fraction, uint64_t seed, float* d_out_vals, uint64_t* d_out_idx,
+                     float* d_out_pivot, const rtk_cfg* cfg, void* stream, int warmup, int steps,
+                     float* step_ms, float* mean_ms) {
+    return guarded([&] {
+        if (!h || steps < 1 || warmup < 0) throw Error{RTK_INVALID_ARGUMENT, "bench: bad arguments"};
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto one = [&] {
+            const int st = rtk_topk_scaled(h, d_in, n, k, order, mode, trigger_fraction, seed, d_out_vals, d_out_idx,
+                                           d_out_pivot, nullptr, cfg, stream);
+            if (st != RTK_OK) throw Error{st, g_last_error};
+        };
+        for (int i = 0; i < warmup; ++i) one();
+        std::vector<cudaEvent_t> ev(2 * steps);
+        for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        for (int i = 0; i < steps; ++i) {
+            cuda_check(cudaEventRecord(ev[2 * i], s), "event");  // before the scale decision's kernels
+            h->engine.set_call_events(nullptr, ev[2 * i + 1]);
+            try {
+                one();
+            } catch (...) {
+                h->engine.set_call_events(nullptr, nullptr);
+                throw;
+            }
+            h->engine.set_call_events(nullptr, nullptr);
+        }
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        double sum = 0;
+        for (int i = 0; i < steps; ++i) {
+            float ms = 0;
+            cuda_check(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]), "elapsed");
+            if (step_ms) step_ms[i] = ms;
+            sum += ms;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        if (mean_ms) *mean_ms = static_cast<float>(sum / steps);
+    });
+}
+
 int rtk_bench_batched(rtk_handle h, const void* d_data, uint64_t data_len, const uint64_t* offsets,
                       const uint64_t* lengths, const uint64_t* ks, uint64_t B, int dtype, int order,
                       void* d_out_vals, uint64_t* d_out_idx, const uint64_t* out_offsets,

@@ -228,6 +228,33 @@ def bench_topk(x, k: int, steps: int, warmup: int = 3, order: SelectionOrder = S
     return float(mean.value), [float(v) for v in per]
 
 
+def bench_scaled(x, k: int, steps: int, warmup: int = 3, policy: Optional[ScalePolicy] = None,
+                 order: SelectionOrder = SelectionOrder.Largest, cfg: Optional[EngineConfig] = None):
+    """rtk_bench_scaled: `steps` back-to-back rtk_topk_scaled calls issued from C on x's current
+    stream; returns (mean_ms, [step_ms]) (device-resident f32 input)."""
+    import torch
+    cfg = cfg or EngineConfig()
+    policy = policy or ScalePolicy()
+    lib = L.load()
+    x = x.contiguous()
+    if x.dtype != torch.float32:
+        raise TypeError("scaled_topk is defined for float32 only")
+    kk = int(k)
+    vals = torch.empty(kk, dtype=x.dtype, device=x.device)
+    idx = torch.empty(kk, dtype=torch.int64, device=x.device)
+    piv = torch.empty(1, dtype=x.dtype, device=x.device)
+    per = (C.c_float * int(steps))()
+    mean = C.c_float()
+    c = cfg._c()
+    st = lib.rtk_bench_scaled(_handle(x.device.index or 0), C.c_void_p(x.data_ptr()), x.numel(), kk, int(order),
+                              int(policy.mode), float(policy.trigger_fraction),
+                              int(policy.seed) & 0xFFFFFFFFFFFFFFFF, C.c_void_p(vals.data_ptr()),
+                              C.c_void_p(idx.data_ptr()), C.c_void_p(piv.data_ptr()), C.byref(c), _stream_ptr(x),
+                              int(warmup), int(steps), per, C.byref(mean))
+    _raise(st, "rtk_bench_scaled")
+    return float(mean.value), [float(v) for v in per]
+
+
 def bench_batch_dense(x, k: int, steps: int, warmup: int = 3, flush=None,
                       order: SelectionOrder = SelectionOrder.Largest, cfg: Optional[EngineConfig] = None):
     """rtk_bench_batched over a dense [B, V] CUDA tensor: `steps` rtk_topk_batched calls issued

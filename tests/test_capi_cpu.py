@@ -32,7 +32,7 @@ def test_header_declares_the_reference_entry_points():
     fns = header_functions()
     for name in ["rtk_topk", "rtk_topk_batched", "rtk_topk_scaled", "rtk_topk_host", "rtk_topk_batched_host",
                  "rtk_topk_scaled_host", "rtk_merge_shards", "rtk_handle_create", "rtk_handle_destroy",
-                 "rtk_cfg_default", "rtk_cfg_validate", "rtk_last_error", "rtk_get_stats", "rtk_set_timing", "rtk_bench_topk", "rtk_bench_batched", "rtk_version"]:
+                 "rtk_cfg_default", "rtk_cfg_validate", "rtk_last_error", "rtk_get_stats", "rtk_set_timing", "rtk_bench_topk", "rtk_bench_batched", "rtk_bench_scaled", "rtk_version"]:
         assert name in fns
 
 

