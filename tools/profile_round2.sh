@@ -25,7 +25,7 @@ for m in (0, 1, 2):
     for i in range(2): rtk.scaled_topk(xa, 1 << 16, policy=pol)
 torch.cuda.synchronize()
 PY
-MODE=2 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+MODE=2 RTK_MSD_Q=1 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/prof_c4_launches.csv python /tmp/c4a.py > /dev/null 2>&1 || true
 ncu --set full --clock-control none --import-source on -k regex:"k_compact" -s 2 -c 1 \
     -o gpurun_out/prof_compact -f python tools/prof_topk.py 28 1048576 3 > gpurun_out/prof_compact.log 2>&1; echo "compact rc=$?"
