@@ -85,7 +85,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_SPARSE_MAX")) sparse_max_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_SPARSE_SEL")) sparse_sel_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_DYN")) dyn_per_cta_ = std::max(0, std::atoi(g));
-    if (const char* g = std::getenv("RTK_LSD")) lsd_mode_ = std::strcmp(g, "all") == 0 ? 2 : std::strcmp(g, "off") == 0 ? 0 : 1;
+    if (const char* g = std::getenv("RTK_LSD")) lsd_mode_ = std::strcmp(g, "16") == 0 ? 1 : std::strcmp(g, "off") == 0 ? 0 : 2;
     if (const char* g = std::getenv("RTK_ROWS_PF")) rows_pf_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_ROWS_TRACE")) rows_trace_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_MSD_CS")) msd_cs_ = std::atoi(g);
@@ -553,7 +553,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     }
     if (!dense) dslots.clear();
     // dense rows of >= 2 tiles each: the segmented one-sweep LSD sort (rtk_lsd.cu)
-    // (16-bit keys by default: 2 passes; RTK_LSD=all also for 32-bit keys, RTK_LSD=off never)
+    // (RTK_LSD=off: the MSD + bucket-sort path; RTK_LSD=16: 16-bit keys only)
     const bool lsd = dense && (lsd_mode_ == 2 || (lsd_mode_ == 1 && dtype == kF16));
     std::vector<uint64_t> l_tile{0}, l_len, l_in, l_buf, l_k, l_out;
     uint64_t l_total = 0;

@@ -211,7 +211,7 @@ private:
     bool no_fused_ = false;
     bool no_dense_ = false;
     int sparse_max_ = 96;            // RTK_SPARSE_MAX (k_compact sparse-hit path threshold)
-    int lsd_mode_ = 1;               // RTK_LSD: dense rows' LSD sort: 0 off, 1 16-bit keys, 2 all
+    int lsd_mode_ = 2;               // RTK_LSD: dense rows' LSD sort: 0 off (MSD + bucket sorts), 1 16-bit keys, 2 all
     size_t lsd_hist_cap_ = 0;
     DevBuf lsd_a_, lsd_b_, lsd_status_, lsd_meta_;
     int sparse_sel_ = 1;

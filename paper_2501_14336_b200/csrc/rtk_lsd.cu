@@ -34,6 +34,9 @@ constexpr int kLsdWarps = kLsdThreads / 32;
 constexpr int kLsdItems = 16;
 constexpr int kLsdTile = kLsdThreads * kLsdItems;  // 4096 elements
 constexpr int kLsdHistThreads = 512;
+#ifndef RTK_LSD_BALLOT
+#define RTK_LSD_BALLOT 0
+#endif
 constexpr unsigned long long kLsdAgg = 1ull << 30, kLsdPrefix = 2ull << 30;
 
 uint32_t lsd_tile() { return kLsdTile; }
@@ -120,6 +123,10 @@ template <int SH, bool FIRST, bool LAST>
 __global__ void __launch_bounds__(kLsdThreads, 3) k_lsd_pass(LsdArgs a, uint32_t pass) {
     __shared__ unsigned long long s_tile[kLsdTile];
     __shared__ uint32_t s_cnt[kLsdWarps][256];
+#if !RTK_LSD_BALLOT
+    // peer masks live in the tile buffer, which is only written after the ranking
+    uint32_t (*s_match)[256] = reinterpret_cast<uint32_t (*)[256]>(s_tile);
+#endif
     __shared__ uint32_t s_dstart[256];
     __shared__ uint32_t s_gbase[256];
     __shared__ uint32_t s_w[kLsdWarps];
@@ -129,7 +136,12 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_lsd_pass(LsdArgs a, uint32_t
     const unsigned full = 0xffffffffu;
     const unsigned lt = (1u << lane) - 1u;
     if (tid == 0) s_t = atomicAdd(a.ctr + pass, 1u);
-    for (int i = tid; i < kLsdWarps * 256; i += kLsdThreads) (&s_cnt[0][0])[i] = 0;
+    for (int i = tid; i < kLsdWarps * 256; i += kLsdThreads) {
+        (&s_cnt[0][0])[i] = 0;
+#if !RTK_LSD_BALLOT
+        (&s_match[0][0])[i] = 0;
+#endif
+    }
     __syncthreads();
     const uint64_t t = s_t;
     const int j = lsd_row_of_tile(a, t);
@@ -140,6 +152,8 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_lsd_pass(LsdArgs a, uint32_t
     const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(a.ctr + 4) * 4u + pass + 1u;
     const uint32_t hrow = __ldcg(a.hist + j * 1024 + pass * 256 + tid);  // consumed after the look-back
     const bool full_tile = cnt == kLsdTile;
+    (void)full_tile;
+    (void)full;
     auto digit = [](unsigned long long K) { return (static_cast<uint32_t>(K >> 32) >> SH) & 255u; };
 
     // load: warp w owns tile elements [512w, 512w + 512), round i covers 32 consecutive ones
@@ -172,13 +186,26 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_lsd_pass(LsdArgs a, uint32_t
         const uint32_t e = warp * (kLsdItems * 32) + i * 32 + lane;
         const bool valid = e < cnt;
         const uint32_t d = digit(c[i]);
-        // ballot multisplit (8 ballots) measured faster here than __match_any_sync
+#if RTK_LSD_BALLOT
+        // ballot multisplit (8 ballots)
         unsigned peers = warp_peers8(d);
         if (!full_tile) peers &= __ballot_sync(full, valid);
+#else
+        // peers through a shared-memory bitmask per (warp, digit): each lane ORs its bit in, reads
+        // the mask back; the lowest peer clears it below (one shared atomic instead of 8 ballots)
+        if (valid) atomicOr(&s_match[warp][d], 1u << lane);
+        __syncwarp();
+        const unsigned peers = valid ? s_match[warp][d] : 0u;
+#endif
         const uint32_t b0 = s_cnt[warp][d];
         rk[i] = b0 + __popc(peers & lt);
         __syncwarp();
-        if (valid && (peers & lt) == 0) s_cnt[warp][d] = b0 + __popc(peers);
+        if (valid && (peers & lt) == 0) {
+            s_cnt[warp][d] = b0 + __popc(peers);
+#if !RTK_LSD_BALLOT
+            s_match[warp][d] = 0u;
+#endif
+        }
         __syncwarp();
     }
     __syncthreads();
