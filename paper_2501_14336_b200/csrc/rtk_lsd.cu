@@ -14,11 +14,12 @@
 //                ranks < k straight into the output and the pivot.
 //
 // Stability + the initial index order give ties in ascending index order, the reference's
-// tie rule. Shipped for 16-bit keys (two passes: bf16 C3 k = vocab 1.37 -> 0.76 ms); with four
-// passes (32-bit keys) it measured 1.41 ms against 1.34 ms for the MSD + bucket-sort path, so
-// f32/u32 dense rows stay there unless RTK_LSD=all (the per-tile latency chain — tile counter,
-// loads, ranks, look-back — and the smem-atomic histogram pass are the known limits). Traffic per element: 4 B (hist) + 4 B in / 8 B out (pass 0) + 16 B per middle pass
-// + 8 B in / 12 B out (last pass) — against ~5 scattered passes of the MSD + bucket-sort path.
+// tie rule. Stable warp ranks: each lane ORs its bit into a shared (warp, digit) mask and reads
+// its peers back — one shared atomic per item instead of an 8-ballot multisplit (which measured
+// 0.74 / 1.35 ms for bf16 / f32 C3 k = vocab against 0.66 / 1.21 ms). RTK_LSD=off selects the
+// MSD + bucket-sort path (1.34 ms f32, 1.37 ms bf16), RTK_LSD=16 this path for 16-bit keys only.
+// Traffic per element: 4 B (hist) + 4 B in / 8 B out (pass 0) + 16 B per middle pass + 8 B in /
+// 12 B out (last pass) — against ~5 scattered passes of the MSD + bucket-sort path.
 #include <cuda_runtime.h>
 
 #include <algorithm>

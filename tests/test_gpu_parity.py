@@ -484,11 +484,11 @@ def test_c2_full_size_small_k(cuda, k):
 
 
 
-@pytest.mark.parametrize("mode", ["all", "off"])
+@pytest.mark.parametrize("mode", ["all", "off", "16"])
 def test_dense_rows_lsd_forced(cuda, mode):
-    # dense rows (k >= n/2): the segmented one-sweep LSD sort is forced for 32-bit keys too
-    # (RTK_LSD=all) or disabled (off) in a fresh process; both must equal the reference per row,
-    # ragged rows, both orders, u32 ties and heavy f32 ties included
+    # dense rows (k >= n/2): the segmented one-sweep LSD sort (default, RTK_LSD=all), the MSD +
+    # bucket-sort path (off) and LSD for 16-bit keys only (16), each in a fresh process; all must
+    # equal the reference per row, ragged rows, both orders, u32 ties and heavy f32 ties included
     import subprocess
     import sys
     code = r'''
