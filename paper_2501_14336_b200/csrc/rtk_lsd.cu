@@ -32,7 +32,13 @@ namespace rtk_b200 {
 
 constexpr int kLsdThreads = 256;
 constexpr int kLsdWarps = kLsdThreads / 32;
-constexpr int kLsdItems = 16;
+#ifndef RTK_LSD_ITEMS
+#define RTK_LSD_ITEMS 16
+#endif
+#ifndef RTK_LSD_MINB
+#define RTK_LSD_MINB 3
+#endif
+constexpr int kLsdItems = RTK_LSD_ITEMS;
 constexpr int kLsdTile = kLsdThreads * kLsdItems;  // 4096 elements
 constexpr int kLsdHistThreads = 512;
 #ifndef RTK_LSD_BALLOT
@@ -121,8 +127,8 @@ __global__ void __launch_bounds__(kLsdHistThreads) k_lsd_hist(LsdArgs a, uint32_
 // SH: the digit's shift in the sort key (compile-time: one byte extract per item); FIRST:
 // pass 0 (reads the input); LAST: writes the output
 template <int SH, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(kLsdThreads, 3) k_lsd_pass(LsdArgs a, uint32_t pass) {
-    __shared__ unsigned long long s_tile[kLsdTile];
+__global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs a, uint32_t pass) {
+    extern __shared__ unsigned long long s_tile[];  // kLsdTile
     __shared__ uint32_t s_cnt[kLsdWarps][256];
 #if !RTK_LSD_BALLOT
     // peer masks live in the tile buffer, which is only written after the ranking
@@ -248,8 +254,7 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_lsd_pass(LsdArgs a, uint32_t
             }
             q -= W;
         }
-        __threadfence();
-        __stcg(st, ep | kLsdPrefix | (excl + tc));
+        __stcg(st, ep | kLsdPrefix | (excl + tc));  // flag and count in one 64-bit word: no fence
     }
     uint32_t tot;
     const uint32_t rowbase = lsd_block_scan(hrow, s_w, &tot);
@@ -308,12 +313,23 @@ void launch_lsd(uint64_t tiles, const LsdArgs& a, cudaStream_t s) {
         const dim3 g(static_cast<unsigned>(tiles));
         const uint32_t sh = a.shift0 + 8 * p;
         const bool first = p == 0, last = p + 1 == a.npass;
-        if (sh == 0) k_lsd_pass<0, true, false><<<g, kLsdThreads, 0, s>>>(b, p);
-        else if (sh == 8) k_lsd_pass<8, false, false><<<g, kLsdThreads, 0, s>>>(b, p);
-        else if (sh == 16 && first) k_lsd_pass<16, true, false><<<g, kLsdThreads, 0, s>>>(b, p);
-        else if (sh == 16) k_lsd_pass<16, false, false><<<g, kLsdThreads, 0, s>>>(b, p);
-        else if (last) k_lsd_pass<24, false, true><<<g, kLsdThreads, 0, s>>>(b, p);
-        else k_lsd_pass<24, false, false><<<g, kLsdThreads, 0, s>>>(b, p);
+        constexpr size_t sm = kLsdTile * sizeof(unsigned long long);
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(k_lsd_pass<0, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            cudaFuncSetAttribute(k_lsd_pass<8, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            cudaFuncSetAttribute(k_lsd_pass<16, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            cudaFuncSetAttribute(k_lsd_pass<16, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            cudaFuncSetAttribute(k_lsd_pass<24, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            cudaFuncSetAttribute(k_lsd_pass<24, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            configured = true;
+        }
+        if (sh == 0) k_lsd_pass<0, true, false><<<g, kLsdThreads, sm, s>>>(b, p);
+        else if (sh == 8) k_lsd_pass<8, false, false><<<g, kLsdThreads, sm, s>>>(b, p);
+        else if (sh == 16 && first) k_lsd_pass<16, true, false><<<g, kLsdThreads, sm, s>>>(b, p);
+        else if (sh == 16) k_lsd_pass<16, false, false><<<g, kLsdThreads, sm, s>>>(b, p);
+        else if (last) k_lsd_pass<24, false, true><<<g, kLsdThreads, sm, s>>>(b, p);
+        else k_lsd_pass<24, false, false><<<g, kLsdThreads, sm, s>>>(b, p);
     }
 }
 

@@ -7,5 +7,5 @@ x = torch.randn(256, 128256, device="cuda")
 for _ in range(2): rtk.batch_topk_dense(x, 128256)
 torch.cuda.synchronize()
 PY
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/lsd_launches.csv python /tmp/d.py > /dev/null 2>&1; echo "launch rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"k_lsd_pass" -s 2 -c 1 -o gpurun_out/prof_lsd -f python /tmp/d.py > gpurun_out/prof_lsd.log 2>&1; echo "full rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:"k_lsd_pass" -s 5 -c 1 -o gpurun_out/prof_lsd32 -f python /tmp/d.py > gpurun_out/prof_lsd32.log 2>&1; echo "full rc=$?"
+ncu -i gpurun_out/prof_lsd32.ncu-rep --page details --section WarpStateStats --section SchedulerStats --section Occupancy > gpurun_out/lsd32_details.txt 2>&1
