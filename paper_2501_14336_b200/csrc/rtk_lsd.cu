@@ -93,25 +93,47 @@ __global__ void __launch_bounds__(kLsdHistThreads) k_lsd_hist(LsdArgs a, uint32_
     const uint64_t e0 = n * c / chunks, e1 = n * (c + 1) / chunks;
     const uint64_t base = a.in_off[j];
     uint32_t* hg = &h[0][warp & 3][0];
-    constexpr int U = 8;
-    for (uint64_t b = e0; b < e1; b += static_cast<uint64_t>(U) * kLsdHistThreads) {
-        uint32_t raw[U];
+    auto count = [&](uint32_t raw) {
+        const uint32_t sk = ~make_key(a.in, raw);
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+            if (p < a.npass) atomicAdd(hg + p * 4 * 256 + ((sk >> (a.shift0 + 8 * p)) & 255u), 1u);
+    };
+    // 16-byte loads over the aligned body (4 f32 / 8 half words each, 4 in flight per thread);
+    // scalar head and tail
+    const int EB = a.in.dtype == kF16 ? 2 : 4;
+    const int VE = 16 / EB;
+    const char* bytes = reinterpret_cast<const char*>(a.in.base) + (base + e0) * EB;
+    const uint64_t mis = (reinterpret_cast<uintptr_t>(bytes) & 15) / EB;
+    const uint64_t head = mis ? min(static_cast<uint64_t>(VE) - mis, e1 - e0) : 0;
+    const uint64_t nvec = (e1 - e0 - head) / VE;
+    for (uint64_t e = e0 + threadIdx.x; e < e0 + head; e += kLsdHistThreads) count(load_elem(a.in, base + e));
+    const uint4* vp = reinterpret_cast<const uint4*>(bytes + head * EB);
+    constexpr int U = 4;
+    for (uint64_t v0 = 0; v0 < nvec; v0 += static_cast<uint64_t>(U) * kLsdHistThreads) {
+        uint4 q[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t e = b + static_cast<uint64_t>(u) * kLsdHistThreads + threadIdx.x;
-            raw[u] = e < e1 ? load_elem(a.in, base + e) : 0u;
+            const uint64_t v = v0 + static_cast<uint64_t>(u) * kLsdHistThreads + threadIdx.x;
+            if (v < nvec) q[u] = __ldcs(vp + v);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t e = b + static_cast<uint64_t>(u) * kLsdHistThreads + threadIdx.x;
-            if (e < e1) {
-                const uint32_t sk = ~make_key(a.in, raw[u]);
+            const uint64_t v = v0 + static_cast<uint64_t>(u) * kLsdHistThreads + threadIdx.x;
+            if (v >= nvec) continue;
+            const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
 #pragma unroll
-                for (int p = 0; p < 4; ++p)
-                    if (p < a.npass) atomicAdd(hg + p * 4 * 256 + ((sk >> (a.shift0 + 8 * p)) & 255u), 1u);
+            for (int i = 0; i < 4; ++i) {
+                if (EB == 2) {
+                    count(w[i] & 0xFFFFu);
+                    count(w[i] >> 16);
+                } else {
+                    count(w[i]);
+                }
             }
         }
     }
+    for (uint64_t e = e0 + head + nvec * VE + threadIdx.x; e < e1; e += kLsdHistThreads) count(load_elem(a.in, base + e));
     __syncthreads();
     for (int i = threadIdx.x; i < static_cast<int>(a.npass) * 256; i += kLsdHistThreads) {
         const int p = i >> 8, d = i & 255;
