@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
                 s_last = old + mine_tiles == tiles;
                 if (s_last) {
                     __threadfence();
-                    plan_row(cur_j, r, pa);
+                    plan_row(cur_j, r, pa, len);
                 }
             }
             __syncthreads();

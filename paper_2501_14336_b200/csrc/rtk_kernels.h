@@ -115,16 +115,19 @@ struct SegSlot {        // one MSD segment; len == 0 means inactive
     uint32_t bits;       // level 0: 11..14; deeper levels: kDigit
     uint32_t src;        // level 0: 1 = read the INPUT row at in_off (dense row, no compaction)
     uint64_t in_off;     // input element offset of the row (src == 1)
-    uint64_t base;       // digit = (rel(K) >> pos) & mask with rel(K) = ((key - key(base)) >> tz) << 32
+    uint64_t base;       // digit = (rel(K) >> pos) & mask with rel(K) = ((key - key(base)) >> tz) << ib
     uint32_t tz;         //   + (lo(K) - lo(base)): the candidates' RANGE, not their XOR, with the
                          //   key's common trailing zeros squeezed out (order-preserving); tie-heavy
-                         //   rows such as C4 split by index bits at level 0. Children inherit both.
+                         //   rows such as C4 split by index bits at level 0. Children inherit all three.
+    uint32_t ib;         // index field width: every row index < 2^ib, so |lo(K) - lo(base)| < 2^ib
+                         //   and the shifted key difference still dominates (0 = 32)
 };
 
 #ifdef __CUDACC__
 __device__ __forceinline__ unsigned long long slot_rel(const SegSlot& sl, unsigned long long K) {
     const uint32_t kd = (static_cast<uint32_t>(K >> 32) - static_cast<uint32_t>(sl.base >> 32)) >> sl.tz;
-    return (static_cast<unsigned long long>(kd) << 32) + (K & 0xffffffffull) - (sl.base & 0xffffffffull);
+    return (static_cast<unsigned long long>(kd) << (sl.ib ? sl.ib : 32u)) + (K & 0xffffffffull) -
+           (sl.base & 0xffffffffull);
 }
 #endif
 

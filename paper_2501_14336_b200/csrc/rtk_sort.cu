@@ -163,7 +163,7 @@ __device__ void seg_plan_block(int j, const SegSlot& sl, const SegPlanArgs& a) {
             const uint32_t q = atomicAdd(next.count, 1u);
             if (q < next.cap)
                 next.slots[q] = SegSlot{sl.off + start[i], c[i], sl.rank_base + start[i], sl.rid,
-                                        sl.pos >= kDigit ? sl.pos - kDigit : 0u, kDigit, 0, 0, sl.base, sl.tz};
+                                        sl.pos >= kDigit ? sl.pos - kDigit : 0u, kDigit, 0, 0, sl.base, sl.tz, sl.ib};
             atomicOr(flags, kFlagMore);
         } else if (gst[i]) {
             uint32_t end = INF;
@@ -395,7 +395,7 @@ __device__ void msd_plan_slice(const SegSlot& sl, uint32_t* tot, uint32_t slice,
                 } else {
                     if (ib < a.next.cap)
                         a.next.slots[ib] = SegSlot{sl.off + st, c, sl.rank_base + st, sl.rid,
-                                                   sl.pos >= kDigit ? sl.pos - kDigit : 0u, kDigit, 0, 0, sl.base, sl.tz};
+                                                   sl.pos >= kDigit ? sl.pos - kDigit : 0u, kDigit, 0, 0, sl.base, sl.tz, sl.ib};
                     else
                         overflow = true;
                     ++ib;

@@ -1,3 +1,5 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -k "batch or randomized or two_value or 16bit or dense" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -25 gpurun_out/pytest_gpu.log | grep -v '^\s*$' | tail -3
-KS=128256 DT=f32,bf16 timeout 300 python tools/c3_ab.py "" "" > gpurun_out/c3ab.log 2>&1; cat gpurun_out/c3ab.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -25 gpurun_out/pytest_gpu.log | grep -v '^\s*$' | tail -3
+timeout 600 python bench.py --batch-ks "" --no-cpu-baseline > gpurun_out/bench_c4.json 2>gpurun_out/bench_c4.err; echo "bench rc=$?"
+python -c "import json; d=json.load(open('gpurun_out/bench_c4.json')); print(d['ms_per_step'], {k:v['ms_per_step'] for k,v in d['k_sweep'].items()}, json.dumps({k:v['ms'] for k,v in d['adversarial_c4']['results'].items()}))"
+bash tools/gpu_marks_c4.sh | tail -4
