@@ -102,13 +102,39 @@ __device__ __forceinline__ uint32_t row_block_scan(uint32_t v, uint32_t* s_w, ui
 // Early stop exactly as select_bin + radix_select (engine.hpp:231-241, 293-312).
 __device__ unsigned long long cta_radix_select(const unsigned long long* buf, uint32_t m, uint64_t k,
                                                uint64_t target, uint32_t* hist, uint32_t* s_w,
-                                               unsigned long long* s_res, uint64_t* count_ge) {
+                                               unsigned long long* s_res, uint64_t* count_ge,
+                                               bool skip_const = false) {
     constexpr int per = kBins / kRowThreads;  // 4 bins per thread, thread 0 owns the top bins
     const int tid = threadIdx.x;
     unsigned long long prefix = 0;
     uint64_t k_rem = k, above = 0;
     unsigned int pos = 53;
+    // bits where the elements differ: digit windows without any are skipped (their bits are
+    // common to all, so they join the prefix as is). 16-bit keys leave bits 32-47 zero and small
+    // rows leave the high index bits constant: up to two wasted passes otherwise.
+    // (16-bit keys only: for f32 rows the extra reduction measured +1-2.5 us and nothing skips)
+    unsigned long long dif = ~0ull;
+    const unsigned long long ref = buf[0];
+    if (skip_const) {
+        dif = 0;
+        for (uint32_t i = tid; i < m; i += kRowThreads) dif |= buf[i] ^ ref;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) dif |= __shfl_xor_sync(0xffffffffu, dif, d);
+        if (tid == 0) s_res[0] = 0;
+        __syncthreads();
+        if ((tid & 31) == 0 && dif) atomicOr(&s_res[0], dif);
+        __syncthreads();
+        dif = s_res[0];
+        __syncthreads();
+    }
     for (;;) {
+        while (pos > 0) {  // skip constant windows
+            const unsigned int h = rows_digit_hi(pos);
+            const unsigned long long wmask = (h >= 64 ? ~0ull : ((1ull << h) - 1)) & ~((1ull << pos) - 1);
+            if (dif & wmask) break;
+            prefix |= ref & wmask;
+            pos = pos == 9 ? 0u : pos - 11u;
+        }
         for (int b = tid; b < kBins; b += kRowThreads) hist[b] = 0;
         __syncthreads();
         const unsigned int hi = rows_digit_hi(pos);
@@ -288,7 +314,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
         uint64_t cge;
         // exact rp-th sample composite: keeps the candidate count (and its spread) minimal
         const uint64_t rpc = rp < kRowSample ? rp : kRowSample;
-        T = cta_radix_select(cand, kRowSample, rpc, rpc, hist, s_w, s_res, &cge);
+        T = cta_radix_select(cand, kRowSample, rpc, rpc, hist, s_w, s_res, &cge, km_is16<KM>());
     }
     if (tid == 0) s_m = 0;
     __syncthreads();
@@ -464,7 +490,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     // ---- 3. exact k-th composite among the candidates, keep exactly k ----------------------
     if (m > k) {
         uint64_t cge;
-        const unsigned long long T2 = cta_radix_select(cand, m, k, k, hist, s_w, s_res, &cge);
+        const unsigned long long T2 = cta_radix_select(cand, m, k, k, hist, s_w, s_res, &cge, km_is16<KM>());
         // compaction to cand[0, k): read everything first, then write
         constexpr int PT = kRowCand / kRowThreads;  // 16
         unsigned long long keep[PT];
