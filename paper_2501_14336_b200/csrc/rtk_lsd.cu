@@ -156,7 +156,6 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
     // peer masks live in the tile buffer, which is only written after the ranking
     uint32_t (*s_match)[256] = reinterpret_cast<uint32_t (*)[256]>(s_tile);
 #endif
-    __shared__ uint32_t s_dstart[256];
     __shared__ uint32_t s_gbase[256];
     __shared__ uint32_t s_w[kLsdWarps];
     __shared__ uint32_t s_t;
@@ -281,8 +280,10 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
     uint32_t tot;
     const uint32_t rowbase = lsd_block_scan(hrow, s_w, &tot);
     const uint32_t dstart = lsd_block_scan(tc, s_w, &tot);
-    s_dstart[d] = dstart;
-    s_gbase[d] = rowbase + excl;
+    // tile-sorted position q of digit d goes to row position q + (rowbase + excl - dstart)
+    s_gbase[d] = rowbase + excl - dstart;
+#pragma unroll
+    for (int w = 0; w < kLsdWarps; ++w) s_cnt[w][d] += dstart;  // warp offsets -> tile positions
     __syncthreads();
     // reorder the tile by digit (stable) in shared memory
 #pragma unroll
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
         const uint32_t e = warp * (kLsdItems * 32) + i * 32 + lane;
         if (e < cnt) {
             const uint32_t dd = digit(c[i]);
-            s_tile[s_dstart[dd] + s_cnt[warp][dd] + rk[i]] = c[i];
+            s_tile[s_cnt[warp][dd] + rk[i]] = c[i];
         }
     }
     __syncthreads();
@@ -300,14 +301,14 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
         for (uint32_t q = tid; q < cnt; q += kLsdThreads) {
             const unsigned long long K = s_tile[q];
             const uint32_t dd = digit(K);
-            __stcs(dst + s_gbase[dd] + (q - s_dstart[dd]), K);
+            __stcs(dst + (s_gbase[dd] + q), K);
         }
     } else {
         const uint64_t k = a.k[j], oo = a.out_off[j];
         for (uint32_t q = tid; q < cnt; q += kLsdThreads) {
             const unsigned long long K = s_tile[q];
             const uint32_t dd = digit(K);
-            const uint64_t rank = s_gbase[dd] + (q - s_dstart[dd]);
+            const uint64_t rank = s_gbase[dd] + q;
             if (rank >= k) continue;
             const uint32_t kv = ~static_cast<uint32_t>(K >> 32);
             const uint32_t idx = static_cast<uint32_t>(K);
