@@ -572,22 +572,36 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     unsigned long long* tmp = cand + kRowKMax;
     // per-warp digit counters live in the (now idle) streaming ring
     uint32_t (*cnt)[256] = reinterpret_cast<uint32_t (*)[256]>(cand + kRowCand);
+    // per-warp peer masks right after them (the large variant's ring holds exactly both)
+    uint32_t (*pmask)[256] = cnt + kRowWarps;
+    static_assert(STAGES * UU * kRowChunk * sizeof(uint32_t) >= 2 * kRowWarps * 256 * sizeof(uint32_t),
+                  "the streaming ring must hold the sort's counters and peer masks");
     const unsigned lt = (1u << lane) - 1u;
     auto lsd = [&](int lo0) {
     for (int lo = lo0; lo < nbits; lo += 8) {
         if (((orv >> lo) & 0xFFull) == 0) continue;  // digit constant across the group: no-op pass
-        for (int i = tid; i < kRowWarps * 256; i += kRowThreads) (&cnt[0][0])[i] = 0;
+        for (int i = tid; i < kRowWarps * 256; i += kRowThreads) {
+            (&cnt[0][0])[i] = 0;
+            (&pmask[0][0])[i] = 0;
+        }
         __syncthreads();
         uint32_t dig[IT], rk[IT];
 #pragma unroll
         for (int q = 0; q < IT; ++q) {
             const uint32_t p = warp * 256 + q * 32 + lane;
             dig[q] = p < kk ? 255u - static_cast<uint32_t>((key[q] >> lo) & 0xFFu) : 255u;
-            const unsigned peers = warp_peers8(dig[q]);
+            // peers: each lane ORs its bit into the (warp, digit) mask and reads it back (one
+            // shared atomic instead of an 8-ballot multisplit); the lowest peer clears it
+            atomicOr(&pmask[warp][dig[q]], 1u << lane);
+            __syncwarp();
+            const unsigned peers = pmask[warp][dig[q]];
             const uint32_t b0 = cnt[warp][dig[q]];
             rk[q] = b0 + __popc(peers & lt);
             __syncwarp();
-            if ((peers & lt) == 0) cnt[warp][dig[q]] = b0 + __popc(peers);
+            if ((peers & lt) == 0) {
+                cnt[warp][dig[q]] = b0 + __popc(peers);
+                pmask[warp][dig[q]] = 0u;
+            }
             __syncwarp();
         }
         __syncthreads();
