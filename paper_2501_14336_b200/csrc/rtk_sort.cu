@@ -883,8 +883,6 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_sort_groups(SortArgs g) {
     __shared__ unsigned long long s_or[kSortThreads / 32];
     __shared__ uint32_t s_g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned full = 0xffffffffu;
-    const unsigned lt = (1u << lane) - 1u;
     pdl_wait();  // launched early (PDL) while the MSD kernel finishes
     for (;;) {
         if (tid == 0) s_g = atomicAdd(g.work, 1u);
