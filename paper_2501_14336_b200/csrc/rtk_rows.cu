@@ -197,20 +197,55 @@ __device__ unsigned long long cta_radix_select(const unsigned long long* buf, ui
     }
 }
 
-// Bitonic sort (descending) of buf[0, n2) in shared memory, n2 a power of two; small k only.
-__device__ void cta_bitonic_desc(unsigned long long* buf, int n2) {
-    for (int kk = 2; kk <= n2; kk <<= 1) {
+// Warp 0 sorts buf[0, 32*IPL) descending in registers (element lane*IPL + i in x[i]): compare-
+// exchanges inside a lane for strides < IPL, shuffles above; no block barrier per stage.
+template <int IPL>
+__device__ __forceinline__ void warp_bitonic_desc_smem(unsigned long long* buf) {
+    const int lane = threadIdx.x & 31;
+    constexpr int N = 32 * IPL;
+    unsigned long long x[IPL];
+#pragma unroll
+    for (int i = 0; i < IPL; ++i) x[i] = buf[lane * IPL + i];
+#pragma unroll
+    for (int kk = 2; kk <= N; kk <<= 1) {
+#pragma unroll
         for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-            for (int i = threadIdx.x; i < (n2 >> 1); i += kRowThreads) {
-                const int lo = ((i & ~(jj - 1)) << 1) | (i & (jj - 1));
-                const int hi = lo + jj;
-                const unsigned long long x = buf[lo], y = buf[hi];
-                const bool desc = (lo & kk) == 0;
-                if (desc ? (x < y) : (x > y)) { buf[lo] = y; buf[hi] = x; }
+            if (jj < IPL) {
+#pragma unroll
+                for (int i = 0; i < IPL; ++i) {
+                    if (i & jj) continue;
+                    const bool desc = ((lane * IPL + i) & kk) == 0;
+                    const unsigned long long u = x[i], v = x[i | jj];
+                    const bool sw = desc ? (u < v) : (u > v);
+                    x[i] = sw ? v : u;
+                    x[i | jj] = sw ? u : v;
+                }
+            } else {
+                const int lm = jj / IPL;
+                const bool lo = (lane & lm) == 0;
+#pragma unroll
+                for (int i = 0; i < IPL; ++i) {
+                    const bool desc = ((lane * IPL + i) & kk) == 0;
+                    const unsigned long long y = __shfl_xor_sync(0xffffffffu, x[i], lm);
+                    x[i] = (desc == lo) ? (x[i] > y ? x[i] : y) : (x[i] < y ? x[i] : y);
+                }
             }
-            __syncthreads();
         }
     }
+#pragma unroll
+    for (int i = 0; i < IPL; ++i) buf[lane * IPL + i] = x[i];
+}
+
+// small-k sort: n2 (a power of two) <= 512 composites by one warp in registers
+__device__ __forceinline__ void small_sort_desc(unsigned long long* buf, int n2) {
+    if (threadIdx.x < 32) {
+        if (n2 <= 32) warp_bitonic_desc_smem<1>(buf);
+        else if (n2 == 64) warp_bitonic_desc_smem<2>(buf);
+        else if (n2 == 128) warp_bitonic_desc_smem<4>(buf);
+        else if (n2 == 256) warp_bitonic_desc_smem<8>(buf);
+        else warp_bitonic_desc_smem<16>(buf);
+    }
+    __syncthreads();
 }
 
 template <int KM, int CAND, int STAGES, int SAMPLE, int UU>
@@ -525,11 +560,11 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
 
     if (kk <= static_cast<uint32_t>(kRowKMaxS)) {
         // ---- 4'. small k: bitonic sort in smem (pad with 0 = smallest composite) ------------
-        int n2 = 1;
+        int n2 = 32;  // one warp sorts in registers (>= 32 slots)
         while (n2 < static_cast<int>(kk)) n2 <<= 1;
         for (int i = kk + tid; i < n2; i += kRowThreads) cand[i] = 0ull;
         __syncthreads();
-        cta_bitonic_desc(cand, n2);
+        small_sort_desc(cand, n2);
         const uint64_t oo = a.row_out_off[r];
         for (uint32_t p = tid; p < kk; p += kRowThreads) {
             const unsigned long long K = cand[p];

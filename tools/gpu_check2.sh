@@ -3,7 +3,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 cp paper_2501_14336_b200/librtk_b200.so /tmp/lib_cur.so
 for v in old new old new; do
   cp paper_2501_14336_b200/build/var/lib_$v.so paper_2501_14336_b200/librtk_b200.so
-  echo "== $v"; KS=256,16384,1048576 timeout 300 python tools/c2_ab.py ""; timeout 300 python tools/c4_ab.py ""
+  echo "== $v"; KS=50 DT=f32,bf16 timeout 300 python tools/c3_ab.py ""
 done > gpurun_out/var.log 2>&1
 cp /tmp/lib_cur.so paper_2501_14336_b200/librtk_b200.so
 cat gpurun_out/var.log
