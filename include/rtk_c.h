@@ -102,6 +102,8 @@ typedef struct rtk_stats {
     uint64_t kernel_launches;    /* kernels launched by the call                          */
     float compact_ms;            /* device time of the streaming k_compact launch (events) */
     float total_ms;              /* device time of the whole call on its stream (events)   */
+    uint64_t deep_levels;        /* host-driven deeper MSD levels (buckets > 2048 after     */
+                                 /* level 0; the GPU analogue of BatchRunInfo::phase_b_rounds) */
 } rtk_stats;
 
 typedef struct rtk_handle_s* rtk_handle;
@@ -156,6 +158,22 @@ int rtk_bench_batched(rtk_handle h, const void* d_data, uint64_t data_len, const
                       void* d_out_vals, uint64_t* d_out_idx, const uint64_t* out_offsets,
                       void* d_out_pivots, const rtk_cfg* cfg, void* stream, void* d_flush,
                       uint64_t flush_bytes, int warmup, int steps, float* step_ms, float* mean_ms);
+/* Test / diagnostic switches of a handle (not tuning: results never change). name:
+ *   "force_exact"  value != 0: every row takes the exact path (the radix passes of
+ *                  radix_select, engine.hpp:293-312, with the early stop) as if its sampled
+ *                  threshold had missed; short rows skip the one-CTA kernel, dense rows the
+ *                  LSD sort. rtk_stats.fallback_rows reports the rows that took it.
+ *   "force_deep"   value != 0: the level-0 MSD digit is cut to 6 bits, so buckets larger than
+ *                  one CTA sort take the host-driven deeper levels (rtk_stats.deep_levels).
+ * Also read from the environment at handle creation (RTK_FORCE_EXACT=1, RTK_FORCE_DEEP=1).
+ * Unknown names -> RTK_INVALID_ARGUMENT. */
+int rtk_set_option(rtk_handle h, const char* name, int64_t value);
+/* rtk::BatchRunInfo (batch.hpp:138-141) of the last call on the handle: task_passes[t] = full
+ * reads of task t's input (1 on the single-read sampled path; + the exact path's digit passes
+ * and its re-compaction when the sampled threshold missed); *phase_b_rounds = deeper MSD levels
+ * run over the live buckets of all tasks (rtk_stats.deep_levels). task_passes may be NULL;
+ * B must not exceed the last call's row count. */
+int rtk_get_batch_info(rtk_handle h, uint64_t* task_passes, uint64_t B, uint64_t* phase_b_rounds);
 void rtk_cfg_default(rtk_cfg* cfg);
 int rtk_cfg_validate(const rtk_cfg* cfg);
 

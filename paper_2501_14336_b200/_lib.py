@@ -47,7 +47,7 @@ class rtk_scale_info(C.Structure):
 class rtk_stats(C.Structure):
     _fields_ = [("passes", u64), ("elements_scanned", u64), ("candidates", u64),
                 ("fallback_rows", u64), ("kernel_launches", u64), ("compact_ms", C.c_float),
-                ("total_ms", C.c_float)]
+                ("total_ms", C.c_float), ("deep_levels", u64)]
 
 
 class rtk_dist(C.Structure):
@@ -63,6 +63,8 @@ SIGNATURES = {
     "rtk_handle_destroy": (C.c_int, [vp]),
     "rtk_get_stats": (C.c_int, [vp, C.POINTER(rtk_stats)]),
     "rtk_set_timing": (C.c_int, [vp, C.c_int]),
+    "rtk_set_option": (C.c_int, [vp, C.c_char_p, C.c_int64]),
+    "rtk_get_batch_info": (C.c_int, [vp, P64, u64, P64]),
     "rtk_bench_batched": (C.c_int, [vp, vp, u64, P64, P64, P64, u64, C.c_int, C.c_int, vp, vp, P64, vp,
                                     C.POINTER(rtk_cfg), vp, vp, u64, C.c_int, C.c_int,
                                     C.POINTER(C.c_float), C.POINTER(C.c_float)]),

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <random>
 #include <string>
@@ -18,6 +19,9 @@ using rtk_b200::Error;
 using rtk_b200::RowReq;
 
 struct rtk_handle_s {
+    // one caller at a time per handle: the engine's workspace, pinned staging, graph cache and
+    // signal words are shared state (recursive: the bench helpers call the entry points)
+    std::recursive_mutex mu;
     Engine engine;
     rtk_b200::DevBuf smp_vals, smp_idx;  // top-k workspace of rtk_topk_sample (when not supplied)
     explicit rtk_handle_s(int dev) : engine(dev) {}
@@ -33,6 +37,18 @@ using rtk_b200::g_last_error;
 using rtk_b200::guarded;
 
 namespace {
+
+// every entry point taking a handle: status codes, the handle's lock, its device made current
+// (and the caller's restored)
+template <typename F>
+int on_handle(rtk_handle h, F&& f) {
+    return guarded([&] {
+        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+        std::lock_guard<std::recursive_mutex> lock(h->mu);
+        rtk_b200::DeviceGuard dg(h->engine.device());
+        f();
+    });
+}
 
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw Error{RTK_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e)};
@@ -172,25 +188,45 @@ int rtk_handle_create(rtk_handle* out, int device) {
         int count = 0;
         cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
         if (device < 0 || device >= count) throw Error{RTK_INVALID_ARGUMENT, "no such CUDA device"};
-        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        rtk_b200::DeviceGuard dg(device);
         *out = new rtk_handle_s(device);
     });
 }
 
 int rtk_handle_destroy(rtk_handle h) {
-    return guarded([&] { delete h; });
+    return guarded([&] {
+        if (!h) return;
+        rtk_b200::DeviceGuard dg(h->engine.device());
+        delete h;
+    });
 }
 
 int rtk_set_timing(rtk_handle h, int on) {
-    return guarded([&] {
-        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+    return on_handle(h, [&] {
         h->engine.set_timing(on != 0);
     });
 }
 
+int rtk_set_option(rtk_handle h, const char* name, int64_t value) {
+    return on_handle(h, [&] {
+        if (!name || !h->engine.set_option(name, value))
+            throw Error{RTK_INVALID_ARGUMENT, std::string("unknown option: ") + (name ? name : "(null)")};
+    });
+}
+
+int rtk_get_batch_info(rtk_handle h, uint64_t* task_passes, uint64_t B, uint64_t* phase_b_rounds) {
+    return on_handle(h, [&] {
+        const std::vector<uint64_t>& p = h->engine.row_passes();
+        if (task_passes && B > p.size()) throw Error{RTK_INVALID_ARGUMENT, "batch info: more tasks than the last call had"};
+        if (task_passes)
+            for (uint64_t t = 0; t < B; ++t) task_passes[t] = p[t];
+        if (phase_b_rounds) *phase_b_rounds = h->engine.last_stats().deep_levels;
+    });
+}
+
 int rtk_get_stats(rtk_handle h, rtk_stats* out) {
-    return guarded([&] {
-        if (!h || !out) throw Error{RTK_INVALID_ARGUMENT, "null argument"};
+    return on_handle(h, [&] {
+        if (!out) throw Error{RTK_INVALID_ARGUMENT, "null argument"};
         *out = h->engine.last_stats();
     });
 }
@@ -198,8 +234,7 @@ int rtk_get_stats(rtk_handle h, rtk_stats* out) {
 int rtk_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, int order,
              void* d_out_vals, uint64_t* d_out_idx, void* d_out_pivot, const rtk_cfg* cfg,
              void* stream) {
-    return guarded([&] {
-        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+    return on_handle(h, [&] {
         const rtk_cfg c = cfg ? *cfg : default_cfg();
         check_common(d_in, n, k, dtype, order, c, "topk");
         h->engine.run(static_cast<const uint32_t*>(d_in), eng_dtype(dtype), order, false, 0.0f, false,
@@ -211,8 +246,8 @@ int rtk_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, 
 int rtk_bench_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, int order,
                    void* d_out_vals, uint64_t* d_out_idx, void* d_out_pivot, const rtk_cfg* cfg,
                    void* stream, int warmup, int steps, float* step_ms, float* mean_ms) {
-    return guarded([&] {
-        if (!h || steps < 1 || warmup < 0) throw Error{RTK_INVALID_ARGUMENT, "bench: bad arguments"};
+    return on_handle(h, [&] {
+        if (steps < 1 || warmup < 0) throw Error{RTK_INVALID_ARGUMENT, "bench: bad arguments"};
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         for (int i = 0; i < warmup; ++i) {
             const int st = rtk_topk(h, d_in, n, k, dtype, order, d_out_vals, d_out_idx, d_out_pivot, cfg, stream);
@@ -246,8 +281,8 @@ int rtk_bench_scaled(rtk_handle h, const float* d_in, uint64_t n, uint64_t k, in
                      double trigger_fraction, uint64_t seed, float* d_out_vals, uint64_t* d_out_idx,
                      float* d_out_pivot, const rtk_cfg* cfg, void* stream, int warmup, int steps,
                      float* step_ms, float* mean_ms) {
-    return guarded([&] {
-        if (!h || steps < 1 || warmup < 0) throw Error{RTK_INVALID_ARGUMENT, "bench: bad arguments"};
+    return on_handle(h, [&] {
+        if (steps < 1 || warmup < 0) throw Error{RTK_INVALID_ARGUMENT, "bench: bad arguments"};
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         auto one = [&] {
             const int st = rtk_topk_scaled(h, d_in, n, k, order, mode, trigger_fraction, seed, d_out_vals, d_out_idx,
@@ -287,8 +322,8 @@ int rtk_bench_batched(rtk_handle h, const void* d_data, uint64_t data_len, const
                       void* d_out_vals, uint64_t* d_out_idx, const uint64_t* out_offsets,
                       void* d_out_pivots, const rtk_cfg* cfg, void* stream, void* d_flush,
                       uint64_t flush_bytes, int warmup, int steps, float* step_ms, float* mean_ms) {
-    return guarded([&] {
-        if (!h || steps < 1 || warmup < 0) throw Error{RTK_INVALID_ARGUMENT, "bench: bad arguments"};
+    return on_handle(h, [&] {
+        if (steps < 1 || warmup < 0) throw Error{RTK_INVALID_ARGUMENT, "bench: bad arguments"};
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         auto one = [&] {
             const int st = rtk_topk_batched(h, d_data, data_len, offsets, lengths, ks, B, dtype, order, d_out_vals,
@@ -328,8 +363,7 @@ int rtk_topk_batched(rtk_handle h, const void* d_data, uint64_t data_len, const 
                      void* d_out_pivots, const rtk_cfg* cfg, const rtk_batch_opts* opts,
                      void* stream) {
     (void)opts;  // rescheduling / padding change the schedule only, never the results
-    return guarded([&] {
-        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+    return on_handle(h, [&] {
         validate_batch(data_len, offsets, lengths, ks, B);
         const rtk_cfg c = cfg ? *cfg : default_cfg();
         validate_cfg(c);
@@ -349,8 +383,7 @@ int rtk_topk_batched(rtk_handle h, const void* d_data, uint64_t data_len, const 
 int rtk_topk_scaled(rtk_handle h, const float* d_in, uint64_t n, uint64_t k, int order, int mode,
                     double trigger_fraction, uint64_t seed, float* d_out_vals, uint64_t* d_out_idx,
                     float* d_out_pivot, rtk_scale_info* info, const rtk_cfg* cfg, void* stream) {
-    return guarded([&] {
-        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+    return on_handle(h, [&] {
         const rtk_cfg c = cfg ? *cfg : default_cfg();
         if (n == 0) throw Error{RTK_EMPTY_INPUT, "scaled_topk: empty input"};
         if (k == 0 || k > n) throw Error{RTK_RANK_OUT_OF_RANGE, "scaled_topk: k outside [1, n]"};
@@ -365,8 +398,7 @@ int rtk_topk_scaled(rtk_handle h, const float* d_in, uint64_t n, uint64_t k, int
 int rtk_topk_sample(rtk_handle h, const void* d_logits, uint64_t B, uint64_t V, uint64_t row_stride, int dtype,
                     uint64_t k, float top_p, float temperature, const float* d_uniform, uint64_t* d_token,
                     float* d_probs, void* d_topk_vals, uint64_t* d_topk_idx, void* stream) {
-    return guarded([&] {
-        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+    return on_handle(h, [&] {
         if (B == 0) throw Error{RTK_INVALID_ARGUMENT, "sample: no rows"};
         if (V == 0) throw Error{RTK_EMPTY_INPUT, "sample: empty rows"};
         if (k == 0 || k > V) throw Error{RTK_RANK_OUT_OF_RANGE, "sample: k outside [1, V]"};
@@ -378,7 +410,7 @@ int rtk_topk_sample(rtk_handle h, const void* d_logits, uint64_t B, uint64_t V, 
         if (!d_logits || !d_uniform || !d_token) throw Error{RTK_INVALID_ARGUMENT, "sample: null argument"};
         if (V > (uint64_t(1) << 32)) throw Error{RTK_INVALID_ARGUMENT, "sample: V > 2^32"};
         Engine& e = h->engine;
-        cuda_check(cudaSetDevice(e.device()), "cudaSetDevice");
+        rtk_b200::DeviceGuard dg(e.device());
         void* tv = d_topk_vals;
         uint64_t* ti = d_topk_idx;
         if (!tv) {
@@ -404,12 +436,11 @@ int rtk_topk_sample(rtk_handle h, const void* d_logits, uint64_t B, uint64_t V, 
 
 int rtk_topk_host(rtk_handle h, const void* in, uint64_t n, uint64_t k, int dtype, int order,
                   void* out_vals, uint64_t* out_idx, void* out_pivot, const rtk_cfg* cfg) {
-    return guarded([&] {
-        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+    return on_handle(h, [&] {
         const rtk_cfg c = cfg ? *cfg : default_cfg();
         check_common(in, n, k, dtype, order, c, "topk");
         Engine& e = h->engine;
-        cuda_check(cudaSetDevice(e.device()), "cudaSetDevice");
+        rtk_b200::DeviceGuard dg(e.device());
         e.io_in.ensure(esize(dtype) * n);
         e.io_vals.ensure(esize(dtype) * k);
         e.io_idx.ensure(8 * k);
@@ -429,15 +460,14 @@ int rtk_topk_batched_host(rtk_handle h, const void* data, uint64_t data_len, con
                           const uint64_t* lengths, const uint64_t* ks, uint64_t B, int dtype, int order,
                           void* out_vals, uint64_t* out_idx, const uint64_t* out_offsets, void* out_pivots,
                           const rtk_cfg* cfg, const rtk_batch_opts* opts) {
-    return guarded([&] {
-        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+    return on_handle(h, [&] {
         validate_batch(data_len, offsets, lengths, ks, B);
         std::vector<uint64_t> oo = out_offsets ? std::vector<uint64_t>(out_offsets, out_offsets + B)
                                                : packed_out_offsets(ks, B);
         uint64_t out_total = 0;
         for (uint64_t t = 0; t < B; ++t) out_total = std::max(out_total, oo[t] + ks[t]);
         Engine& e = h->engine;
-        cuda_check(cudaSetDevice(e.device()), "cudaSetDevice");
+        rtk_b200::DeviceGuard dg(e.device());
         e.io_in.ensure(esize(dtype) * std::max<uint64_t>(data_len, 1));
         e.io_vals.ensure(esize(dtype) * out_total);
         e.io_idx.ensure(8 * out_total);
@@ -471,14 +501,13 @@ int rtk_topk_batched_host(rtk_handle h, const void* data, uint64_t data_len, con
 int rtk_topk_scaled_host(rtk_handle h, const float* in, uint64_t n, uint64_t k, int order, int mode,
                          double trigger_fraction, uint64_t seed, float* out_vals, uint64_t* out_idx,
                          float* out_pivot, rtk_scale_info* info, const rtk_cfg* cfg) {
-    return guarded([&] {
-        if (!h) throw Error{RTK_INVALID_ARGUMENT, "null handle"};
+    return on_handle(h, [&] {
         const rtk_cfg c = cfg ? *cfg : default_cfg();
         if (n == 0) throw Error{RTK_EMPTY_INPUT, "scaled_topk: empty input"};
         if (k == 0 || k > n) throw Error{RTK_RANK_OUT_OF_RANGE, "scaled_topk: k outside [1, n]"};
         check_common(in, n, k, RTK_F32, order, c, "scaled_topk");
         Engine& e = h->engine;
-        cuda_check(cudaSetDevice(e.device()), "cudaSetDevice");
+        rtk_b200::DeviceGuard dg(e.device());
         e.io_in.ensure(4 * n);
         e.io_vals.ensure(4 * k);
         e.io_idx.ensure(8 * k);
@@ -498,8 +527,8 @@ int rtk_merge_shards(rtk_handle h, const void* d_cand_vals, const uint64_t* d_ca
                      const uint64_t* block_len, const uint64_t* shard_base, uint32_t G, uint64_t k,
                      int dtype, int order, void* d_out_vals, uint64_t* d_out_idx, void* d_out_pivot,
                      void* stream) {
-    return guarded([&] {
-        if (!h || !block_len || !shard_base || G == 0) throw Error{RTK_INVALID_ARGUMENT, "bad shard descriptor"};
+    return on_handle(h, [&] {
+        if (!block_len || !shard_base || G == 0) throw Error{RTK_INVALID_ARGUMENT, "bad shard descriptor"};
         std::vector<uint64_t> start(G), base(shard_base, shard_base + G);
         uint64_t total = 0;
         for (uint32_t g = 0; g < G; ++g) {

@@ -111,14 +111,24 @@ __device__ __forceinline__ uint32_t load_elem(const InputSrc& s, uint64_t i) {
     return __ldg(s.base + i);
 }
 
+// y = x - a_s as the reference computes it on x86-64 (scaling.hpp:69-70, SSE subss): IEEE fp32
+// round-to-nearest with denormals kept (the library is built without -use_fast_math / -ftz);
+// a NaN result follows the x86 rule instead of the GPU's canonical 0x7FFFFFFF — the first NaN
+// operand quieted (x, then a_s, sign and payload kept), else the default NaN 0xFFC00000
+// (inf - inf). The NaN's sign decides whether it ranks above +inf or below -inf.
+__device__ __forceinline__ uint32_t sub_x86(uint32_t xb, float a) {
+    const float y = __fsub_rn(__uint_as_float(xb), a);
+    if (y == y) return __float_as_uint(y);
+    const uint32_t ab = __float_as_uint(a);
+    if ((xb & 0x7fffffffu) > 0x7f800000u) return xb | 0x00400000u;
+    if ((ab & 0x7fffffffu) > 0x7f800000u) return ab | 0x00400000u;
+    return 0xFFC00000u;
+}
+
 __device__ __forceinline__ uint32_t make_key(const InputSrc& s, uint32_t raw) {
     if (s.dtype == kF16) return encode_f16_key(raw, s.smallest);
     if (s.dtype == kF32) {
-        if (s.scaled) {
-            // y = x - a_s in IEEE fp32 round-to-nearest, denormals kept (scaling.hpp:69-70);
-            // the library is built without -use_fast_math / -ftz.
-            raw = __float_as_uint(__fsub_rn(__uint_as_float(raw), s.a_s));
-        }
+        if (s.scaled) raw = sub_x86(raw, s.a_s);
         return encode_f32_bits(raw, s.smallest);
     }
     return s.smallest ? ~raw : raw;  // KeyCodec<u32>, keycodec.hpp:72-81
@@ -142,7 +152,7 @@ template <int KM>
 __device__ __forceinline__ uint32_t key_of(uint32_t raw, const InputSrc& in) {
     const float a_s = in.a_s;
     if (KM == kKmF32LAdapt || KM == kKmF32SAdapt) {  // decided on the device: kernel-uniform branch
-        if (in.scaled) raw = __float_as_uint(__fsub_rn(__uint_as_float(raw), a_s));
+        if (in.scaled) raw = sub_x86(raw, a_s);
         const uint32_t m = static_cast<uint32_t>(static_cast<int32_t>(raw) >> 31) | 0x80000000u;
         const uint32_t bits = raw ^ m;
         return KM == kKmF32SAdapt ? ~bits : bits;
@@ -156,7 +166,7 @@ __device__ __forceinline__ uint32_t key_of(uint32_t raw, const InputSrc& in) {
     if (KM == kKmU32L) return raw;
     if (KM == kKmU32S) return ~raw;
     if (KM == kKmF32LScaled || KM == kKmF32SScaled)
-        raw = __float_as_uint(__fsub_rn(__uint_as_float(raw), a_s));
+        raw = sub_x86(raw, a_s);
     // sign-flip map as mask arithmetic: negative -> ~raw, positive -> raw | sign
     const uint32_t m = static_cast<uint32_t>(static_cast<int32_t>(raw) >> 31) | 0x80000000u;
     const uint32_t bits = raw ^ m;

@@ -91,8 +91,20 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_MSD_CS")) msd_cs_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_TILE_CONTIG")) tile_contig_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_DENSE_BITS")) dense_bits_ = static_cast<uint32_t>(std::atoi(g));
+    if (const char* g = std::getenv("RTK_FORCE_EXACT")) force_exact_ = *g && *g != '0';
+    if (const char* g = std::getenv("RTK_FORCE_DEEP")) force_deep_ = *g && *g != '0';
     const char* cs = std::getenv("RTK_COUNT_STATS");
     count_stats_ = profile_ || (cs && *cs && *cs != '0');
+}
+
+bool Engine::set_option(const std::string& name, int64_t value) {
+    if (name == "force_exact") force_exact_ = value != 0;
+    else if (name == "force_deep") force_deep_ = value != 0;
+    else return false;
+    graph_.valid = false;  // captured graphs embed the previous plan
+    have_last_ = false;
+    needs_init_ = true;
+    return true;
 }
 
 Engine::~Engine() {
@@ -273,7 +285,7 @@ const rtk_stats& Engine::last_stats() {
 void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, float a_s,
                  bool gather, const std::vector<RowReq>& rows, uint32_t* d_vals, uint64_t* d_idx,
                  uint32_t* d_pivots, cudaStream_t s) {
-    check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     if (rows.empty()) return;
     if (!ev_[0]) {
         for (auto& e : ev_) check(cudaEventCreate(&e), "cudaEventCreate");
@@ -318,6 +330,7 @@ void Engine::run(const uint32_t* d_base, int dtype, int smallest, bool scaled, f
         wgroup_base_ = graph_.wgroup_base;
         stats = graph_.stats;
         const int R = static_cast<int>(rows.size());
+        row_passes_.assign(R, 1);
         if (!graph_.has_init && (needs_init_ || R > clean_upto_)) {
             launch_init_call(R, count_.as<unsigned long long>(), kmin_.as<unsigned long long>(),
                              kmax_.as<unsigned long long>(), kor_.as<uint32_t>(), T_.as<uint64_t>(), row_fail_.as<uint32_t>(),
@@ -416,6 +429,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     pin_used_ = 0;
     stats = rtk_stats{};
     const int R = static_cast<int>(rows.size());
+    row_passes_.assign(R, 1);  // one streaming read per row (sampled, fused, dense and LSD rows)
     record(0, s);
     mark("start", s);
     group_base_ = 0;
@@ -445,7 +459,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     std::vector<uint64_t> f_off[2], f_len[2], f_k[2];
     // returns -1 (general path), 0 (large-buffer fused variant) or 1 (small-buffer variant)
     auto fused_class = [&](const RowReq& q) {
-        if (no_fused_) return -1;
+        if (no_fused_ || force_exact_) return -1;
         if (q.k == 0 || q.k > rows_fused_kmax(false)) return -1;
         if (q.n > (uint64_t(1) << 18) && R < 64) return -1;  // long rows want many CTAs
         for (int small = 1; small >= 0; --small) {
@@ -542,12 +556,12 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     // Dense mode: every general row is unsampled with k >= n/2 (e.g. k = vocab): all elements are
     // candidates, so the compaction would only rewrite the rows as composites. The level-0 MSD
     // reads the input instead (slot.src = 1), its digit the top bits of the key.
-    bool dense = !grow.empty() && no_dense_ == false;
+    bool dense = !grow.empty() && no_dense_ == false && !force_exact_;
     std::vector<SegSlot> dslots;
     for (uint32_t r : grow) {
         const RowReq& q = rows[r];
         if (sampled[r] || 2 * q.k < q.n || q.n <= kSortCap) { dense = false; break; }
-        const uint32_t bits = std::min<uint32_t>(dense_bits_ ? dense_bits_ : fine_bits(q.n), msd_max_bits_);
+        const uint32_t bits = std::min<uint32_t>(dense_bits_ ? dense_bits_ : fine_bits(q.n), level0_bits());
         SegSlot sl{cand_off[r], q.n, 0, r, 64u - bits, bits, 1u, q.in_off};
         dslots.push_back(sl);
     }
@@ -855,7 +869,8 @@ PlanArgs Engine::plan_args(const Call& c, const FinishPrep& f) {
     pa.flags = ctl_.as<uint32_t>();
     pa.row_fail = row_fail_.as<uint32_t>();
     pa.done = done_.as<uint32_t>();
-    pa.max_bits = static_cast<uint32_t>(msd_max_bits_);
+    pa.max_bits = level0_bits();
+    pa.force_fail = force_exact_ && !in_fallback_ ? 1u : 0u;
     pa.prefetch_mb = static_cast<uint32_t>(prefetch_mb_);
     pa.sparse_max = static_cast<uint32_t>(sparse_max_);
     pa.sparse_sel = static_cast<uint32_t>(sparse_sel_);
@@ -1045,6 +1060,7 @@ void Engine::drain(Call& c, uint32_t (&ctl)[8]) {
                            bstart_.as<uint32_t>(), gcursor_.as<uint32_t>(), c.s);
         launch_sort(static_cast<uint32_t>(max_groups), sort_args(c, gl), c.s);
         stats.kernel_launches += 2;
+        ++stats.deep_levels;
         group_base_ += max_groups;
         check(cudaMemcpyAsync(hctl_, ctl_.p, 32, cudaMemcpyDeviceToHost, c.s), "d2h");
         sync(c.s, "msd level");
@@ -1105,6 +1121,7 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
                           ghist_.as<unsigned long long>(), s);
         ++stats.passes;
         ++stats.kernel_launches;
+        for (uint32_t r : active) ++row_passes_[r];
         check(cudaMemcpyAsync(st.data(), sel_.p, sizeof(RowSel) * R, cudaMemcpyDeviceToHost, s), "d2h");
         sync(s, "fallback pass");
         std::vector<uint32_t> still;
@@ -1157,14 +1174,18 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
     check(cudaMemsetAsync(ctl_.as<uint32_t>() + 3, 0, 8, s), "memset");
     check(cudaMemcpyAsync(ctl_.as<uint32_t>() + 2, ctl_.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToDevice, s), "work");
     check(cudaMemcpyAsync(ctl_.as<uint32_t>() + 6, ctl_.as<uint32_t>() + 5, 4, cudaMemcpyDeviceToDevice, s), "wwork");
+    for (uint32_t r : fb) ++row_passes_[r];  // the re-compaction reads the row once more
     FinishPrep fp = prepare_finish(c, fb);
     check(cudaMemsetAsync(seg_hist_.p, 0, 4ull * kBins * fb.size(), s), "memset");
     check(cudaMemsetAsync(seg_ticket_.p, 0, 4ull * fb.size(), s), "memset");
     Rows rr{static_cast<int>(fb.size()), at<uint32_t>(D, o_rid), at<uint64_t>(D, o_off),
             at<uint64_t>(D, o_len), at<uint32_t>(D, o_lead), at<uint64_t>(D, o_tile)};
+    in_fallback_ = true;
+    const PlanArgs fpa = plan_args(c, fp);
+    in_fallback_ = false;
     launch_compact(tiles.back(), rr, src, T_.as<uint64_t>(), cand_a_.as<uint64_t>(),
                    c.d_coff, c.d_cap, count_.as<unsigned long long>(),
-                   kmin_.as<unsigned long long>(), kmax_.as<unsigned long long>(), plan_args(c, fp), s);
+                   kmin_.as<unsigned long long>(), kmax_.as<unsigned long long>(), fpa, s);
     ++stats.kernel_launches;
     launch_finish(c, fp);
     std::vector<uint64_t> count(R);
@@ -1178,7 +1199,7 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
 // ---------------------------------------------------------------------------------------
 std::vector<uint64_t> Engine::first_digit_hist(const uint32_t* d_in, uint64_t n, unsigned d,
                                                int smallest, cudaStream_t s) {
-    check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     const uint64_t nb = uint64_t(1) << d;
     DevBuf& h = io_aux;
     h.ensure(8 * nb);
@@ -1203,7 +1224,7 @@ std::vector<uint64_t> Engine::first_digit_hist(const uint32_t* d_in, uint64_t n,
 
 void Engine::enqueue_scale_decide(const uint32_t* d_in, uint64_t n, uint64_t k, unsigned d, int smallest,
                                   int mode, double tau, uint64_t a_index, cudaStream_t s) {
-    check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     if (!hscale_) {
         check(cudaHostAlloc(reinterpret_cast<void**>(&hscale_), 16, cudaHostAllocMapped), "cudaHostAlloc");
         std::memset(hscale_, 0, 16);

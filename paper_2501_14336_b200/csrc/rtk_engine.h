@@ -30,6 +30,29 @@ struct RowReq {
     uint64_t out_off;  // element offset of the row's outputs
 };
 
+// Makes `dev` current for the scope and restores the caller's device afterwards (the caller's
+// framework, e.g. torch.cuda.current_device(), must not see a different device after a call).
+class DeviceGuard {
+public:
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+        if (prev_ != dev) {
+            const cudaError_t e = cudaSetDevice(dev);
+            if (e != cudaSuccess) throw Error{RTK_CUDA_ERROR, std::string("cudaSetDevice: ") + cudaGetErrorString(e)};
+            set_ = true;
+        }
+    }
+    ~DeviceGuard() {
+        if (set_ && prev_ >= 0) cudaSetDevice(prev_);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+
+private:
+    int prev_ = -1;
+    bool set_ = false;
+};
+
 // Growable device buffer.
 struct DevBuf {
     void* p = nullptr;
@@ -79,6 +102,11 @@ public:
     // bench: events recorded on the call's stream right before its first and after its last
     // device operation (host planning and the completion wait stay outside); null = off
     void set_call_events(cudaEvent_t start, cudaEvent_t end) { call_start_ = start; call_end_ = end; }
+
+    // test switches (rtk_set_option): "force_exact", "force_deep"; false for unknown names
+    bool set_option(const std::string& name, int64_t value);
+    // full reads of each row's input in the last call (BatchRunInfo::task_passes)
+    const std::vector<uint64_t>& row_passes() const { return row_passes_; }
 
     int device() const { return device_; }
     rtk_stats stats{};
@@ -208,6 +236,11 @@ private:
     bool no_graph_events_ = true;   // no stats events inside graphs (RTK_GRAPH_EVENTS=1 keeps them)
     cudaEvent_t call_start_ = nullptr, call_end_ = nullptr;
     bool timing_ = false;           // rtk_set_timing: no graph replay, events around k_compact
+    bool force_exact_ = false;      // RTK_FORCE_EXACT / "force_exact"
+    bool force_deep_ = false;       // RTK_FORCE_DEEP / "force_deep"
+    bool in_fallback_ = false;      // the exact path's own compaction (no forced failure there)
+    std::vector<uint64_t> row_passes_;
+    uint32_t level0_bits() const { return force_deep_ ? 6u : static_cast<uint32_t>(msd_max_bits_); }
     bool no_fused_ = false;
     bool no_dense_ = false;
     int sparse_max_ = 96;            // RTK_SPARSE_MAX (k_compact sparse-hit path threshold)

@@ -682,6 +682,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
                         const unsigned long long K = (static_cast<unsigned long long>(v[u][i]) << 32) | (nidx0 - l);
                         mn = min(mn, K);
                         mx = max(mx, K);
+                        ko |= v[u][i] ^ thi;  // same per-row OR as warp_flush (plan_row's tz)
                         if (base < ccap) cand[coff + base] = K;
                         ++base;
                     }
@@ -880,12 +881,11 @@ void launch_sample_select(int rows, int cs, uint32_t per_cta, const SampleRows& 
     // double buffer (per_cta <= 8192) + 4 sub-histograms
     const size_t smem = 2 * 8192 * sizeof(unsigned long long) + 4 * kBins * sizeof(uint32_t);
     (void)per_cta;
-    static bool configured = false;
-    if (!configured) {
+    static DeviceOnce configured;
+    configured([&] {
         cudaFuncSetAttribute(k_sample_select, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         cudaFuncSetAttribute(k_sample_select, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        configured = true;
-    }
+    });
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(rows * cs);
     cfg.blockDim = dim3(1024);

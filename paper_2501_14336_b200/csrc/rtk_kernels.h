@@ -1,5 +1,6 @@
 // rtk_kernels.h — host-visible launchers of the sm_100a kernels (rtk_kernels.cu).
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -212,6 +213,7 @@ struct PlanArgs {         // per-row plan after the compaction (fused into k_com
     uint32_t* dyn_ctr;       // [2] dynamic-tail tile counter + CTAs done (self-resetting); null = static
     uint32_t dyn_per_cta;    // dynamic-tail tiles per CTA of the grid
     uint32_t contig;         // 1: contiguous tile runs per CTA (many-row batches), 0: interleaved
+    uint32_t force_fail;     // test switch "force_exact": every row takes the exact path
 };
 
 struct SortArgs {
@@ -234,15 +236,33 @@ struct SortArgs {
     CallTail tail;           // completion signal + self-cleaning (see CallTail)
 };
 
-inline int num_sms() {
-    static int sms = 0;
-    if (!sms) {
+// One-time setup per DEVICE (kernel attributes such as the dynamic shared-memory limit are
+// per device, and handles may live on any device of the process). Idempotent work only: two
+// threads racing on the first call may both run it.
+struct DeviceOnce {
+    std::atomic<uint64_t> done{0};
+    template <typename F>
+    void operator()(F&& f) {
         int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+        const uint64_t bit = uint64_t(1) << (dev & 63);
+        if (done.load(std::memory_order_acquire) & bit) return;
+        f();
+        done.fetch_or(bit, std::memory_order_release);
     }
-    return sms;
+};
+
+inline int num_sms() {
+    static std::atomic<int> sms[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int v = sms[dev & 63].load(std::memory_order_relaxed);
+    if (!v) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 148;
+        sms[dev & 63].store(v, std::memory_order_relaxed);
+    }
+    return v;
 }
 
 template <typename K>

@@ -337,16 +337,15 @@ void launch_lsd(uint64_t tiles, const LsdArgs& a, cudaStream_t s) {
         const uint32_t sh = a.shift0 + 8 * p;
         const bool first = p == 0, last = p + 1 == a.npass;
         constexpr size_t sm = kLsdTile * sizeof(unsigned long long);
-        static bool configured = false;
-        if (!configured) {
+        static DeviceOnce configured;
+        configured([&] {
             cudaFuncSetAttribute(k_lsd_pass<0, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
             cudaFuncSetAttribute(k_lsd_pass<8, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
             cudaFuncSetAttribute(k_lsd_pass<16, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
             cudaFuncSetAttribute(k_lsd_pass<16, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
             cudaFuncSetAttribute(k_lsd_pass<24, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
             cudaFuncSetAttribute(k_lsd_pass<24, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-            configured = true;
-        }
+        });
         if (sh == 0) k_lsd_pass<0, true, false><<<g, kLsdThreads, sm, s>>>(b, p);
         else if (sh == 8) k_lsd_pass<8, false, false><<<g, kLsdThreads, sm, s>>>(b, p);
         else if (sh == 16 && first) k_lsd_pass<16, true, false><<<g, kLsdThreads, sm, s>>>(b, p);

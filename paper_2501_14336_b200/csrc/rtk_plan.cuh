@@ -11,7 +11,7 @@ namespace rtk_b200 {
 __device__ __forceinline__ void plan_row(int j, uint32_t r, const PlanArgs& pa, uint64_t n) {
     const uint64_t m = __ldcg(pa.count + r);
     SegSlot sl{pa.cand_off[r], 0, 0, r, 0, 0, 0};
-    if (m < pa.row_k[r] || m > pa.cap[r]) {
+    if (m < pa.row_k[r] || m > pa.cap[r] || pa.force_fail) {
         pa.row_fail[r] = 1;
         atomicOr(pa.flags, kFlagFail);
     } else if (m <= kSortCap) {

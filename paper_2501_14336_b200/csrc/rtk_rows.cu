@@ -720,12 +720,11 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
 template <int KM, int CAND, int STAGES, int SAMPLE, int UU>
 static void rows_km(int R, const RowsFusedArgs& a, cudaStream_t s) {
     constexpr size_t smem = CAND * sizeof(unsigned long long) + STAGES * UU * kRowChunk * sizeof(uint32_t);
-    static bool configured = false;
-    if (!configured) {
+    static DeviceOnce configured;
+    configured([&] {
         cudaFuncSetAttribute(k_rows_fused<KM, CAND, STAGES, SAMPLE, UU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-        configured = true;
-    }
+    });
     k_rows_fused<KM, CAND, STAGES, SAMPLE, UU><<<R, kRowThreads, smem, s>>>(a);
 }
 

@@ -930,18 +930,20 @@ static size_t msd_smem(int cs) {
 }
 
 static void msd_configure() {
-    static bool configured = false;
-    if (!configured) {
+    static DeviceOnce configured;
+    configured([&] {
         cudaFuncSetAttribute(k_msd_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         cudaFuncSetAttribute(k_msd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        configured = true;
-    }
+    });
 }
 
 int msd_max_clusters(int cs) {
-    static int cache[17] = {0};
+    static std::atomic<int> cache_all[64][17];  // per device
     if (cs < 1 || cs > 16) return 1;
-    if (!cache[cs]) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::atomic<int>* cache = cache_all[dev & 63];
+    if (!cache[cs].load()) {
         msd_configure();
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(cs);
@@ -959,9 +961,9 @@ int msd_max_clusters(int cs) {
             cudaGetLastError();
             n = 1;
         }
-        cache[cs] = n > 0 ? n : 1;
+        cache[cs].store(n > 0 ? n : 1);
     }
-    return cache[cs];
+    return cache[cs].load();
 }
 
 bool launch_msd_cluster(int nslots, int cs, const SegSlot* slots, const uint64_t* src, uint64_t* dst,
@@ -1000,11 +1002,10 @@ bool launch_msd_cluster(int nslots, int cs, const SegSlot* slots, const uint64_t
 void launch_sort_groups(uint32_t max_groups, const SortArgs& g, cudaStream_t s) {
     if (max_groups == 0) return;
     constexpr size_t smem = kSortCap * sizeof(unsigned long long);
-    static bool configured = false;
-    if (!configured) {
+    static DeviceOnce configured;
+    configured([&] {
         cudaFuncSetAttribute(k_sort_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured = true;
-    }
+    });
     const int grid = persistent_grid(k_sort_groups, kSortThreads, smem, max_groups);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);

@@ -154,6 +154,7 @@ class Instrumentation:
     kernel_launches: int = 0
     compact_ms: float = 0.0
     total_ms: float = 0.0
+    deep_levels: int = 0
 
 
 class TopKResult:
@@ -197,7 +198,12 @@ def last_stats(device: int = 0) -> Instrumentation:
     st = L.rtk_stats()
     _raise(L.load().rtk_get_stats(_handle(device), C.byref(st)))
     return Instrumentation(st.passes, st.elements_scanned, st.candidates, st.fallback_rows,
-                           st.kernel_launches, st.compact_ms, st.total_ms)
+                           st.kernel_launches, st.compact_ms, st.total_ms, st.deep_levels)
+
+
+def set_option(name: str, value: int, device: int = 0) -> None:
+    """rtk_set_option: test switches of the device's handle ("force_exact", "force_deep")."""
+    _raise(L.load().rtk_set_option(_handle(device), name.encode(), int(value)), "rtk_set_option")
 
 
 def set_timing(on: bool, device: int = 0) -> None:
@@ -295,13 +301,15 @@ def _dtype_code(x) -> int:
         import torch
         if x.dtype == torch.float32:
             return 0
-        if x.dtype in (torch.uint32, torch.int32):
+        if x.dtype == torch.uint32:
             return 1
         if x.dtype == torch.float16:
             return 2
         if x.dtype == torch.bfloat16:
             return 3
-        raise TypeError(f"unsupported dtype {x.dtype}")
+        # the reference defines float and uint32 keys only (keycodec.hpp:55-81): signed int32
+        # would rank negative values above positive ones under the u32 codec, so it is refused
+        raise TypeError(f"unsupported dtype {x.dtype} (float32, uint32, float16, bfloat16)")
     a = np.asarray(x)
     if a.dtype == np.float32:
         return 0
@@ -460,9 +468,13 @@ def batch_topk(batch: BatchInput, order: SelectionOrder = SelectionOrder.Largest
         vs, ix = np.split(vals, cut), np.split(idx, cut)
         pl = list(pivs[:B])
     out = [TopKResult(vs[t], ix[t], pl[t]) for t in range(B)]
-    if info is not None:
-        info.task_passes = [1] * B
-        info.phase_b_rounds = 0
+    if info is not None:  # BatchRunInfo (batch.hpp:138-141) as measured by the engine
+        dev = (batch.data.device.index or 0) if _is_cuda(batch.data) else 0
+        tp, p_tp = _arr64(np.zeros(max(B, 1), dtype=np.uint64))
+        rounds = C.c_uint64()
+        _raise(lib.rtk_get_batch_info(_handle(dev), p_tp, B, C.byref(rounds)), "rtk_get_batch_info")
+        info.task_passes = [int(v) for v in tp[:B]]
+        info.phase_b_rounds = int(rounds.value)
     return out
 
 

@@ -475,15 +475,6 @@ def test_topk_sample_errors(cuda):
         rtk.topk_sample(x, 101)
 
 
-@pytest.mark.parametrize("k", [256, 1])
-def test_c2_full_size_small_k(cuda, k):
-    # BASELINE C2 at full size, n = 2^28 U[0,1), small k (C2's k = 2^8 and the extreme k = 1),
-    # bit-exact against the reference engine compiled in place (oracle/_ref)
-    x = O.ref_generate(UNIFORM, 1 << 28, 1)
-    assert_same(gpu_topk(x, k, 0, cuda), O.ref_topk(x, k, 0, grid=8), f"C2 k={k}")
-
-
-
 @pytest.mark.parametrize("mode", ["all", "off", "16"])
 def test_dense_rows_lsd_forced(cuda, mode):
     # dense rows (k >= n/2): the segmented one-sweep LSD sort (default, RTK_LSD=all), the MSD +
