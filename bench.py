@@ -1,22 +1,32 @@
 #!/usr/bin/env python3
 """bench.py — B200 radix top-k benchmark (contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1], the headline): ONE fp32 query, n = 2^28 Uniform[0,1)
-elements resident in HBM per GPU, k = 2^20 (largest), values + u64 indices in the reference's
-canonical order. The metric is the paper/north-star "effective GB/s" = algorithmic bytes
-(4n + 12k per query: read every key once, write k values + k u64 indices) / time.
+Headline (N = 1, BASELINE.json configs[1]): ONE fp32 query, n = 2^28 Uniform[0,1) elements
+resident in HBM, k = 2^20 (largest), values + u64 indices in the reference's canonical order.
+Metric: the north-star "effective GB/s" = algorithmic bytes (4n + 12k per query: every key read
+once, k values + k u64 indices written) / time.
 
-* value     device-resident input, CUDA events on the launching stream around rtk_topk.
-* e2e       the same metric through the host entry point rtk_topk_host (pinned host input,
-            H2D of the 1 GiB input and D2H of the result inside the timed region).
-* roofline  the dominant kernel (k_compact, the single streaming pass) timed with CUDA events
-            inside the library on its stream; algorithmic bytes per launch = 4n.
-* cpu_baseline  the reference's own CPU engine (oracle/_ref: rtk::topk compiled from the
-            reference headers) on this box's host cores, on a bounded sample.
+* value         median device time of back-to-back rtk_topk calls issued from C
+                (rtk_bench_topk: CUDA events the engine records on the launching stream around
+                its device work); the input (1 GiB) is larger than L2.
+* host_ms       the same calls' host wall time (C steady_clock around each rtk_topk, which
+                returns after the device's completion signal).
+* e2e           the same metric through the host entry point rtk_topk_host: the 1 GiB H2D copy
+                from pinned memory and the D2H of the result inside the timed region.
+* roofline      the dominant kernel (k_compact, the single streaming pass) timed with CUDA
+                events on its stream; algorithmic bytes per launch = 4n.
+* cpu_baseline  the reference's own engine (rtk::topk from its headers, oracle/_ref) on this
+                box's host cores, on the SAME input and config (n = 2^28, k = 2^20).
+* legs          C1 (n = 2^20, k = 256, L2 flushed), the k sweep of C2, C3 (256 x 128256 logits,
+                f32 and bf16, L2 flushed), C4 (n = 2^26 adversarial, scale off/always/adaptive),
+                the C5 shard shape (2^29 Philox elements, k = 2^16) — each with the reference
+                engine timed on the same input where it runs in bounded time.
 
-Multi-GPU (torchrun, N>1): weak scaling of the same query shape — each rank owns a 2^28 shard
-of one N*2^28-element query, runs the local top-k, the k candidates are all-gathered over NCCL
-and merged with rtk_merge_shards. Time = max over ranks.
+Multi-GPU (N > 1; `--gpus N` re-launches itself under torch.distributed.run when WORLD_SIZE is
+unset): BASELINE configs[4] (C5) — one query of N * 2^29 fp32 elements (n = 2^32 at N = 8), each
+rank generating its shard on its device (Philox, rtk_generate_philox), k = 2^16; per step
+rtk_topk_sharded: local top-k + ncclAllGather of the candidates + final select on every rank.
+Weak scaling; time = max over ranks of the median step.
 
 --impl reference: the reference CPU engine (oracle/_ref) on the host cores, same metric.
 """
@@ -25,6 +35,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,6 +46,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0
+METRIC = "topk_effective_GBps"
+C5_SEED = 5
 
 
 def measured_peak():
@@ -42,7 +55,18 @@ def measured_peak():
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"]), "measured"
     except Exception:
-        return HBM_FALLBACK_GBS, "fallback"
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -93,292 +117,429 @@ class ClockSampler:
                 "samples": len(self.sm)}
 
 
-def cpu_reference_leg(n: int, k: int, reps: int, seed: int = 1):
-    """Time the reference's CPU engine (oracle/_ref) on the host cores: effective GB/s."""
-    import numpy as np
-    import oracle as O
-    cores = os.cpu_count() or 1
-    x = np.random.default_rng(seed).random(n, dtype=np.float32)
-    times = []
+def gbs(n_elem_bytes: float, k: int, ms: float) -> float:
+    return (n_elem_bytes + 12 * k) / (ms * 1e-3) / 1e9
+
+
+# ---- the reference CPU engine (oracle/_ref), timed on the host cores -------------------------
+def _timed(fn, reps):
+    ts = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        O.ref_topk(x, k, 0, 12, cores)
-        times.append(time.perf_counter() - t0)
-    t = statistics.median(times)
-    return (4 * n + 12 * k) / t / 1e9, cores, t
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts), ts
 
 
+def cpu_topk(x, k, reps, cores):
+    import oracle as O
+    t, _ = _timed(lambda: O.ref_topk(x, k, 0, 12, cores), reps)
+    return t
+
+
+def host_inputs(n, k):
+    """The headline query on the host: numpy's PCG64 (seed 1) Uniform[0,1) fp32 — the same array
+    is uploaded for the GPU arm and handed to the reference engine."""
+    import numpy as np
+    return np.random.default_rng(1).random(n, dtype=np.float32)
+
+
+def reference_arm(args, world, rank):
+    """bench.py --impl reference: rtk::topk (the reference engine compiled from its headers) on the
+    host cores, on this arm's workload. N = 1: the full C2 query (n = 2^28, k = 2^20), one call per
+    step. N > 1: the query is N * 2^29 elements (C5), beyond host memory for the reference's four
+    copies; each step runs a 2^28-element prefix sample with k scaled by the sample fraction."""
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    if world == 1:
+        n, k = 1 << args.logn, args.k
+        ns, ks = n, k
+        sample = f"the full query: n=2^{args.logn} PCG64(1) U[0,1) k={k}, rtk::topk grid_size={cores}, one call per step"
+        config = headline_config(args, 1)
+    else:
+        n, k = world * (1 << args.shard_logn), args.shard_k
+        ns = 1 << 28
+        ks = max(1, k * ns // n)
+        sample = (f"the first 2^28 elements (Philox seed {C5_SEED}) of the {world}x2^{args.shard_logn} query, k "
+                  f"scaled to {ks}, rtk::topk grid_size={cores}, one call per step (the full query exceeds host "
+                  "memory for the reference's copies)")
+        config = c5_config(args, world)
+    if world == 1:
+        x = host_inputs(ns, ks)
+    else:
+        import oracle as O
+        x = O.philox_fill(C5_SEED, 0, ns)
+    for _ in range(args.warmup):
+        cpu_topk(x, ks, 1, cores)
+    vals = []
+    for _ in range(args.steps):
+        t = cpu_topk(x, ks, 1, cores)
+        vals.append(gbs(4 * ns, ks, t * 1e3))
+    v = statistics.median(vals)
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": (4 * ns + 12 * ks) / v / 1e6,
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                      "data": "synthetic", "config": config,
+                      "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "reference",
+                                       "cpu_model": cpu_model(), "sample": sample},
+                      "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def headline_config(args, world):
+    n = 1 << args.logn
+    return {"workload": f"C2: single query fp32 Uniform[0,1) n=2^{args.logn}, k={args.k}, largest, values+u64 "
+                        "indices, sorted (BASELINE configs[1])",
+            "n": n, "k": args.k, "dtype": "f32", "order": "largest",
+            "l2": "input 1 GiB > 126 MB L2 (no flush needed)", "parallelism": "single"}
+
+
+def c5_config(args, world):
+    ns = 1 << args.shard_logn
+    return {"workload": f"C5: single huge query fp32 Uniform[0,1) n={world}x2^{args.shard_logn}"
+                        f"{' = 2^32' if world * ns == 1 << 32 else ''}, k={args.shard_k}, largest, sharded by index "
+                        "range: local top-k + NCCL allgather + final select (BASELINE configs[4])",
+            "n": world * ns, "n_per_gpu": ns, "k": args.shard_k, "dtype": "f32", "order": "largest",
+            "generator": f"Philox4x32-10 seed {C5_SEED} on each rank's device (rtk_generate_philox)",
+            "l2": "input 2 GiB per GPU > L2 (no flush needed)", "parallelism": f"n-sharded x{world} (NCCL)"}
+
+
+# ---- self-launch for --gpus N ------------------------------------------------------------------
+def self_launch(args) -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+# ---- the GPU arm --------------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--logn", type=int, default=28)
     ap.add_argument("--k", type=int, default=1 << 20)
-    ap.add_argument("--sweep", type=str, default="256,16384", help="extra k values (device value only)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--shard-logn", type=int, default=29, help="C5: elements per GPU (2^x)")
+    ap.add_argument("--shard-k", type=int, default=1 << 16, help="C5: k")
+    ap.add_argument("--sweep", type=str, default="256,16384", help="extra C2 k values")
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--batch-ks", type=str, default="50,4096,128256",
-                    help="C3 batched LLM-vocab top-k: k values measured into batch_llm (empty = skip)")
+    ap.add_argument("--legs", type=str, default="c1,c3,c4,c5", help="secondary legs (N = 1)")
+    ap.add_argument("--batch-ks", type=str, default="50,4096,128256")
     ap.add_argument("--batch-rows", type=int, default=256)
-    ap.add_argument("--c4", type=int, default=1, help="C4 adversarial scaled_topk leg (1 = on)")
     ap.add_argument("--vocab", type=int, default=128256)
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "reference":  # rank 0's work only: no ranks to launch
+            os.environ.update(WORLD_SIZE=str(args.gpus), RANK="0")
+        else:
+            sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    n, k = 1 << args.logn, args.k
-    metric = "topk_effective_GBps"
-    config = {"workload": f"single query fp32 Uniform[0,1) n=2^{args.logn} per GPU, k={k}, largest, "
-                          "values+u64 indices, sorted (BASELINE configs[1])",
-              "n_per_gpu": n, "k": k, "dtype": "f32", "order": "largest",
-              "l2": "input 1 GiB per GPU > 126 MB L2 (no flush needed)",
-              "parallelism": f"n-sharded x{world}: local top-k + NCCL allgather + merge" if world > 1 else "single"}
-
     if args.impl == "reference":
-        if rank != 0:
-            return
-        # bounded sample of the same workload per step: n_s = 2^26, k scaled by n_s / n
-        ns = min(n, 1 << 26)
-        ks = max(1, k * ns // n)
-        for _ in range(args.warmup):
-            cpu_reference_leg(ns, ks, 1)
-        vals = [cpu_reference_leg(ns, ks, 1)[0] for _ in range(args.steps)]
-        gbs = statistics.median(vals)
-        cores = os.cpu_count() or 1
-        sample = f"n=2^{ns.bit_length() - 1} U[0,1) k={ks} per step (k scaled by n_s/n), rtk::topk grid_size={cores}"
-        print(json.dumps({"impl": "reference", "metric": metric, "value": gbs, "unit": "GB/s",
-                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                          "higher_is_better": True, "dtype": "f32", "data": "synthetic",
-                          "config": config,
-                          "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
-                                           "sample": sample},
-                          "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0,
-                                  "d2h_bytes_per_step": 0}}))
+        reference_arm(args, world, rank)
         return
+    if world > 1:
+        multi_gpu(args, rank, world, local)
+    else:
+        single_gpu(args)
 
+
+def single_gpu(args):
+    import numpy as np
     import torch
+
     import paper_2501_14336_b200 as rtk
     from paper_2501_14336_b200 import rtk as R
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1 + rank)
-    x = torch.rand(n, device=dev, dtype=torch.float32, generator=gen)
-    stream = torch.cuda.current_stream(dev)
-
-    def step(kk):
-        r = rtk.topk(x, kk)
-        if world > 1:
-            import torch.distributed as dist
-            vals = torch.empty(world * kk, dtype=torch.float32, device=dev)
-            idx = torch.empty(world * kk, dtype=torch.int64, device=dev)
-            dist.all_gather_into_tensor(vals, r.values)
-            dist.all_gather_into_tensor(idx, r.indices)
-            r = rtk.merge_shards(vals, idx, [kk] * world, [g * n for g in range(world)], kk)
-        return r
-
-    def python_loop(kk, steps, warmup):
-        for _ in range(warmup):
-            step(kk)
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-        for a, b in ev:
-            a.record(stream)
-            step(kk)
-            b.record(stream)
-        torch.cuda.synchronize()
-        return [a.elapsed_time(b) for a, b in ev]
-
-    def timed(kk, steps, warmup):
-        if world == 1:
-            # steps issued from C through rtk_topk (the drop-in boundary; the reference's call
-            # sites are C++ loops over rtk::topk), CUDA events per step on the stream
-            torch.cuda.synchronize()
-            _, ms = R.bench_topk(x, kk, steps, warmup)
-        else:
-            ms = python_loop(kk, steps, warmup)
-        # kernel share: k_compact bracketed by CUDA events on its stream (library timing mode:
-        # no graph replay), on separate steps so no stats readback sits inside the timed region
-        # (on the local top-k call: with N > 1 the merge that follows is a separate small call)
-        R.set_timing(True, local)
-        comp = []
-        per_step = 0
-        for _ in range(min(steps, 10)):
-            rtk.topk(x, kk)
-            st = R.last_stats(local)
-            comp.append(st.compact_ms)
-            per_step = st.kernel_launches
-        R.set_timing(False, local)
-        if world > 1:  # + the merge of the gathered candidates (rtk_merge_shards)
-            step(kk)
-            per_step += R.last_stats(local).kernel_launches
-        launches = per_step * steps
-        if world > 1:
-            t = torch.tensor([statistics.mean(ms)], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            mean_ms = float(t.item())
-        else:
-            mean_ms = statistics.mean(ms)
-        return mean_ms, ms, comp, launches
-
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    n, k = 1 << args.logn, args.k
+    legs = set(v for v in args.legs.split(",") if v)
     peak, peak_kind = measured_peak()
-    with ClockSampler(local) as clk:
-        mean_ms, ms, comp, launches = timed(k, args.steps, args.warmup)
+    cores = os.cpu_count() or 1
+    do_cpu = not args.no_cpu_baseline
+    hx = host_inputs(n, k)
+    x = torch.from_numpy(hx).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
+    launches_before = 0
+
+    # ---- headline: C2 k = 2^20 ---------------------------------------------------------------
+    with ClockSampler(0) as clk:
+        b = R.bench_topk(x, k, args.steps, args.warmup)
     clocks = clk.summary()
-    py_ms = statistics.mean(python_loop(k, max(5, args.steps // 2), 2)) if world == 1 else None
-    total_bytes = world * (4 * n) + 12 * k
-    value = total_bytes / (mean_ms * 1e-3) / 1e9
+    med = b.median_ms
+    value = gbs(4 * n, k, med)
+    # kernel share: k_compact bracketed by CUDA events on its stream (library timing mode: no graph
+    # replay), on separate calls so no stats readback sits inside the timed region
+    R.set_timing(True)
+    comp, per_step = [], 0
+    for _ in range(10):
+        rtk.topk(x, k)
+        st = R.last_stats()
+        comp.append(st.compact_ms)
+        per_step = st.kernel_launches
+    R.set_timing(False)
+    comp_ms = statistics.median(comp)
+    achieved = 4 * n / (comp_ms * 1e-3) / 1e9
+    launches = per_step * args.steps
 
     sweep = {}
     for kk in [int(v) for v in args.sweep.split(",") if v]:
-        m2, _, c2, _ = timed(kk, max(5, args.steps // 2), 2)
-        sweep[str(kk)] = {"ms_per_step": m2, "GBps": (world * 4 * n + 12 * kk) / (m2 * 1e-3) / 1e9,
-                          "compact_ms": statistics.mean(c2)}
+        bk = R.bench_topk(x, kk, max(5, args.steps // 2), 3)
+        sweep[str(kk)] = {"ms": bk.median_ms, "host_ms": bk.median_host_ms, "GBps": gbs(4 * n, kk, bk.median_ms),
+                          "fraction_of_hbm_peak": gbs(4 * n, kk, bk.median_ms) / peak}
 
-    comp_ms = statistics.mean(comp)
-    achieved = 4 * n / (comp_ms * 1e-3) / 1e9
-
-    # C4: adversarial distribution (one first-pass bin, ~6.5K distinct values => heavy ties),
-    # scaled_topk with the reference's three scale policies (scaling.hpp:42-86)
-    adversarial = {}
-    if args.c4 and rank == 0:
-        na, ka = 1 << 26, 1 << 16
-        xa = (128.6 + 0.1 * torch.rand(na, device=dev, generator=gen)).float()
-        for name, mode in (("off", 0), ("always", 1), ("adaptive", 2)):
-            pol = R.ScalePolicy(mode=R.ScaleMode(mode), trigger_fraction=0.5, seed=31)
-            # steps issued from C (rtk_bench_scaled): events before the scale decision's kernels
-            # and after the call's last device operation, as for the C2 value
-            ms_a, _ = R.bench_scaled(xa, ka, max(5, args.steps // 2), 3, policy=pol)
-            adversarial[name] = {"ms": ms_a, "GBps": (4 * na + 12 * ka) / (ms_a * 1e-3) / 1e9,
-                                 "fraction_of_hbm_peak": (4 * na + 12 * ka) / (ms_a * 1e-3) / 1e9 / peak}
-        del xa
-
-    # C3: batched LLM sampling top-k, rows sharded across ranks (no collective)
-    batch_llm, batch_bf16, sampling = {}, {}, {}
-    if args.batch_ks:
-        from paper_2501_14336_b200 import sharded as SH
-        r0, r1 = SH.row_shard(args.batch_rows, world, rank)
-        rows_here = r1 - r0
-        V = args.vocab
-        logits = torch.randn(rows_here, V, device=dev, generator=gen)
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2: flush between steps
-        for kb in [int(v) for v in args.batch_ks.split(",") if v]:
-            kb = min(kb, V)
-            # steps issued from C (rtk_bench_batched), L2 flushed between steps outside the events
-            torch.cuda.synchronize()
-            ms_b, _ = R.bench_batch_dense(logits, kb, max(5, args.steps // 2), 3, flush)
-            if world > 1:
-                t = torch.tensor([ms_b], device=dev)
-                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-                ms_b = float(t.item())
-            q = args.batch_rows / (ms_b * 1e-3)
-            byts = args.batch_rows * (4 * V + 12 * kb)
-            batch_llm[str(kb)] = {"ms_per_batch": ms_b, "queries_per_s": q, "effective_GBps": byts / (ms_b * 1e-3) / 1e9,
-                                  "fraction_of_hbm_peak": byts / (ms_b * 1e-3) / 1e9 / peak}
-        # the same batches with bf16 logits (16-bit keys, SURVEY §8f): half the bytes per element
-        batch_bf16 = {}
-        lb = logits.to(torch.bfloat16)
-        for kb in [int(v) for v in args.batch_ks.split(",") if v]:
-            kb = min(kb, V)
-            torch.cuda.synchronize()
-            ms_h, _ = R.bench_batch_dense(lb, kb, max(5, args.steps // 2), 3, flush)
-            byts = args.batch_rows * (2 * V + 10 * kb)
-            batch_bf16[str(kb)] = {"ms_per_batch": ms_h, "queries_per_s": args.batch_rows / (ms_h * 1e-3),
-                                   "effective_GBps": byts / (ms_h * 1e-3) / 1e9,
-                                   "fraction_of_hbm_peak": byts / (ms_h * 1e-3) / 1e9 / peak}
-        # LLM sampling consumer (SURVEY §8f row 2): top-k 50 -> softmax -> top-p 0.9 -> one draw per
-        # row, through rtk.topk_sample (Python loop, torch events, L2 flushed outside the events)
-        sampling = {}
-        u = torch.rand(rows_here, device=dev, generator=gen)
-        for kb, tp in ((50, 0.9), (4096, 0.95)):
-            ev = []
-            for it in range(3 + max(5, args.steps // 2)):
-                flush.zero_()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                R.topk_sample(logits, kb, top_p=tp, temperature=1.0, uniform=u)
-                e1.record()
-                if it >= 3:
-                    ev.append((e0, e1))
-            torch.cuda.synchronize()
-            ms_s = statistics.median(a.elapsed_time(b) for a, b in ev)
-            sampling[f"k{kb}_p{tp}"] = {"ms_per_batch": ms_s, "queries_per_s": args.batch_rows / (ms_s * 1e-3)}
-        del logits, flush, lb
-
-    # e2e through the host entry point (rank 0 / N=1 semantics: per-GPU query from pinned host)
-    e2e = None
-    if rank == 0:
-        hx = x.cpu().pin_memory()
-        hv = hx.numpy()
-        R.topk(hv, k)
-        t_e2e = []
-        for _ in range(args.e2e_steps):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            R.topk(hv, k)
-            t_e2e.append(time.perf_counter() - t0)
-        te = statistics.median(t_e2e)
-        e2e = {"value": (4 * n + 12 * k) / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
-               "d2h_bytes_per_step": 12 * k + 4, "ms_per_step": te * 1e3}
+    # ---- e2e through the host entry point (pinned host input, copies inside) ------------------
+    hp = torch.from_numpy(hx).pin_memory().numpy()
+    R.topk(hp, k)
+    t_e2e = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        R.topk(hp, k)
+        t_e2e.append(time.perf_counter() - t0)
+    te = statistics.median(t_e2e)
+    e2e = {"value": gbs(4 * n, k, te * 1e3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
+           "d2h_bytes_per_step": 12 * k + 4, "ms_per_step": te * 1e3, "entry": "rtk_topk_host"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ns = 1 << 26
-        ks = max(1, k * ns // n)
-        gbs, cores, t = cpu_reference_leg(ns, ks, 3)
-        cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
-               "sample": f"rtk::topk (reference engine, oracle/_ref) n=2^26 U[0,1) k={ks}, "
-                         f"grid_size={cores}, median of 3 ({t:.2f} s each)"}
+    if do_cpu:
+        t = cpu_topk(hx, k, 3, cores)
+        cpu = {"value": gbs(4 * n, k, t * 1e3), "unit": "GB/s", "cores": cores, "kind": "reference",
+               "cpu_model": cpu_model(), "ms": t * 1e3,
+               "sample": f"the same query and input (n=2^{args.logn}, k={k}): rtk::topk (oracle/_ref) "
+                         f"grid_size={cores}, median of 3"}
+    del hp
 
+    out_legs = {}
+    if "c1" in legs:
+        out_legs["c1"] = leg_c1(args, R, dev, flush, peak, cores, do_cpu)
+    if "c3" in legs:
+        out_legs["c3"] = leg_c3(args, R, dev, flush, peak, cores, do_cpu)
+    if "c4" in legs:
+        out_legs["c4"] = leg_c4(args, R, dev, peak, cores, do_cpu)
+    if "c5" in legs:
+        del x
+        torch.cuda.empty_cache()
+        out_legs["c5_shard_1gpu"] = leg_c5_1gpu(args, R, dev, peak)
+
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    traffic = None
+    try:
+        with open(prof) as f:
+            traffic = json.load(f).get(f"k_compact_n{n}")
+    except Exception:
+        pass
+    out = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": med, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic: numpy PCG64(1) Uniform[0,1) fp32 on the host, uploaded once",
+           "config": headline_config(args, 1),
+           "queries_per_s": 1e3 / med, "elements_per_s": n / (med * 1e-3), "fraction_of_hbm_peak": value / peak,
+           "host_ms_per_step": b.median_host_ms,
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "traffic": traffic, "kernel": "k_compact", "peak_kind": peak_kind,
+                        "kernel_ms": comp_ms, "kernel_share_of_step": comp_ms / med},
+           "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+           "timing": "median over steps of back-to-back rtk_topk calls issued from C (rtk_bench_topk): device "
+                     "time between CUDA events the engine records on the launching stream right before its "
+                     "first and after its last device operation of the call; host_ms = steady_clock around "
+                     "each rtk_topk call (returns after the device's completion signal)",
+           "step_ms_all": b.device_ms, "host_ms_all": b.host_ms,
+           "k_sweep": sweep, "legs": out_legs}
+    print(json.dumps(out))
+
+
+def leg_c1(args, R, dev, flush, peak, cores, do_cpu):
+    """C1 (BASELINE configs[0]): n = 2^20 Uniform[0,1), k = 256 — launch/latency-bound (4 MB);
+    L2 flushed before every step outside the clocks."""
+    import numpy as np
+    import torch
+    n, k = 1 << 20, 256
+    hx = np.random.default_rng(2).random(n, dtype=np.float32)
+    x = torch.from_numpy(hx).to(dev)
+    b = R.bench_topk(x, k, max(10, args.steps), 5, flush=flush)
+    leg = {"config": "n=2^20 PCG64(2) U[0,1) fp32, k=256, largest; L2 flushed before each step",
+           "ms": b.median_ms, "host_ms": b.median_host_ms, "GBps": gbs(4 * n, k, b.median_ms),
+           "fraction_of_hbm_peak": gbs(4 * n, k, b.median_ms) / peak, "queries_per_s": 1e3 / b.median_host_ms}
+    if do_cpu:
+        t = cpu_topk(hx, k, 5, cores)
+        leg["cpu_baseline"] = {"ms": t * 1e3, "GBps": gbs(4 * n, k, t * 1e3), "cores": cores, "kind": "reference",
+                               "sample": "same input, rtk::topk grid_size=cores, median of 5"}
+    return leg
+
+
+def leg_c3(args, R, dev, flush, peak, cores, do_cpu):
+    """C3 (BASELINE configs[2]): batched LLM-vocab top-k, 256 x 128256 N(0,1) fp32 logits (and the
+    same logits in bf16), k in {50, 4096, vocab}; L2 flushed before every step (the 131 MB batch
+    fits the 126 MB L2 almost entirely)."""
+    import numpy as np
+    import oracle as O
+    import torch
+    B, V = args.batch_rows, args.vocab
+    hl = np.random.default_rng(3).standard_normal((B, V), dtype=np.float32)
+    logits = torch.from_numpy(hl).to(dev)
+    lb = logits.to(torch.bfloat16)
+    res = {"config": f"{B} x {V} PCG64(3) N(0,1) fp32 logits (bf16: the same rounded); L2 flushed before "
+                     "each step", "f32": {}, "bf16": {}, "sampling": {}}
+    for kb in [min(int(v), V) for v in args.batch_ks.split(",") if v]:
+        b = R.bench_batch_dense(logits, kb, max(5, args.steps // 2), 3, flush)
+        byts = B * (4 * V + 12 * kb)
+        e = {"ms": b.median_ms, "host_ms": b.median_host_ms, "queries_per_s": B / (b.median_ms * 1e-3),
+             "effective_GBps": byts / (b.median_ms * 1e-3) / 1e9,
+             "fraction_of_hbm_peak": byts / (b.median_ms * 1e-3) / 1e9 / peak}
+        if do_cpu:
+            reps = 1 if kb > 8192 else 3
+            t, _ = _timed(lambda: O.ref_batch_topk(hl.reshape(-1), [i * V for i in range(B)], [V] * B, [kb] * B,
+                                                   0, 12, cores), reps)
+            e["cpu_baseline"] = {"ms": t * 1e3, "queries_per_s": B / t, "cores": cores, "kind": "reference",
+                                 "sample": f"same logits, rtk::batch_topk grid_size=cores, median of {reps}"}
+        res["f32"][str(kb)] = e
+        bh = R.bench_batch_dense(lb, kb, max(5, args.steps // 2), 3, flush)
+        byts = B * (2 * V + 10 * kb)
+        res["bf16"][str(kb)] = {"ms": bh.median_ms, "host_ms": bh.median_host_ms,
+                                "queries_per_s": B / (bh.median_ms * 1e-3),
+                                "effective_GBps": byts / (bh.median_ms * 1e-3) / 1e9,
+                                "fraction_of_hbm_peak": byts / (bh.median_ms * 1e-3) / 1e9 / peak}
+    # LLM sampling consumer (SURVEY §8f row 2): top-k -> softmax -> top-p -> one draw per row
+    u = torch.rand(B, device=dev, generator=torch.Generator(device=dev).manual_seed(4))
+    for kb, tp in ((50, 0.9), (4096, 0.95)):
+        ev = []
+        for it in range(3 + max(5, args.steps // 2)):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            R.topk_sample(logits, kb, top_p=tp, temperature=1.0, uniform=u)
+            e1.record()
+            if it >= 3:
+                ev.append((e0, e1))
+        torch.cuda.synchronize()
+        ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+        res["sampling"][f"k{kb}_p{tp}"] = {"ms": ms, "rows_per_s": B / (ms * 1e-3)}
+    return res
+
+
+def leg_c4(args, R, dev, peak, cores, do_cpu):
+    """C4 (BASELINE configs[3]): n = 2^26 Uniform[128.6, 128.7) fp32 (one first-window bin, heavy
+    ties), k = 2^16, scaled_topk Off / Always / Adaptive (tau 0.5, seed 31)."""
+    import numpy as np
+    import oracle as O
+    import torch
+    n, k = 1 << 26, 1 << 16
+    hx = (np.float32(128.6) + np.float32(0.1) * np.random.default_rng(5).random(n, dtype=np.float32)).astype(np.float32)
+    x = torch.from_numpy(hx).to(dev)
+    res = {"config": "n=2^26 128.6 + 0.1 * PCG64(5) U[0,1) fp32, k=2^16, largest, scaled_topk tau=0.5 seed=31; "
+                     "input 256 MB > L2"}
+    for name, mode in (("off", 0), ("always", 1), ("adaptive", 2)):
+        pol = R.ScalePolicy(mode=R.ScaleMode(mode), trigger_fraction=0.5, seed=31)
+        b = R.bench_scaled(x, k, max(5, args.steps // 2), 3, policy=pol)
+        e = {"ms": b.median_ms, "host_ms": b.median_host_ms, "GBps": gbs(4 * n, k, b.median_ms),
+             "fraction_of_hbm_peak": gbs(4 * n, k, b.median_ms) / peak}
+        if do_cpu:
+            t, _ = _timed(lambda: O.ref_scaled_topk(hx, k, 0, 12, mode, 0.5, 31, cores), 1)
+            e["cpu_baseline"] = {"ms": t * 1e3, "GBps": gbs(4 * n, k, t * 1e3), "cores": cores, "kind": "reference",
+                                 "sample": "same input, rtk::scaled_topk grid_size=cores, one call"}
+        res[name] = e
+    return res
+
+
+def leg_c5_1gpu(args, R, dev, peak):
+    """The C5 shard shape on one GPU (2^29 Philox elements, k = 2^16): the per-GPU baseline the
+    N > 1 runs scale from."""
+    ns, k = 1 << args.shard_logn, args.shard_k
+    x = R.generate_philox(ns, C5_SEED, 0, device=dev)
+    b = R.bench_topk(x, k, max(5, args.steps // 2), 3)
+    return {"config": f"n=2^{args.shard_logn} Philox seed {C5_SEED} elements [0, 2^{args.shard_logn}), k={k}",
+            "ms": b.median_ms, "host_ms": b.median_host_ms, "GBps": gbs(4 * ns, k, b.median_ms),
+            "fraction_of_hbm_peak": gbs(4 * ns, k, b.median_ms) / peak}
+
+
+def multi_gpu(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_14336_b200 as rtk
+    from paper_2501_14336_b200 import rtk as R
+    from paper_2501_14336_b200 import sharded as SH
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    peak, peak_kind = measured_peak()
+    ns, k = 1 << args.shard_logn, args.shard_k
+    n = world * ns
+    x = R.generate_philox(ns, C5_SEED, rank * ns, device=dev)
+    comm = SH.NcclComm(rank, world, local)
+    lens = [ns] * world
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return SH.topk_sharded(x, k, lens, comm)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for a, b in ev:
+            a.record(stream)
+            step()
+            b.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([statistics.median(ms)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    med = float(t.item())
+    per_step = rtk.last_stats(local).kernel_launches  # the merge call's; + the local call's below
+    rtk.topk(x, k)
+    per_step += rtk.last_stats(local).kernel_launches
+
+    # e2e: this rank's shard from pinned host memory, the sharded call, the result back to the host
+    hx = x.cpu().pin_memory()
+    xd = torch.empty_like(x)
+    te = []
+    for i in range(args.e2e_steps + 1):
+        dist.barrier()
+        t0 = time.perf_counter()
+        xd.copy_(hx, non_blocking=True)
+        r = SH.topk_sharded(xd, k, lens, comm)
+        vals, idx = r.values.cpu(), r.indices.cpu()
+        if i:
+            te.append(time.perf_counter() - t0)
+    tt = torch.tensor([statistics.median(te)], device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    te_s = float(tt.item())
     if rank == 0:
-        prof = os.path.join(ROOT, "profiles", "traffic.json")
-        traffic = None
-        try:
-            with open(prof) as f:
-                traffic = json.load(f).get(f"k_compact_n{n}")
-        except Exception:
-            pass
-        out = {"metric": metric, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (torch.rand on device)",
-               "config": config,
-               "queries_per_s": world / (mean_ms * 1e-3) if world == 1 else 1 / (mean_ms * 1e-3),
-               "elements_per_s": world * n / (mean_ms * 1e-3),
-               "fraction_of_hbm_peak": value / peak,
-               "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                            "frac": achieved / peak, "traffic": traffic, "kernel": "k_compact",
-                            "peak_kind": peak_kind, "kernel_ms": comp_ms,
-                            "kernel_share_of_step": comp_ms / mean_ms},
-               "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-               "timing": "steps issued back-to-back from C through rtk_topk (rtk_bench_topk); per step two "
-                         "CUDA events the engine records on the launching stream right before its first and "
-                         "after its last device operation of the call (host planning and the host's wait for "
-                         "the completion signal are outside; they are inside e2e and python_loop_ms); "
-                         "python_loop_ms = the same call through the Python mirror (rtk.topk) with torch "
-                         "events around the whole call",
-               "python_loop_ms": py_ms,
-               "k_sweep": sweep,
-               "adversarial_c4": {"config": "n=2^26 Uniform[128.6,128.7) fp32, k=2^16, largest, scaled_topk "
-                                            "tau=0.5 seed=31 (device-resident)", "results": adversarial},
-               "batch_llm_bf16": {"config": "the same logits rounded to bf16 (2 B per element; bytes = "
-                                            "rows * (2V + 10k))", "results": batch_bf16},
-               "llm_sampling": {"config": "the fp32 logits batch: top-k -> softmax -> top-p -> one draw per row "
-                                          "(rtk.topk_sample, Python loop, torch events)", "results": sampling},
-               "batch_llm": {"config": f"{args.batch_rows} x {args.vocab} fp32 N(0,1) logits, rows sharded over "
-                                       f"{world} GPU(s), L2 flushed between batches", "results": batch_llm},
-               "step_ms_all": ms}
-        print(json.dumps(out))
-    if world > 1:
-        torch.distributed.destroy_process_group()
+        value = gbs(4 * n, k, med)
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": med, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (Philox on each rank's device)",
+            "config": c5_config(args, world), "elements_per_s": n / (med * 1e-3),
+            "fraction_of_hbm_peak_per_gpu": value / world / peak,
+            "roofline": {"bound": "hbm", "achieved": value / world, "peak": peak, "unit": "GB/s",
+                         "frac": value / world / peak, "traffic": None, "kernel": "whole step per GPU",
+                         "peak_kind": peak_kind},
+            "cpu_baseline": None,
+            "e2e": {"value": gbs(4 * n, k, te_s * 1e3), "unit": "GB/s", "h2d_bytes_per_step": 4 * ns,
+                    "d2h_bytes_per_step": 12 * k, "ms_per_step": te_s * 1e3,
+                    "note": "per rank: pinned H2D of its shard + rtk_topk_sharded + D2H of the result; max over ranks"},
+            "gpu_launches": per_step * args.steps, "clocks": clk.summary(),
+            "timing": "torch CUDA events around each rtk_topk_sharded step on each rank, median over steps, max "
+                      "over ranks", "step_ms_rank0": ms}))
+    comm.destroy()
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

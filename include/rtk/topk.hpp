@@ -74,6 +74,7 @@ struct Instrumentation {
     std::uint64_t elements_scanned = 0;
     std::uint64_t candidates = 0;
     std::uint64_t fallback_rows = 0;
+    std::uint64_t deep_levels = 0;
     void reset(unsigned = 0) { *this = {}; }
 };
 
@@ -135,6 +136,7 @@ inline void fill(Instrumentation& instr) {
         instr.elements_scanned = st.elements_scanned;
         instr.candidates = st.candidates;
         instr.fallback_rows = st.fallback_rows;
+        instr.deep_levels = st.deep_levels;
     }
 }
 
@@ -237,9 +239,9 @@ std::vector<TopKResult<T>> batch_topk(const BatchInput<T>& batch, SelectionOrder
         res[t].pivot = pivots[t];
     }
     detail::fill(instr);
-    if (info) {
-        info->task_passes.assign(B, 1);  // one streaming pass per task on the GPU
-        info->phase_b_rounds = 0;
+    if (info) {  // batch.hpp:138-141 as measured by the engine (rtk_get_batch_info)
+        info->task_passes.assign(B, 0);
+        detail::raise(rtk_get_batch_info(detail::handle(), info->task_passes.data(), B, &info->phase_b_rounds));
     }
     return res;
 }

@@ -17,6 +17,8 @@
  *                                               :61-67, BatchInput::validate batch.hpp:40-53)
  *   rtk_merge_shards                         <- (new) final select of the n-sharded multi-GPU
  *                                               query after the NCCL allgather
+ *   rtk_topk_sharded (+ rtk_nccl_*)          <- (new) the n-sharded query itself: local top-k,
+ *                                               ncclAllGather, final select
  *
  * Result semantics are the reference's (engine.hpp:402-420, oracle.hpp:19-39): the k
  * selected elements sorted by (encoded key descending, index ascending); ties at the pivot
@@ -137,27 +139,30 @@ int rtk_get_stats(rtk_handle h, rtk_stats* out);
 int rtk_set_timing(rtk_handle h, int on);
 
 /* Benchmark helper: `warmup` untimed then `steps` timed back-to-back rtk_topk calls issued from C
- * (the reference's own call sites are C++ loops over rtk::topk, rtk_cli.cpp:398). The device time
- * of every step is measured with CUDA events on `stream`, recorded by the engine right before its
- * first and after its last device operation of the call (host planning and the host's wait for
- * the completion signal excluded); step_ms (nullable) receives `steps`
- * values, *mean_ms their mean. Same arguments and errors as rtk_topk. */
+ * (the reference's own call sites are C++ loops over rtk::topk, rtk_cli.cpp:398). Per step:
+ * step_ms[i] (nullable) = device time between CUDA events the engine records on `stream` right
+ * before its first and after its last device operation of the call (host planning and the
+ * completion wait excluded); step_host_ms[i] (nullable) = host wall time of the rtk_topk call
+ * (steady_clock; the call returns after the device's completion signal); *mean_ms = mean of
+ * step_ms. When flush_bytes > 0, d_flush is overwritten before every step OUTSIDE both clocks
+ * (evicts the input from L2). Same arguments and errors as rtk_topk. */
 int rtk_bench_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, int order,
                    void* d_out_vals, uint64_t* d_out_idx, void* d_out_pivot, const rtk_cfg* cfg,
-                   void* stream, int warmup, int steps, float* step_ms, float* mean_ms);
+                   void* stream, void* d_flush, uint64_t flush_bytes, int warmup, int steps, float* step_ms,
+                   float* step_host_ms, float* mean_ms);
 /* Scaled counterpart (rtk_topk_scaled per step; the start event precedes the scale decision's
  * kernels). Same arguments and errors as rtk_topk_scaled. */
 int rtk_bench_scaled(rtk_handle h, const float* d_in, uint64_t n, uint64_t k, int order, int mode,
                      double trigger_fraction, uint64_t seed, float* d_out_vals, uint64_t* d_out_idx,
-                     float* d_out_pivot, const rtk_cfg* cfg, void* stream, int warmup, int steps,
-                     float* step_ms, float* mean_ms);
-/* Batched counterpart (rtk_topk_batched per step). When flush_bytes > 0, d_flush is overwritten
- * before every step OUTSIDE the timed events (evicts the inputs from L2). */
+                     float* d_out_pivot, const rtk_cfg* cfg, void* stream, void* d_flush, uint64_t flush_bytes,
+                     int warmup, int steps, float* step_ms, float* step_host_ms, float* mean_ms);
+/* Batched counterpart (rtk_topk_batched per step). */
 int rtk_bench_batched(rtk_handle h, const void* d_data, uint64_t data_len, const uint64_t* offsets,
                       const uint64_t* lengths, const uint64_t* ks, uint64_t B, int dtype, int order,
                       void* d_out_vals, uint64_t* d_out_idx, const uint64_t* out_offsets,
                       void* d_out_pivots, const rtk_cfg* cfg, void* stream, void* d_flush,
-                      uint64_t flush_bytes, int warmup, int steps, float* step_ms, float* mean_ms);
+                      uint64_t flush_bytes, int warmup, int steps, float* step_ms, float* step_host_ms,
+                      float* mean_ms);
 /* Test / diagnostic switches of a handle (not tuning: results never change). name:
  *   "force_exact"  value != 0: every row takes the exact path (the radix passes of
  *                  radix_select, engine.hpp:293-312, with the early stop) as if its sampled
@@ -222,6 +227,26 @@ int rtk_merge_shards(rtk_handle h, const void* d_cand_vals, const uint64_t* d_ca
                      uint64_t k, int dtype, int order, void* d_out_vals, uint64_t* d_out_idx,
                      void* d_out_pivot, void* stream);
 
+/* ---- one huge query over several GPUs (BASELINE C5) ------------------------
+ * The query is split by contiguous index ranges over the `world` ranks of an NCCL communicator:
+ * rank r holds shard_n[r] elements whose global indices start at sum_{g<r} shard_n[g]
+ * (shard_n: host array of `world` entries, rank order). The call drives L >= 1 local ranks:
+ * handles[i] (on the rank's device), comms[i] (ncclComm_t), d_shards[i], streams[i] and the
+ * outputs of local rank i — L = 1 with one process per GPU, L = world in the single-process
+ * multi-GPU form. Per rank: local top-k of the shard (rtk_topk, canonical order) ->
+ * ncclAllGather of the min(k, shard_n[g]) (value, local u64 index) candidates of every rank ->
+ * the rtk_merge_shards select over the gathered candidates -> every local rank receives the
+ * global top-k (values, GLOBAL u64 indices, pivot), identical to rtk_topk on the whole query.
+ * NCCL is loaded at run time (libnccl.so.2); without it the call fails with
+ * RTK_INVALID_ARGUMENT. d_out_pivots and streams may be NULL. */
+int rtk_nccl_get_unique_id(void* id_out /* 128 bytes (ncclUniqueId) */);
+int rtk_nccl_comm_init_rank(void** comm_out, int nranks, const void* id /* 128 bytes */, int rank, int device);
+int rtk_nccl_comm_destroy(void* comm);
+int rtk_topk_sharded(const rtk_handle* handles, void* const* comms, int L, const void* const* d_shards,
+                     const uint64_t* shard_n, int world, uint64_t k, int dtype, int order,
+                     void* const* d_out_vals, uint64_t* const* d_out_idx, void* const* d_out_pivots,
+                     void* const* streams);
+
 /* LLM sampling consumer: top-k of B logit rows (row b at
  * d_logits + b*row_stride elements, V elements, dtype F32/F16/BF16), then per row, in fp32:
  *   e_j = expf((v_j - v_0) / temperature) over the top-k in canonical order (v_0 = row max);
@@ -244,6 +269,14 @@ int rtk_topk_sample(rtk_handle h, const void* d_logits, uint64_t B, uint64_t V, 
  * rtk_write_batch / rtk_read_batch     <- rtk::write_batch / read_batch      io.cpp:82-110 (RTKB)
  * Readers are two-call: pass NULL outputs to query the sizes first. */
 int rtk_generate(const rtk_dist* spec, int dtype, void* out);
+/* Counter-based uniform f32 generator for queries too large for host memory (BASELINE C5,
+ * n = 2^32 over 8 GPUs): element j of the output is element offset + j of
+ * the Philox4x32-10 stream keyed by seed (word (g & 3) of block g >> 2), mapped to [a, b) as
+ * a + ((w >> 8) * 2^-24) * (b - a) in fp32 round-to-nearest (exactly (w >> 8) * 2^-24 for [0, 1)).
+ * rtk_generate_philox writes DEVICE memory on `stream`; rtk_generate_philox_host is the
+ * bit-identical host twin (any index range, e.g. single elements for verification). */
+int rtk_generate_philox(float* d_out, uint64_t n, uint64_t seed, uint64_t offset, float a, float b, void* stream);
+int rtk_generate_philox_host(float* out, uint64_t n, uint64_t seed, uint64_t offset, float a, float b);
 uint64_t rtk_result_checksum(const void* values, int dtype, const uint64_t* indices, uint64_t k);
 int rtk_write_dataset(const char* path, int dtype, const void* data, uint64_t n);
 int rtk_read_dataset(const char* path, int* dtype, uint64_t* n, void* out, uint64_t capacity);

@@ -75,6 +75,12 @@ def port() -> C.CDLL:
         lib.rtko_extract_digit.restype = u32
         lib.rtko_mt19937_64_first.argtypes = [u64]
         lib.rtko_mt19937_64_first.restype = u64
+        lib.rtkv_philox_elem.argtypes = [u64, u64, C.c_float, C.c_float]
+        lib.rtkv_philox_elem.restype = u32
+        lib.rtkv_philox_fill.argtypes = [u64, u64, u64, C.c_float, C.c_float, vp]
+        lib.rtkv_philox_fill.restype = None
+        lib.rtkv_verify_philox_topk.argtypes = [u64, u64, C.c_float, C.c_float, C.c_int, u64, vp, vp, C.c_int,
+                                                vp, C.c_char_p, C.c_int]
         _port = lib
     return _port
 
@@ -293,3 +299,23 @@ def ref_batch_topk(data: np.ndarray, offsets, lengths, ks, order: int = 0, d: in
                              oo.ctypes.data_as(P64), piv.ctypes.data))
     return [(vals[int(oo[t]):int(oo[t]) + int(kk[t])], idx[int(oo[t]):int(oo[t]) + int(kk[t])], piv[t])
             for t in range(B)]
+
+
+# ---- Philox stream (rtk_verify.c: an independent restatement of rtk_generate_philox) ---------
+def philox_fill(seed: int, offset: int, n: int, a: float = 0.0, b: float = 1.0) -> np.ndarray:
+    out = np.empty(n, dtype=np.uint32)
+    port().rtkv_philox_fill(seed, offset, n, a, b, out.ctypes.data)
+    return out.view(np.float32)
+
+
+def verify_philox_topk(seed: int, n: int, k: int, values, indices, order: int = 0, a: float = 0.0,
+                       b: float = 1.0, threads: int = 0):
+    """Streaming O(k)-memory check of a top-k of the Philox query (rtk_verify.c). Returns
+    (ok, message, [#{key > P}, #{key == P}, #{key == P, index <= last returned index}])."""
+    v = np.ascontiguousarray(np.asarray(values, dtype=np.float32).view(np.uint32))
+    i = np.ascontiguousarray(np.asarray(indices).astype(np.uint64))
+    stats = np.zeros(3, dtype=np.uint64)
+    msg = C.create_string_buffer(256)
+    rc = port().rtkv_verify_philox_topk(seed, n, a, b, order, k, v.ctypes.data, i.ctypes.data,
+                                        threads or (os.cpu_count() or 1), stats.ctypes.data, msg, 256)
+    return rc == 0, msg.value.decode(), [int(x) for x in stats]

@@ -6,11 +6,11 @@ this package is the thin host mirror of /root/reference/proj/include/rtk/.
 from .rtk import (BatchInput, BatchOptions, BatchRunInfo, BufferPolicy, EngineConfig,
                   Instrumentation, ScaleInfo, ScaleMode, ScalePolicy, SelectionOrder, TopKResult,
                   batch_topk, batch_topk_dense, empty_input_error, invariant_violation, last_stats, merge_shards,
-                  rank_out_of_range, scaled_topk, topk, topk_sample)
+                  rank_out_of_range, scaled_topk, set_option, topk, topk_sample)
 
 __all__ = [
     "BatchInput", "BatchOptions", "BatchRunInfo", "BufferPolicy", "EngineConfig",
     "Instrumentation", "ScaleInfo", "ScaleMode", "ScalePolicy", "SelectionOrder", "TopKResult",
     "batch_topk", "batch_topk_dense", "empty_input_error", "invariant_violation", "last_stats", "merge_shards",
-    "rank_out_of_range", "scaled_topk", "topk", "topk_sample",
+    "rank_out_of_range", "scaled_topk", "set_option", "topk", "topk_sample",
 ]

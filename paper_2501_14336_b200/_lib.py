@@ -64,15 +64,21 @@ SIGNATURES = {
     "rtk_get_stats": (C.c_int, [vp, C.POINTER(rtk_stats)]),
     "rtk_set_timing": (C.c_int, [vp, C.c_int]),
     "rtk_set_option": (C.c_int, [vp, C.c_char_p, C.c_int64]),
+    "rtk_nccl_get_unique_id": (C.c_int, [vp]),
+    "rtk_nccl_comm_init_rank": (C.c_int, [C.POINTER(vp), C.c_int, vp, C.c_int, C.c_int]),
+    "rtk_nccl_comm_destroy": (C.c_int, [vp]),
+    "rtk_topk_sharded": (C.c_int, [C.POINTER(vp), C.POINTER(vp), C.c_int, C.POINTER(vp), P64, C.c_int, u64,
+                                   C.c_int, C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     "rtk_get_batch_info": (C.c_int, [vp, P64, u64, P64]),
     "rtk_bench_batched": (C.c_int, [vp, vp, u64, P64, P64, P64, u64, C.c_int, C.c_int, vp, vp, P64, vp,
                                     C.POINTER(rtk_cfg), vp, vp, u64, C.c_int, C.c_int,
-                                    C.POINTER(C.c_float), C.POINTER(C.c_float)]),
-    "rtk_bench_topk": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, vp, vp, vp, C.POINTER(rtk_cfg), vp,
-                                 C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+                                    C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "rtk_bench_topk": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, vp, vp, vp, C.POINTER(rtk_cfg), vp, vp, u64,
+                                 C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                 C.POINTER(C.c_float)]),
     "rtk_bench_scaled": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, C.c_double, u64, vp, vp, vp,
-                                   C.POINTER(rtk_cfg), vp, C.c_int, C.c_int, C.POINTER(C.c_float),
-                                   C.POINTER(C.c_float)]),
+                                   C.POINTER(rtk_cfg), vp, vp, u64, C.c_int, C.c_int, C.POINTER(C.c_float),
+                                   C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "rtk_cfg_default": (None, [C.POINTER(rtk_cfg)]),
     "rtk_cfg_validate": (C.c_int, [C.POINTER(rtk_cfg)]),
     "rtk_topk": (C.c_int, [vp, vp, u64, u64, C.c_int, C.c_int, vp, vp, vp, C.POINTER(rtk_cfg), vp]),
@@ -89,6 +95,8 @@ SIGNATURES = {
     "rtk_topk_sample": (C.c_int, [vp, vp, u64, u64, u64, C.c_int, u64, C.c_float, C.c_float, vp, vp, vp, vp,
                                   vp, vp]),
     "rtk_generate": (C.c_int, [C.POINTER(rtk_dist), C.c_int, vp]),
+    "rtk_generate_philox": (C.c_int, [vp, u64, u64, u64, C.c_float, C.c_float, vp]),
+    "rtk_generate_philox_host": (C.c_int, [vp, u64, u64, u64, C.c_float, C.c_float]),
     "rtk_result_checksum": (u64, [vp, C.c_int, P64, u64]),
     "rtk_write_dataset": (C.c_int, [C.c_char_p, C.c_int, vp, u64]),
     "rtk_read_dataset": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), P64, vp, u64]),

@@ -3,6 +3,7 @@
 // 274-280; scaling.hpp:47-48) as status codes + a thread-local message.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -13,6 +14,7 @@
 #include "../../include/rtk_c.h"
 #include "rtk_engine.h"
 #include "rtk_guard.h"
+#include "rtk_sharded.h"
 
 using rtk_b200::Engine;
 using rtk_b200::Error;
@@ -24,10 +26,12 @@ struct rtk_handle_s {
     std::recursive_mutex mu;
     Engine engine;
     rtk_b200::DevBuf smp_vals, smp_idx;  // top-k workspace of rtk_topk_sample (when not supplied)
+    rtk_b200::ShardWork shard;           // candidate slots of rtk_topk_sharded
     explicit rtk_handle_s(int dev) : engine(dev) {}
     ~rtk_handle_s() {
         smp_vals.release();
         smp_idx.release();
+        shard.release();
     }
 };
 
@@ -53,6 +57,54 @@ int on_handle(rtk_handle h, F&& f) {
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw Error{RTK_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e)};
 }
+
+// Step timing of the rtk_bench_* helpers: per step a start/end CUDA event pair (recorded by the
+// engine on the call's stream around its device work) and the host wall time of the call
+// (steady_clock around the C entry point, which returns after the device's completion signal).
+// An optional L2 flush (memset of > L2 bytes) runs before each step, outside both clocks.
+class BenchSteps {
+public:
+    BenchSteps(int steps, cudaStream_t s, void* flush, uint64_t flush_bytes)
+        : ev_(2 * steps), host_(steps), s_(s), flush_(flush), flush_bytes_(flush_bytes) {
+        for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "event");
+        cuda_check(cudaStreamSynchronize(s_), "sync");
+    }
+    ~BenchSteps() {
+        for (auto& e : ev_) cudaEventDestroy(e);
+    }
+    cudaEvent_t start(int i) const { return ev_[2 * i]; }
+    cudaEvent_t end(int i) const { return ev_[2 * i + 1]; }
+    void before(int i) {
+        if (flush_ && flush_bytes_) {
+            cuda_check(cudaMemsetAsync(flush_, i & 0xff, flush_bytes_, s_), "flush");
+            cuda_check(cudaStreamSynchronize(s_), "flush sync");
+        }
+        t0_ = std::chrono::steady_clock::now();
+    }
+    void after(int i) {
+        host_[i] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
+    }
+    void finish(float* step_ms, float* step_host_ms, float* mean_ms) {
+        cuda_check(cudaStreamSynchronize(s_), "sync");
+        double sum = 0;
+        for (size_t i = 0; i < host_.size(); ++i) {
+            float ms = 0;
+            cuda_check(cudaEventElapsedTime(&ms, ev_[2 * i], ev_[2 * i + 1]), "elapsed");
+            if (step_ms) step_ms[i] = ms;
+            if (step_host_ms) step_host_ms[i] = static_cast<float>(host_[i]);
+            sum += ms;
+        }
+        if (mean_ms) *mean_ms = static_cast<float>(sum / host_.size());
+    }
+
+private:
+    std::vector<cudaEvent_t> ev_;
+    std::vector<double> host_;
+    cudaStream_t s_;
+    void* flush_;
+    uint64_t flush_bytes_;
+    std::chrono::steady_clock::time_point t0_;
+};
 
 rtk_cfg default_cfg() {
     rtk_cfg c;
@@ -245,7 +297,8 @@ int rtk_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, 
 
 int rtk_bench_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int dtype, int order,
                    void* d_out_vals, uint64_t* d_out_idx, void* d_out_pivot, const rtk_cfg* cfg,
-                   void* stream, int warmup, int steps, float* step_ms, float* mean_ms) {
+                   void* stream, void* d_flush, uint64_t flush_bytes, int warmup, int steps, float* step_ms,
+                   float* step_host_ms, float* mean_ms) {
     return on_handle(h, [&] {
         if (steps < 1 || warmup < 0) throw Error{RTK_INVALID_ARGUMENT, "bench: bad arguments"};
         cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -255,32 +308,23 @@ int rtk_bench_topk(rtk_handle h, const void* d_in, uint64_t n, uint64_t k, int d
         }
         // per step: events the engine records right before its first and after its last device
         // operation of the call (host planning and the host's completion wait excluded)
-        std::vector<cudaEvent_t> ev(2 * steps);
-        for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
-        cuda_check(cudaStreamSynchronize(s), "sync");
+        BenchSteps b(steps, s, d_flush, flush_bytes);
         for (int i = 0; i < steps; ++i) {
-            h->engine.set_call_events(ev[2 * i], ev[2 * i + 1]);
+            b.before(i);
+            h->engine.set_call_events(b.start(i), b.end(i));
             const int st = rtk_topk(h, d_in, n, k, dtype, order, d_out_vals, d_out_idx, d_out_pivot, cfg, stream);
             h->engine.set_call_events(nullptr, nullptr);
             if (st != RTK_OK) throw Error{st, g_last_error};
+            b.after(i);
         }
-        cuda_check(cudaStreamSynchronize(s), "sync");
-        double sum = 0;
-        for (int i = 0; i < steps; ++i) {
-            float ms = 0;
-            cuda_check(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]), "elapsed");
-            if (step_ms) step_ms[i] = ms;
-            sum += ms;
-        }
-        for (auto& e : ev) cudaEventDestroy(e);
-        if (mean_ms) *mean_ms = static_cast<float>(sum / steps);
+        b.finish(step_ms, step_host_ms, mean_ms);
     });
 }
 
 int rtk_bench_scaled(rtk_handle h, const float* d_in, uint64_t n, uint64_t k, int order, int mode,
                      double trigger_fraction, uint64_t seed, float* d_out_vals, uint64_t* d_out_idx,
-                     float* d_out_pivot, const rtk_cfg* cfg, void* stream, int warmup, int steps,
-                     float* step_ms, float* mean_ms) {
+                     float* d_out_pivot, const rtk_cfg* cfg, void* stream, void* d_flush, uint64_t flush_bytes,
+                     int warmup, int steps, float* step_ms, float* step_host_ms, float* mean_ms) {
     return on_handle(h, [&] {
         if (steps < 1 || warmup < 0) throw Error{RTK_INVALID_ARGUMENT, "bench: bad arguments"};
         cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -290,12 +334,11 @@ int rtk_bench_scaled(rtk_handle h, const float* d_in, uint64_t n, uint64_t k, in
             if (st != RTK_OK) throw Error{st, g_last_error};
         };
         for (int i = 0; i < warmup; ++i) one();
-        std::vector<cudaEvent_t> ev(2 * steps);
-        for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
-        cuda_check(cudaStreamSynchronize(s), "sync");
+        BenchSteps b(steps, s, d_flush, flush_bytes);
         for (int i = 0; i < steps; ++i) {
-            cuda_check(cudaEventRecord(ev[2 * i], s), "event");  // before the scale decision's kernels
-            h->engine.set_call_events(nullptr, ev[2 * i + 1]);
+            b.before(i);
+            cuda_check(cudaEventRecord(b.start(i), s), "event");  // before the scale decision's kernels
+            h->engine.set_call_events(nullptr, b.end(i));
             try {
                 one();
             } catch (...) {
@@ -303,17 +346,9 @@ int rtk_bench_scaled(rtk_handle h, const float* d_in, uint64_t n, uint64_t k, in
                 throw;
             }
             h->engine.set_call_events(nullptr, nullptr);
+            b.after(i);
         }
-        cuda_check(cudaStreamSynchronize(s), "sync");
-        double sum = 0;
-        for (int i = 0; i < steps; ++i) {
-            float ms = 0;
-            cuda_check(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]), "elapsed");
-            if (step_ms) step_ms[i] = ms;
-            sum += ms;
-        }
-        for (auto& e : ev) cudaEventDestroy(e);
-        if (mean_ms) *mean_ms = static_cast<float>(sum / steps);
+        b.finish(step_ms, step_host_ms, mean_ms);
     });
 }
 
@@ -321,7 +356,8 @@ int rtk_bench_batched(rtk_handle h, const void* d_data, uint64_t data_len, const
                       const uint64_t* lengths, const uint64_t* ks, uint64_t B, int dtype, int order,
                       void* d_out_vals, uint64_t* d_out_idx, const uint64_t* out_offsets,
                       void* d_out_pivots, const rtk_cfg* cfg, void* stream, void* d_flush,
-                      uint64_t flush_bytes, int warmup, int steps, float* step_ms, float* mean_ms) {
+                      uint64_t flush_bytes, int warmup, int steps, float* step_ms, float* step_host_ms,
+                      float* mean_ms) {
     return on_handle(h, [&] {
         if (steps < 1 || warmup < 0) throw Error{RTK_INVALID_ARGUMENT, "bench: bad arguments"};
         cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -331,11 +367,10 @@ int rtk_bench_batched(rtk_handle h, const void* d_data, uint64_t data_len, const
             if (st != RTK_OK) throw Error{st, g_last_error};
         };
         for (int i = 0; i < warmup; ++i) one();
-        std::vector<cudaEvent_t> ev(2 * steps);
-        for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
+        BenchSteps b(steps, s, d_flush, flush_bytes);
         for (int i = 0; i < steps; ++i) {
-            if (d_flush && flush_bytes) cuda_check(cudaMemsetAsync(d_flush, i & 0xff, flush_bytes, s), "flush");
-            h->engine.set_call_events(ev[2 * i], ev[2 * i + 1]);
+            b.before(i);
+            h->engine.set_call_events(b.start(i), b.end(i));
             try {
                 one();
             } catch (...) {
@@ -343,17 +378,9 @@ int rtk_bench_batched(rtk_handle h, const void* d_data, uint64_t data_len, const
                 throw;
             }
             h->engine.set_call_events(nullptr, nullptr);
+            b.after(i);
         }
-        cuda_check(cudaStreamSynchronize(s), "sync");
-        double sum = 0;
-        for (int i = 0; i < steps; ++i) {
-            float ms = 0;
-            cuda_check(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]), "elapsed");
-            if (step_ms) step_ms[i] = ms;
-            sum += ms;
-        }
-        for (auto& e : ev) cudaEventDestroy(e);
-        if (mean_ms) *mean_ms = static_cast<float>(sum / steps);
+        b.finish(step_ms, step_host_ms, mean_ms);
     });
 }
 
@@ -520,6 +547,51 @@ int rtk_topk_scaled_host(rtk_handle h, const float* in, uint64_t n, uint64_t k, 
         cuda_check(cudaMemcpyAsync(out_idx, e.io_idx.p, 8 * k, cudaMemcpyDeviceToHost, s), "d2h");
         if (out_pivot) cuda_check(cudaMemcpyAsync(out_pivot, e.io_piv.p, 4, cudaMemcpyDeviceToHost, s), "d2h");
         cuda_check(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+int rtk_nccl_get_unique_id(void* id_out) {
+    return guarded([&] {
+        if (!id_out) throw Error{RTK_INVALID_ARGUMENT, "null id"};
+        rtk_b200::nccl_unique_id(id_out);
+    });
+}
+
+int rtk_nccl_comm_init_rank(void** comm_out, int nranks, const void* id, int rank, int device) {
+    return guarded([&] {
+        if (!comm_out || !id || nranks < 1 || rank < 0 || rank >= nranks)
+            throw Error{RTK_INVALID_ARGUMENT, "nccl comm init: bad arguments"};
+        *comm_out = rtk_b200::nccl_comm_init(nranks, id, rank, device);
+    });
+}
+
+int rtk_nccl_comm_destroy(void* comm) {
+    return guarded([&] { rtk_b200::nccl_comm_destroy(comm); });
+}
+
+int rtk_topk_sharded(const rtk_handle* handles, void* const* comms, int L, const void* const* d_shards,
+                     const uint64_t* shard_n, int world, uint64_t k, int dtype, int order,
+                     void* const* d_out_vals, uint64_t* const* d_out_idx, void* const* d_out_pivots,
+                     void* const* streams) {
+    return guarded([&] {
+        if (!handles || !comms || !d_shards || !shard_n || !d_out_vals || !d_out_idx || L < 1 || world < 1 || L > world)
+            throw Error{RTK_INVALID_ARGUMENT, "topk_sharded: bad arguments"};
+        if (!dtype_ok(dtype)) throw Error{RTK_INVALID_ARGUMENT, "dtype must be F32, U32, F16 or BF16"};
+        if (order != RTK_LARGEST && order != RTK_SMALLEST) throw Error{RTK_INVALID_ARGUMENT, "bad order"};
+        std::vector<Engine*> eng(L);
+        std::vector<rtk_b200::ShardWork*> work(L);
+        std::vector<std::unique_lock<std::recursive_mutex>> locks;
+        for (int i = 0; i < L; ++i) {
+            if (!handles[i] || !comms[i] || !d_shards[i] || !d_out_vals[i] || !d_out_idx[i])
+                throw Error{RTK_INVALID_ARGUMENT, "topk_sharded: null entry"};
+            locks.emplace_back(handles[i]->mu);
+            eng[i] = &handles[i]->engine;
+            work[i] = &handles[i]->shard;
+        }
+        for (int g = 0; g < world; ++g)
+            if (shard_n[g] > (uint64_t(1) << 32)) throw Error{RTK_INVALID_ARGUMENT, "shard longer than 2^32"};
+        rtk_b200::topk_sharded(eng.data(), work.data(), comms, L, d_shards, shard_n, world, k, eng_dtype(dtype),
+                               static_cast<int>(esize(dtype)), order, d_out_vals, d_out_idx, d_out_pivots, streams);
     });
 }
 

@@ -1169,9 +1169,13 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
         check(cudaMemsetAsync(row_fail_.as<uint32_t>() + r, 0, 4, s), "memset");
         check(cudaMemsetAsync(done_.as<uint32_t>() + r, 0, 4, s), "memset");
     }
-    // control words: flags = 0, slot lists empty, work = groups so far
+    // control words: flags = 0, slot lists empty, work = groups so far; the level-0 MSD's grid
+    // barrier restarts from 0 (the main path's MSD may have returned before its barrier — a row
+    // whose plan failed has an empty slot — so the device count need not match bar_gen_)
     check(cudaMemsetAsync(ctl_.p, 0, 4, s), "memset");
     check(cudaMemsetAsync(ctl_.as<uint32_t>() + 3, 0, 8, s), "memset");
+    check(cudaMemsetAsync(ctl_.as<uint32_t>() + 7, 0, 4, s), "memset");
+    bar_gen_ = 0;
     check(cudaMemcpyAsync(ctl_.as<uint32_t>() + 2, ctl_.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToDevice, s), "work");
     check(cudaMemcpyAsync(ctl_.as<uint32_t>() + 6, ctl_.as<uint32_t>() + 5, 4, cudaMemcpyDeviceToDevice, s), "wwork");
     for (uint32_t r : fb) ++row_passes_[r];  // the re-compaction reads the row once more

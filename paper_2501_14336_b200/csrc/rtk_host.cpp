@@ -14,6 +14,8 @@
 
 #include "../../include/rtk_c.h"
 #include "rtk_guard.h"
+#include "rtk_kernels.h"
+#include "rtk_philox.h"
 
 using rtk_b200::Error;
 using rtk_b200::guarded;
@@ -225,3 +227,29 @@ int rtk_read_batch(const char* path, uint32_t* tasks, uint64_t* payload_bytes, u
 }
 
 }  // extern "C"
+
+extern "C" int rtk_generate_philox(float* d_out, uint64_t n, uint64_t seed, uint64_t offset, float a, float b,
+                                   void* stream) {
+    return guarded([&] {
+        if (!d_out && n) throw bad("philox: null output");
+        if (!(a < b)) throw bad("uniform: requires a < b");
+        rtk_b200::launch_philox_uniform(d_out, n, seed, offset, a, b, static_cast<cudaStream_t>(stream));
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw Error{RTK_CUDA_ERROR, std::string("philox launch: ") + cudaGetErrorString(e)};
+    });
+}
+
+extern "C" int rtk_generate_philox_host(float* out, uint64_t n, uint64_t seed, uint64_t offset, float a, float b) {
+    return guarded([&] {
+        if (!out && n) throw bad("philox: null output");
+        if (!(a < b)) throw bad("uniform: requires a < b");
+        const float span = b - a;
+        uint64_t g = offset;
+        for (uint64_t j = 0; j < n;) {
+            uint32_t w[4];
+            rtk_b200::philox_block(seed, g >> 2, w);
+            for (uint32_t q = static_cast<uint32_t>(g & 3); q < 4 && j < n; ++q, ++j, ++g)
+                out[j] = rtk_b200::philox_uniform(w[q], a, span);
+        }
+    });
+}

@@ -329,6 +329,8 @@ void launch_rows_fused(int R, const RowsFusedArgs& a, bool small, cudaStream_t s
 uint32_t rows_fused_kmax(bool small);
 uint32_t rows_fused_cand(bool small);
 uint32_t rows_fused_sample(bool small);
+void launch_philox_uniform(float* out, uint64_t n, uint64_t seed, uint64_t offset, float a, float b,
+                           cudaStream_t s);
 void launch_sample_rows(uint64_t rows, const void* vals, int fmt, const uint64_t* idx, uint64_t k, float top_p,
                         float temperature, const float* uniform, uint64_t* token, float* probs, cudaStream_t s);
 void launch_scale_decide(int mode, const unsigned long long* hist, uint32_t nbins, uint64_t n, uint64_t k,

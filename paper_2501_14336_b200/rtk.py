@@ -211,10 +211,36 @@ def set_timing(on: bool, device: int = 0) -> None:
     _raise(L.load().rtk_set_timing(_handle(device), int(bool(on))))
 
 
+@dataclass
+class BenchResult:
+    """Per-step times of an rtk_bench_* run: device_ms (CUDA events the engine records on the
+    launching stream around its device work) and host_ms (wall time of each C entry-point call,
+    which returns after the device's completion signal)."""
+    device_ms: List[float]
+    host_ms: List[float]
+
+    @property
+    def median_ms(self) -> float:
+        return float(np.median(self.device_ms))
+
+    @property
+    def median_host_ms(self) -> float:
+        return float(np.median(self.host_ms))
+
+
+def _steps(steps: int):
+    return (C.c_float * int(steps))(), (C.c_float * int(steps))(), C.c_float()
+
+
+def _flush_args(flush):
+    return C.c_void_p(flush.data_ptr() if flush is not None else 0), int(flush.numel() if flush is not None else 0)
+
+
 def bench_topk(x, k: int, steps: int, warmup: int = 3, order: SelectionOrder = SelectionOrder.Largest,
-               cfg: Optional[EngineConfig] = None):
-    """rtk_bench_topk: `steps` back-to-back rtk_topk calls issued from C on x's current stream;
-    returns (mean_ms, [step_ms]) measured with CUDA events (device-resident input)."""
+               cfg: Optional[EngineConfig] = None, flush=None) -> BenchResult:
+    """rtk_bench_topk: `steps` back-to-back rtk_topk calls issued from C on x's current stream
+    (device-resident input); `flush` (a CUDA byte tensor larger than L2) is overwritten before
+    every step outside the clocks."""
     import torch
     cfg = cfg or EngineConfig()
     lib = L.load()
@@ -223,21 +249,22 @@ def bench_topk(x, k: int, steps: int, warmup: int = 3, order: SelectionOrder = S
     vals = torch.empty(kk, dtype=x.dtype, device=x.device)
     idx = torch.empty(kk, dtype=torch.int64, device=x.device)
     piv = torch.empty(1, dtype=x.dtype, device=x.device)
-    per = (C.c_float * int(steps))()
-    mean = C.c_float()
+    per, host, mean = _steps(steps)
     c = cfg._c()
+    fp, fb = _flush_args(flush)
     st = lib.rtk_bench_topk(_handle(x.device.index or 0), C.c_void_p(x.data_ptr()), x.numel(), kk,
                             _dtype_code(x), int(order), C.c_void_p(vals.data_ptr()), C.c_void_p(idx.data_ptr()),
-                            C.c_void_p(piv.data_ptr()), C.byref(c), _stream_ptr(x), int(warmup), int(steps),
-                            per, C.byref(mean))
+                            C.c_void_p(piv.data_ptr()), C.byref(c), _stream_ptr(x), fp, fb, int(warmup), int(steps),
+                            per, host, C.byref(mean))
     _raise(st, "rtk_bench_topk")
-    return float(mean.value), [float(v) for v in per]
+    return BenchResult([float(v) for v in per], [float(v) for v in host])
 
 
 def bench_scaled(x, k: int, steps: int, warmup: int = 3, policy: Optional[ScalePolicy] = None,
-                 order: SelectionOrder = SelectionOrder.Largest, cfg: Optional[EngineConfig] = None):
+                 order: SelectionOrder = SelectionOrder.Largest, cfg: Optional[EngineConfig] = None,
+                 flush=None) -> BenchResult:
     """rtk_bench_scaled: `steps` back-to-back rtk_topk_scaled calls issued from C on x's current
-    stream; returns (mean_ms, [step_ms]) (device-resident f32 input)."""
+    stream (device-resident f32 input)."""
     import torch
     cfg = cfg or EngineConfig()
     policy = policy or ScalePolicy()
@@ -249,23 +276,23 @@ def bench_scaled(x, k: int, steps: int, warmup: int = 3, policy: Optional[ScaleP
     vals = torch.empty(kk, dtype=x.dtype, device=x.device)
     idx = torch.empty(kk, dtype=torch.int64, device=x.device)
     piv = torch.empty(1, dtype=x.dtype, device=x.device)
-    per = (C.c_float * int(steps))()
-    mean = C.c_float()
+    per, host, mean = _steps(steps)
     c = cfg._c()
+    fp, fb = _flush_args(flush)
     st = lib.rtk_bench_scaled(_handle(x.device.index or 0), C.c_void_p(x.data_ptr()), x.numel(), kk, int(order),
                               int(policy.mode), float(policy.trigger_fraction),
                               int(policy.seed) & 0xFFFFFFFFFFFFFFFF, C.c_void_p(vals.data_ptr()),
                               C.c_void_p(idx.data_ptr()), C.c_void_p(piv.data_ptr()), C.byref(c), _stream_ptr(x),
-                              int(warmup), int(steps), per, C.byref(mean))
+                              fp, fb, int(warmup), int(steps), per, host, C.byref(mean))
     _raise(st, "rtk_bench_scaled")
-    return float(mean.value), [float(v) for v in per]
+    return BenchResult([float(v) for v in per], [float(v) for v in host])
 
 
 def bench_batch_dense(x, k: int, steps: int, warmup: int = 3, flush=None,
-                      order: SelectionOrder = SelectionOrder.Largest, cfg: Optional[EngineConfig] = None):
+                      order: SelectionOrder = SelectionOrder.Largest,
+                      cfg: Optional[EngineConfig] = None) -> BenchResult:
     """rtk_bench_batched over a dense [B, V] CUDA tensor: `steps` rtk_topk_batched calls issued
-    from C, CUDA events per step; `flush` (a CUDA byte tensor) is overwritten between steps
-    outside the timed events. Returns (mean_ms, [step_ms])."""
+    from C; `flush` (a CUDA byte tensor) is overwritten between steps outside the clocks."""
     import torch
     cfg = cfg or EngineConfig()
     lib = L.load()
@@ -278,17 +305,15 @@ def bench_batch_dense(x, k: int, steps: int, warmup: int = 3, flush=None,
     vals = torch.empty((B, k), dtype=x.dtype, device=x.device)
     idx = torch.empty((B, k), dtype=torch.int64, device=x.device)
     piv = torch.empty(B, dtype=x.dtype, device=x.device)
-    per = (C.c_float * int(steps))()
-    mean = C.c_float()
+    per, host, mean = _steps(steps)
     c = cfg._c()
+    fp, fb = _flush_args(flush)
     st = lib.rtk_bench_batched(_handle(x.device.index or 0), C.c_void_p(x.data_ptr()), x.numel(), p_off, p_len,
                                p_ks, B, _dtype_code(x), int(order), C.c_void_p(vals.data_ptr()),
                                C.c_void_p(idx.data_ptr()), p_oo, C.c_void_p(piv.data_ptr()), C.byref(c),
-                               _stream_ptr(x), C.c_void_p(flush.data_ptr() if flush is not None else 0),
-                               int(flush.numel() if flush is not None else 0), int(warmup), int(steps),
-                               per, C.byref(mean))
+                               _stream_ptr(x), fp, fb, int(warmup), int(steps), per, host, C.byref(mean))
     _raise(st, "rtk_bench_batched")
-    return float(mean.value), [float(v) for v in per]
+    return BenchResult([float(v) for v in per], [float(v) for v in host])
 
 
 def _is_cuda(x) -> bool:
@@ -551,6 +576,25 @@ def scaled_topk(input, k: int, order: SelectionOrder = SelectionOrder.Largest,
         info.a_s = float(si.a_s)
         info.a_index = int(si.a_index)
     return res
+
+
+def generate_philox(n: int, seed: int, offset: int = 0, a: float = 0.0, b: float = 1.0, device=None):
+    """rtk_generate_philox: elements [offset, offset + n) of the Philox uniform f32 stream written
+    straight into a new CUDA tensor (the per-shard generator of the n = 2^32 configuration)."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    out = torch.empty(int(n), dtype=torch.float32, device=dev)
+    _raise(L.load().rtk_generate_philox(C.c_void_p(out.data_ptr()), int(n), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                        int(offset), float(a), float(b), _stream_ptr(out)), "rtk_generate_philox")
+    return out
+
+
+def generate_philox_host(n: int, seed: int, offset: int = 0, a: float = 0.0, b: float = 1.0) -> np.ndarray:
+    """rtk_generate_philox_host: the bit-identical host twin of generate_philox."""
+    out = np.empty(int(n), dtype=np.float32)
+    _raise(L.load().rtk_generate_philox_host(C.c_void_p(out.ctypes.data), int(n), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                             int(offset), float(a), float(b)), "rtk_generate_philox_host")
+    return out
 
 
 def merge_shards(cand_vals, cand_idx, block_len: Sequence[int], shard_base: Sequence[int], k: int,

@@ -94,3 +94,19 @@ def test_handle_without_gpu_fails_loudly(lib):
     import paper_2501_14336_b200 as rtk
     with pytest.raises(Exception):
         rtk.topk(np.ones(16, dtype=np.float32), 4)  # no silent CPU fallback
+
+
+def test_cpp_header_compiles_against_the_library(tmp_path):
+    # the drop-in C++ front end (include/rtk/topk.hpp) and the retargeted acceptance program
+    # compile and link against librtk_b200.so (run on the GPU in tests/test_gpu_sharded.py)
+    import shutil
+    import subprocess
+    if not shutil.which("g++"):
+        pytest.skip("no g++")
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    out = tmp_path / "acc"
+    p = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "acceptance_b200.cpp"), "-o", str(out),
+                        "-L", os.path.join(ROOT, "paper_2501_14336_b200"), "-lrtk_b200", "-L", ref, "-lrtk_ref"],
+                       capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-3000:]

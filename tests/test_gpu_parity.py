@@ -520,11 +520,12 @@ def test_bench_helpers_time_the_same_call(cuda):
     import torch
     from paper_2501_14336_b200 import rtk as R
     x = torch.from_numpy(O.ref_generate(UNIFORM, 1 << 22, 5, a=128.6, b=128.7)).to(cuda)
-    ms, per = R.bench_topk(x, 4096, 4, 1)
-    assert ms > 0 and len(per) == 4 and all(p > 0 for p in per)
+    b = R.bench_topk(x, 4096, 4, 1)
+    assert b.median_ms > 0 and len(b.device_ms) == 4 and all(p > 0 for p in b.device_ms)
+    assert all(h >= d * 0.5 for h, d in zip(b.host_ms, b.device_ms))
     pol = R.ScalePolicy(mode=R.ScaleMode(2), trigger_fraction=0.5, seed=31)
-    ms, per = R.bench_scaled(x, 4096, 4, 1, policy=pol)
-    assert ms > 0 and all(p > 0 for p in per)
+    b = R.bench_scaled(x, 4096, 4, 1, policy=pol)
+    assert b.median_ms > 0 and all(p > 0 for p in b.device_ms)
     got = R.scaled_topk(x, 4096, policy=pol)
     want = O.ref_scaled_topk(x.cpu().numpy(), 4096, 0, mode=2, tau=0.5, seed=31)
     assert np.array_equal(got.indices.cpu().numpy().astype(np.uint64), np.asarray(want[1], dtype=np.uint64))

@@ -1,9 +1,12 @@
 """CPU, world_size 2 over gloo: host logic of the multi-GPU paths.
 
-The local top-k is the C restatement (oracle), the exchange is a real torch.distributed
-all-gather over gloo, and the merge applies the same rule rtk_merge_shards implements
-(position-in-gathered-array tie-break, then remap to global indices). The result must equal the
-single-device reference on the whole query, including ties that straddle the shard boundary.
+rtk_topk_sharded (csrc/rtk_sharded.cpp) runs, per rank: local top-k of the shard -> all-gather of
+every rank's min(k, shard_n) candidates -> final select with the position in the gathered array
+as tie-break index -> remap to global indices. Here the same steps run with the C restatement
+(oracle) as the local top-k and the final select, and a real torch.distributed all-gather over
+gloo as the exchange; the result must equal the single-device reference on the whole query,
+including ties that straddle the shard boundary. The NCCL bootstrap (rank 0's ncclUniqueId
+broadcast to every rank, sharded.bootstrap_unique_id) runs over gloo as well.
 """
 import os
 import socket
@@ -53,14 +56,23 @@ def _oracle_merge(cv, ci, block_len, shard_base, k):
     return v, np.array(gidx, dtype=np.uint64), piv
 
 
+def _sharded_steps(x_local, k, n_total, rank, world):
+    # the steps of rtk_topk_sharded with the oracle for the two selects
+    start, length = SH.shard_bounds(n_total, world, rank)
+    assert length == len(x_local)
+    v, i, _ = O.port_topk(x_local, min(k, length))
+    vb, ib = _gloo_gather(v, i)
+    block_len = [len(b) for b in vb]
+    shard_base = [SH.shard_bounds(n_total, world, g)[0] for g in range(world)]
+    return _oracle_merge(np.concatenate(vb), np.concatenate(ib), block_len, shard_base, k)
+
+
 def _worker(rank, world, port, x, k, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         s, l = SH.shard_bounds(len(x), world, rank)
-        v, i, piv = SH.sharded_topk(x[s:s + l], k, len(x), rank, world,
-                                    local_topk=lambda xs, kk: O.port_topk(xs, kk)[:2],
-                                    all_gather=_gloo_gather, merge=_oracle_merge)
+        v, i, piv = _sharded_steps(x[s:s + l], k, len(x), rank, world)
         q.put((rank, v.view(np.uint32).tolist(), i.tolist()))
     finally:
         dist.destroy_process_group()
@@ -105,3 +117,36 @@ def test_sharded_ties_across_shard_boundary_gloo():
     want_v, want_i, _ = O.port_topk(x, k)
     for rank, v, i in _run(x, k):
         assert i == want_i.tolist(), rank
+
+
+def _boot_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        made = []
+
+        def make_id():
+            made.append(rank)
+            return bytes((rank * 31 + j) & 0xFF for j in range(128))
+
+        uid = SH.bootstrap_unique_id(rank, make_id=make_id)
+        q.put((rank, uid, made))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_bootstrap_broadcasts_rank0_id_gloo():
+    # only rank 0 draws the id; every rank ends up with rank 0's 128 bytes
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_boot_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = bytes(j & 0xFF for j in range(128))
+    assert [o[1] for o in out] == [want, want]
+    assert out[0][2] == [0] and out[1][2] == []

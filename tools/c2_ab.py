@@ -14,7 +14,7 @@ g = torch.Generator(device="cuda"); g.manual_seed(1)
 x = torch.rand(1 << int(os.environ.get("LOGN", "28")), device="cuda", generator=g)
 out = []
 for k in [int(v) for v in os.environ.get("KS", "256,1048576").split(",")]:
-    ms, _ = R.bench_topk(x, k, 30, 3)
+    ms = R.bench_topk(x, k, 30, 3).median_ms
     out.append(f"k={k} {ms*1e3:.1f}us")
 print(" | ".join(out))
 ''' % ROOT

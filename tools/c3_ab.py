@@ -18,7 +18,7 @@ out = []
 for dt in os.environ.get("DT", "f32").split(","):
     X = L if dt == "f32" else L.to(torch.bfloat16)
     for k in [int(v) for v in os.environ.get("KS", "50,4096").split(",")]:
-        ms, _ = R.bench_batch_dense(X, k, 20, 3, flush)
+        ms = R.bench_batch_dense(X, k, 20, 3, flush).median_ms
         out.append(f"{dt} k={k} {ms*1e3:.1f}us")
 print(" | ".join(out))
 ''' % ROOT

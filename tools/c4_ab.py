@@ -15,7 +15,7 @@ xa = (128.6 + 0.1 * torch.rand(1 << 26, device="cuda", generator=g)).float()
 out = []
 for m in (0, 1, 2):
     pol = R.ScalePolicy(mode=R.ScaleMode(m), trigger_fraction=0.5, seed=31)
-    ms, _ = R.bench_scaled(xa, 1 << 16, 20, 3, policy=pol)
+    ms = R.bench_scaled(xa, 1 << 16, 20, 3, policy=pol).median_ms
     out.append(f"mode{m} {ms*1e3:.1f}us")
 print(" | ".join(out))
 ''' % ROOT
