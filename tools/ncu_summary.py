@@ -20,9 +20,25 @@ if len(sys.argv) > 2:
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(src.splitlines()))
-    hh = rows[1]
-    si, ci, wi = hh.index("Source"), hh.index("Instructions Executed"), hh.index("Warp Stall Sampling (All Samples)")
-    data = [(r[si], int(r[ci] or 0), int(r[wi] or 0)) for r in rows[2:] if len(r) > wi]
+    # one table per kernel; each starts with a header row holding the column names
+    data, hh = [], None
+    for r in rows:
+        if "Source" in r and "Instructions Executed" in r:
+            hh = r
+            continue
+        if hh is None or len(r) != len(hh):
+            continue
+        wcol = next((c for c in hh if c.startswith("Warp Stall Sampling (All")), None)
+        if wcol is None:
+            continue
+        si, ci, wi = hh.index("Source"), hh.index("Instructions Executed"), hh.index(wcol)
+        try:
+            data.append((r[si], int(r[ci] or 0), int(r[wi] or 0)))
+        except ValueError:
+            continue
+    if not data:
+        print("(no source-level samples in the report)")
+        sys.exit(0)
     tot = sum(d[2] for d in data)
     print("top stall lines (samples, executed, sass):")
     for d in sorted(data, key=lambda d: -d[2])[:int(sys.argv[2])]:
