@@ -573,6 +573,22 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         const uint32_t idx0 = static_cast<uint32_t>(span0 - lead);  // low 32 bits of the row index
         load_tile(t);
 
+        // K >= T with T = (T.hi, T.lo): key > T.hi, or key == T.hi and index <= ~T.lo. T.lo != 0
+        // when ties at the threshold key were split by index (tie-heavy inputs, the exact path).
+        // The index condition is decided per TILE: a tile whose valid indices all lie at or below
+        // ~T.lo keeps equal keys (compare with T.hi), one wholly above drops them (compare with
+        // T.hi + 1); only the one tile straddling ~T.lo compares element by element.
+        uint32_t tthr = thi;
+        bool straddle = false;
+        if (tlo != 0) {
+            const uint32_t tidx = ~tlo, first = idx0 + vlo, last = idx0 + vhi - 1;
+            if (last <= tidx) {
+            } else if (first > tidx && thi != 0xFFFFFFFFu) {
+                tthr = thi + 1;
+            } else {
+                straddle = true;
+            }
+        }
         // pass 1: key transform + per-thread hit mask (bit u*8+i)
         uint32_t mask = 0;
         if (vlo == 0 && vhi == kTile) {
@@ -582,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
                 for (int i = 0; i < kVec; ++i) {
                     const uint32_t key = key_of<KM>(v[u][i], in);
                     v[u][i] = key;
-                    mask |= static_cast<uint32_t>(key >= thi) << (u * kVec + i);
+                    mask |= static_cast<uint32_t>(key >= tthr) << (u * kVec + i);
                 }
         } else {
 #pragma unroll
@@ -592,11 +608,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
                     const uint32_t key = key_of<KM>(v[u][i], in);
                     v[u][i] = key;
                     const uint32_t l = (u * kThreads + threadIdx.x) * kVec + i;
-                    mask |= static_cast<uint32_t>(key >= thi && l >= vlo && l < vhi) << (u * kVec + i);
+                    mask |= static_cast<uint32_t>(key >= tthr && l >= vlo && l < vhi) << (u * kVec + i);
                 }
         }
-        // exact composite compare: only differs from key >= T.hi when T.lo != 0 (exact path)
-        if (tlo != 0) {
+        if (straddle) {
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
