@@ -415,9 +415,12 @@ __global__ void __launch_bounds__(1024) k_sample_select(SampleRows sr, InputSrc 
 // Counts are exact even past `cap` (writes beyond cap are dropped -> host falls back).
 // ----------------------------------------------------------------------------------------
 constexpr int kWarpStage = 512;
+#ifndef RTK_COMPACT_MINB
+#define RTK_COMPACT_MINB 3
+#endif
 
 template <int KM>
-__global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in, const uint64_t* T,
+__global__ void __launch_bounds__(kThreads, RTK_COMPACT_MINB) k_compact(Rows rows, InputSrc in, const uint64_t* T,
                                                          uint64_t* cand, const uint64_t* cand_off,
                                                          const uint64_t* cap,
                                                          unsigned long long* count,
@@ -431,13 +434,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
     const unsigned lt_mask = (1u << lane) - 1u;
     unsigned long long* stage = stage_all[warp];
 
-    int cur = -1;
-    unsigned long long thr = 0, mn = ~0ull, mx = 0;
+    // CTA-uniform state of the current row that the streaming loop does not touch lives in
+    // shared memory (register pressure: the loop holds 32 input words per thread)
+    struct RowState {
+        uint64_t coff, ccap, len;
+        uint32_t r, j;
+    };
+    __shared__ RowState s_row;
+    bool have_row = false;
+    unsigned long long mn = ~0ull, mx = 0;
     uint32_t ko = 0;  // OR of (key ^ T.hi) over this thread's hits of the current row
     uint32_t thi = 0, tlo = 0, wcur = 0;
-    uint64_t off = 0, len = 0, coff = 0, ccap = 0, tile0 = 0, tile1 = 0;
-    uint32_t lead = 0, r = 0, mine_tiles = 0;
-    int cur_j = -1;
+    uint64_t base_el = 0, span_len = 0, tile0 = 0, tile1 = 0;  // base_el = row offset - lead
+    uint32_t lead = 0, mine_tiles = 0;
 
     // PDL: this grid may start while k_sample_select still runs. The input does not depend on
     // it: each CTA pulls its first tiles into L2 with TMA bulk prefetches (<= ~96 MB in total,
@@ -464,8 +473,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         if (wcur == 0) return;
         __syncwarp();
         unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(count + r, static_cast<unsigned long long>(wcur));
+        if (lane == 0) base = atomicAdd(count + s_row.r, static_cast<unsigned long long>(wcur));
         base = __shfl_sync(full, base, 0);
+        const uint64_t coff = s_row.coff, ccap = s_row.ccap;
         for (uint32_t i = lane; i < wcur; i += 32) {
             const unsigned long long K = stage[i];
             mn = min(mn, K);
@@ -486,6 +496,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
             b = max(b, __shfl_xor_sync(full, b, d));
             o |= __shfl_xor_sync(full, o, d);
         }
+        const uint32_t r = s_row.r;
         if (lane == 0 && a <= b) {
             atomicMin(kmin + r, a);
             atomicMax(kmax + r, b);
@@ -504,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
                 s_last = old + mine_tiles == tiles;
                 if (s_last) {
                     __threadfence();
-                    plan_row(cur_j, r, pa, len);
+                    plan_row(static_cast<int>(s_row.j), r, pa, s_row.len);
                 }
             }
             __syncthreads();
@@ -522,11 +533,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
     auto load_tile = [&](uint64_t tt) {
         const uint64_t sp = (tt - tile0) * kTile;
         const uint32_t lo = sp >= lead ? 0u : static_cast<uint32_t>(lead - sp);
-        const uint32_t hi = static_cast<uint32_t>(len + lead - sp < kTile ? len + lead - sp : kTile);
+        const uint32_t hi = static_cast<uint32_t>(span_len - sp < kTile ? span_len - sp : kTile);
         if constexpr (km_is16<KM>())
-            load_tile_local16(reinterpret_cast<const unsigned short*>(in.base) + off - lead + sp, lo, hi, v);
+            load_tile_local16(reinterpret_cast<const unsigned short*>(in.base) + base_el + sp, lo, hi, v);
         else
-            load_tile_local(in.base + off - lead + sp, lo, hi, v);
+            load_tile_local(in.base + base_el + sp, lo, hi, v);
     };
     // interleaved mode: the last `dyn` tiles are handed out from a counter, so CTAs that start
     // late (PDL launch next to the sample kernel's cluster) do not leave a tail
@@ -546,27 +557,27 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
     };
     const uint64_t t_first = (dyn != 0 && t_begin >= ns) ? grab() : t_begin;
     for (uint64_t t = t_first; t < t_end; t = next_tile(t)) {
-        if (t >= tile1 || cur < 0) {
-            if (cur >= 0) finish_row();
+        if (t >= tile1 || !have_row) {  // CTA-uniform
+            if (have_row) finish_row();
+            have_row = true;
             const int j = row_of_tile(rows, t);
-            cur = j;
-            cur_j = j;
-            mine_tiles = 0;
-            r = rows.rid[j];
-            thr = T[r];
+            const uint32_t r = rows.rid[j];
+            const unsigned long long thr = T[r];
             thi = static_cast<uint32_t>(thr >> 32);
             tlo = static_cast<uint32_t>(thr);
-            off = rows.off[j];
-            len = rows.len[j];
             lead = rows.lead[j];
-            coff = cand_off[r];
-            ccap = cap[r];
+            const uint64_t len = rows.len[j];
+            base_el = rows.off[j] - lead;
+            span_len = len + lead;
             tile0 = rows.tile_start[j];
             tile1 = rows.tile_start[j + 1];
+            mine_tiles = 0;
+            __syncthreads();  // every warp is done with the previous row's shared state
+            if (threadIdx.x == 0) s_row = RowState{cand_off[r], cap[r], len, r, static_cast<uint32_t>(j)};
+            __syncthreads();
         }
         ++mine_tiles;
         const uint64_t span0 = (t - tile0) * kTile;
-        const uint64_t span_len = len + lead;
         // validity window of this tile in tile-local positions (32-bit math from here on)
         const uint32_t vlo = span0 >= lead ? 0u : static_cast<uint32_t>(lead - span0);
         const uint32_t vhi = static_cast<uint32_t>(span_len - span0 < kTile ? span_len - span0 : kTile);
@@ -636,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
         if (wtot <= pa.sparse_max) {
             // sparse hits (the common case): visit only the set bits; the element is re-read
             // from L2 (its tile was just streamed) instead of indexing registers dynamically
-            const uint64_t tp = off - lead + span0;  // element offset of the tile
+            const uint64_t tp = base_el + span0;  // element offset of the tile
             uint32_t o = wcur + incl - c;
             uint32_t m = mask;
             if (pa.sparse_sel) {
@@ -686,7 +697,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
             wcur += wtot;
         } else {  // dense hits (k close to n): straight to global with one cursor atomic
             unsigned long long base = 0;
-            if (lane == 0) base = atomicAdd(count + r, static_cast<unsigned long long>(wtot));
+            if (lane == 0) base = atomicAdd(count + s_row.r, static_cast<unsigned long long>(wtot));
             base = __shfl_sync(full, base, 0) + (incl - c);
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
@@ -698,13 +709,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_compact(Rows rows, InputSrc in,
                         mn = min(mn, K);
                         mx = max(mx, K);
                         ko |= v[u][i] ^ thi;  // same per-row OR as warp_flush (plan_row's tz)
-                        if (base < ccap) cand[coff + base] = K;
+                        if (base < s_row.ccap) cand[s_row.coff + base] = K;
                         ++base;
                     }
                 }
         }
     }
-    if (cur >= 0) finish_row();
+    if (have_row) finish_row();
     if (dyn) {  // the last CTA out resets the tile counters for the next launch
         __syncthreads();
         if (threadIdx.x == 0) {
