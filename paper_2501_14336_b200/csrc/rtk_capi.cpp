@@ -182,19 +182,44 @@ void run_scaled(Engine& e, const float* d_in, uint64_t n, uint64_t k, int order,
     }
     std::mt19937_64 rng(seed);
     const uint64_t a_index = rng() % n;
-    e.enqueue_scale_decide(reinterpret_cast<const uint32_t*>(d_in), n, k, cfg.d, order,
-                           mode == RTK_SCALE_ALWAYS ? 1 : 2, tau, a_index, s);
-    e.set_adapt(e.device_scale());
-    try {
-        e.run(reinterpret_cast<const uint32_t*>(d_in), RTK_F32, order, false, 0.0f, /*gather=*/true,
-              {RowReq{0, n, k, 0}}, reinterpret_cast<uint32_t*>(d_vals), d_idx,
-              reinterpret_cast<uint32_t*>(d_piv), s);
-    } catch (...) {
+    auto select = [&](bool count_trigger) {
+        e.set_adapt(e.device_scale());
+        e.set_trigger_count(count_trigger);
+        try {
+            e.run(reinterpret_cast<const uint32_t*>(d_in), RTK_F32, order, false, 0.0f, /*gather=*/true,
+                  {RowReq{0, n, k, 0}}, reinterpret_cast<uint32_t*>(d_vals), d_idx,
+                  reinterpret_cast<uint32_t*>(d_piv), s);
+        } catch (...) {
+            e.set_adapt(nullptr);
+            e.set_trigger_count(false);
+            throw;
+        }
         e.set_adapt(nullptr);
-        throw;
+        e.set_trigger_count(false);
+    };
+    // Adaptive on a row that streams through k_compact (not a one-CTA row, not a dense k >= n/2
+    // row): speculate on a sampled trigger and verify it with the exact counts of the same pass
+    const bool speculate = mode == RTK_SCALE_ADAPTIVE && cfg.d <= 14 && n > (uint64_t(1) << 18) && 2 * k < n;
+    bool exact_trigger = mode == RTK_SCALE_ADAPTIVE && !speculate;
+    if (speculate) {
+        e.enqueue_scale_guess(reinterpret_cast<const uint32_t*>(d_in), n, k, cfg.d, order, tau, a_index, s);
+        select(true);
+        uint64_t gt = 0, eq = 0;
+        e.trigger_counts(&gt, &eq);
+        bool guessed = false;
+        float unused = 0.0f;
+        e.scale_result(&guessed, &unused);
+        // gt < k <= gt + eq: the guessed bin IS select_bin's bin (engine.hpp:231-241), eq its count
+        const bool bin_ok = gt < k && k <= gt + eq;
+        const bool fat = static_cast<double>(eq) > tau * static_cast<double>(n);
+        if (!bin_ok || fat != guessed) exact_trigger = true;  // wrong guess: the exact trigger, rerun
     }
-    e.set_adapt(nullptr);
-    if (mode == RTK_SCALE_ADAPTIVE) {
+    if (mode == RTK_SCALE_ALWAYS || exact_trigger) {
+        e.enqueue_scale_decide(reinterpret_cast<const uint32_t*>(d_in), n, k, cfg.d, order,
+                               mode == RTK_SCALE_ALWAYS ? 1 : 2, tau, a_index, s);
+        select(false);
+    }
+    if (exact_trigger) {
         e.stats.passes += 1;
         e.stats.elements_scanned += n;
     }

@@ -277,6 +277,10 @@ const rtk_stats& Engine::last_stats() {
     if (stats_pending_) {
         cudaEventSynchronize(ev_[3]);
         cudaEventElapsedTime(&stats.total_ms, ev_[0], ev_[3]);
+        // events not recorded in this call (graph replay without event nodes) leave compact_ms
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, ev_[1], ev_[2]) == cudaSuccess) stats.compact_ms = ms;
+        cudaGetLastError();
         stats_pending_ = false;
     }
     return stats;
@@ -766,6 +770,7 @@ void Engine::complete(const uint32_t* d_base, const std::vector<RowReq>& rows, C
     const bool cleaned = clean_rows_ >= R && sig_pending_;
     needs_init_ = true;
     drain(c, ctl);
+    std::memcpy(trig_words_, drain_trig_, sizeof(trig_words_));  // the main path's trigger counts
     // host-driven rare paths enqueue more device work: the call's end moves behind it
     const bool extra = (first_flags_ & (kFlagMore | kFlagFail)) != 0;
     // first_flags_: the flag word as the main path left it (drain's deeper levels clear kFlagMore)
@@ -798,8 +803,7 @@ void Engine::complete(const uint32_t* d_base, const std::vector<RowReq>& rows, C
     mark("drain", s);
     report_marks();
     release_retired();
-    cudaEventElapsedTime(&stats.compact_ms, ev_[1], ev_[2]);
-    stats_pending_ = true;
+    stats_pending_ = true;  // compact_ms / total_ms resolved lazily (the events may still be pending)
     if (profile_) last_stats();
 }
 
@@ -871,6 +875,7 @@ PlanArgs Engine::plan_args(const Call& c, const FinishPrep& f) {
     pa.done = done_.as<uint32_t>();
     pa.max_bits = level0_bits();
     pa.force_fail = force_exact_ && !in_fallback_ ? 1u : 0u;
+    pa.trig = trig_count_ && !in_fallback_ ? 1u : 0u;
     pa.prefetch_mb = static_cast<uint32_t>(prefetch_mb_);
     pa.sparse_max = static_cast<uint32_t>(sparse_max_);
     pa.sparse_sel = static_cast<uint32_t>(sparse_sel_);
@@ -1006,13 +1011,15 @@ void Engine::drain(Call& c, uint32_t (&ctl)[8]) {
         check(cudaHostAlloc(reinterpret_cast<void**>(&hcount_), 8 * hcount_cap_, cudaHostAllocDefault), "cudaHostAlloc");
     }
     if (sig_pending_ && !count_stats_) {
-        wait_signal(c.s);  // the last sort CTA published ctl[0..7]: no copy, no stream sync
+        wait_signal(c.s);  // the last sort CTA published ctl[0..14]: no copy, no stream sync
         for (int i = 0; i < 8; ++i) ctl[i] = reinterpret_cast<volatile uint32_t*>(hmap_)[i];
+        for (int i = 0; i < 4; ++i) drain_trig_[i] = reinterpret_cast<volatile uint32_t*>(hmap_)[10 + i];
     } else {
-        check(cudaMemcpyAsync(hctl_, ctl_.p, 32, cudaMemcpyDeviceToHost, c.s), "d2h");
+        check(cudaMemcpyAsync(hctl_, ctl_.p, 64, cudaMemcpyDeviceToHost, c.s), "d2h");
         if (count_stats_) check(cudaMemcpyAsync(hcount_, count_.p, 8 * c.R, cudaMemcpyDeviceToHost, c.s), "d2h");
         sync(c.s, "finish");
         std::memcpy(ctl, hctl_, 32);
+        std::memcpy(drain_trig_, hctl_ + 10, 16);
     }
     sig_pending_ = false;
     first_flags_ = ctl[0];
@@ -1262,6 +1269,19 @@ void Engine::enqueue_scale_decide(const uint32_t* d_in, uint64_t n, uint64_t k, 
     }
     launch_scale_decide(mode, hist, static_cast<uint32_t>(nb), n, k, tau, d_in, a_index,
                         adapt_buf_.as<uint32_t>(), d_hscale_, s);
+}
+
+void Engine::enqueue_scale_guess(const uint32_t* d_in, uint64_t n, uint64_t k, unsigned d, int smallest, double tau,
+                                 uint64_t a_index, cudaStream_t s) {
+    DeviceGuard dg(device_);
+    if (!hscale_) {
+        check(cudaHostAlloc(reinterpret_cast<void**>(&hscale_), 16, cudaHostAllocMapped), "cudaHostAlloc");
+        std::memset(hscale_, 0, 16);
+        check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_hscale_), hscale_, 0), "mapped pointer");
+    }
+    adapt_buf_.ensure(16);
+    launch_scale_guess(d_in, n, k, d, smallest, tau, a_index, adapt_buf_.as<uint32_t>(), d_hscale_, s);
+    check(cudaGetLastError(), "scale guess launch");
 }
 
 void Engine::scale_result(bool* scaled, float* a_s) const {

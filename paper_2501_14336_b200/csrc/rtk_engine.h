@@ -92,6 +92,16 @@ public:
     void enqueue_scale_decide(const uint32_t* d_in, uint64_t n, uint64_t k, unsigned d, int smallest,
                               int mode, double tau, uint64_t a_index, cudaStream_t s);
     const uint32_t* device_scale() const { return adapt_buf_.as<uint32_t>(); }
+    // Adaptive without the counting pass: k_scale_guess decides from a sample; the next run()
+    // with set_trigger_count(true) counts the exact #{digit > b} / #{digit == b} of the unscaled
+    // first window over all n (k_compact), readable afterwards through trigger_counts()
+    void enqueue_scale_guess(const uint32_t* d_in, uint64_t n, uint64_t k, unsigned d, int smallest, double tau,
+                             uint64_t a_index, cudaStream_t s);
+    void set_trigger_count(bool on) { trig_count_ = on; }
+    void trigger_counts(uint64_t* gt, uint64_t* eq) const {
+        *gt = trig_words_[0] | (static_cast<uint64_t>(trig_words_[1]) << 32);
+        *eq = trig_words_[2] | (static_cast<uint64_t>(trig_words_[3]) << 32);
+    }
     // {flag, a_s bits} of the last decision (valid once the following run() returned)
     void scale_result(bool* scaled, float* a_s) const;
     void set_adapt(const uint32_t* p) { adapt_ = p; }
@@ -236,6 +246,9 @@ private:
     bool no_graph_events_ = true;   // no stats events inside graphs (RTK_GRAPH_EVENTS=1 keeps them)
     cudaEvent_t call_start_ = nullptr, call_end_ = nullptr;
     bool timing_ = false;           // rtk_set_timing: no graph replay, events around k_compact
+    bool trig_count_ = false;       // count the speculative Adaptive trigger in the main compaction
+    uint32_t trig_words_[4] = {0, 0, 0, 0};  // ctl[10..13] as the main path left them
+    uint32_t drain_trig_[4] = {0, 0, 0, 0};
     bool force_exact_ = false;      // RTK_FORCE_EXACT / "force_exact"
     bool force_deep_ = false;       // RTK_FORCE_DEEP / "force_deep"
     bool in_fallback_ = false;      // the exact path's own compaction (no forced failure there)

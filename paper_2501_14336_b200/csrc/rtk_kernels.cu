@@ -467,7 +467,17 @@ __global__ void __launch_bounds__(kThreads, RTK_COMPACT_MINB) k_compact(Rows row
         }
     }
     pdl_wait();
-    resolve_src(in);  // scaled_topk decided on the device (k_scale_decide)
+    resolve_src(in);  // scaled_topk decided on the device (k_scale_decide / k_scale_guess)
+    // speculative Adaptive trigger (k_scale_guess): count the unscaled first-window digits
+    // above / at the guessed bin over every element of the row (main path only)
+    constexpr bool kAdapt = KM == kKmF32LAdapt || KM == kKmF32SAdapt;
+    uint32_t g_bin = 0, g_shift = 32, c_gt = 0, c_eq = 0;
+    if constexpr (kAdapt) {
+        if (pa.trig) {
+            g_bin = __ldcg(in.adapt + 2);
+            g_shift = __ldcg(in.adapt + 3);
+        }
+    }
 
     auto warp_flush = [&]() {  // warp-uniform
         if (wcur == 0) return;
@@ -600,6 +610,37 @@ __global__ void __launch_bounds__(kThreads, RTK_COMPACT_MINB) k_compact(Rows row
                 straddle = true;
             }
         }
+        if constexpr (kAdapt) {
+            if (g_shift < 32) {  // digit >= b  <=>  key >= b << shift;  digit > b  <=>  key > ((b + 1) << shift) - 1
+                const uint32_t lo = g_bin << g_shift, hm1 = ((g_bin + 1) << g_shift) - 1u;  // top bin: hm1 = ~0
+                uint32_t ge = 0, gt = 0;
+                if (vlo == 0 && vhi == kTile) {
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                        for (int i = 0; i < kVec; ++i) {
+                            const uint32_t ku = encode_f32_bits(v[u][i], KM == kKmF32SAdapt);
+                            // two compares + two predicated increments per element
+                            asm("{\n.reg .pred p, q;\nsetp.ge.u32 p, %2, %3;\nsetp.gt.u32 q, %2, %4;\n"
+                                "@p add.u32 %0, %0, 1;\n@q add.u32 %1, %1, 1;\n}"
+                                : "+r"(ge), "+r"(gt) : "r"(ku), "r"(lo), "r"(hm1));
+                        }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                        for (int i = 0; i < kVec; ++i) {
+                            const uint32_t l = (u * kThreads + threadIdx.x) * kVec + i;
+                            const uint32_t ku = encode_f32_bits(v[u][i], KM == kKmF32SAdapt);
+                            const bool ok = l >= vlo && l < vhi;
+                            ge += ok && ku >= lo;
+                            gt += ok && ku > hm1;
+                        }
+                }
+                c_gt += gt;
+                c_eq += ge - gt;
+            }
+        }
         // pass 1: key transform + per-thread hit mask (bit u*8+i)
         uint32_t mask = 0;
         if (vlo == 0 && vhi == kTile) {
@@ -716,6 +757,20 @@ __global__ void __launch_bounds__(kThreads, RTK_COMPACT_MINB) k_compact(Rows row
         }
     }
     if (have_row) finish_row();
+    if constexpr (kAdapt) {
+        if (g_shift < 32) {  // warp totals -> ctl[10..11] (#{digit > b}), ctl[12..13] (#{digit == b})
+            unsigned long long a = c_gt, b = c_eq;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                a += __shfl_xor_sync(full, a, d);
+                b += __shfl_xor_sync(full, b, d);
+            }
+            if (lane == 0) {
+                atomicAdd(reinterpret_cast<unsigned long long*>(pa.flags + 10), a);
+                atomicAdd(reinterpret_cast<unsigned long long*>(pa.flags + 12), b);
+            }
+        }
+    }
     if (dyn) {  // the last CTA out resets the tile counters for the next launch
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -871,6 +926,105 @@ __global__ void k_scale_decide(int mode, const unsigned long long* hist, uint32_
             __threadfence_system();
         }
     }
+}
+
+// k_scale_guess: Adaptive scaled_topk without the extra counting pass. One CTA samples the
+// unscaled keys (kGuessSeg segments of 32 consecutive elements spread over the row), takes
+// select_bin of their first d-bit window at the sample rank of k, and GUESSES the trigger
+// (sample fraction of that bin > tau). out = {flag, a_s bits, bin b, 32 - d}; the selection then
+// runs in the guessed mode while k_compact counts, over ALL n elements, #{digit > b} and
+// #{digit == b} of the unscaled keys (ctl[10..13]). The host accepts the run only if those
+// counts prove b is the exact select_bin bin (#{> b} < k <= #{>= b}) and reproduce the decision
+// hist[b] > tau * n of scaling.hpp:50-58; otherwise it reruns with the exact trigger pass.
+constexpr int kGuessSeg = 512;
+__global__ void __launch_bounds__(1024) k_scale_guess(const uint32_t* x, uint64_t n, uint64_t k, uint32_t d,
+                                                      int smallest, double tau, uint64_t a_index, uint32_t* out,
+                                                      volatile uint32_t* host_out) {
+    extern __shared__ uint32_t h[];  // 2^d bins (d <= 14)
+    __shared__ unsigned long long s_warp[32];
+    __shared__ uint32_t s_bin, s_cnt;
+    const int tid = threadIdx.x;
+    const uint32_t nb = 1u << d;
+    for (uint32_t b = tid; b < nb; b += blockDim.x) h[b] = 0;
+    if (tid == 0) {
+        s_bin = 0;
+        s_cnt = 0;
+    }
+    __syncthreads();
+    const uint64_t segs = n >= 32ull * kGuessSeg ? kGuessSeg : (n + 31) / 32;
+    const uint64_t stride = segs > 1 ? (n - 32) / (segs - 1) : 0;
+    uint32_t S = 0;
+    // warp-aggregated (the adversarial case puts every sample in ONE bin: 16K same-address
+    // shared atomics would serialise); the trip count is warp-uniform (blockDim | 32 * segs)
+    // all 16 loads per thread in flight before the first use (one DRAM round trip, not 16)
+    constexpr int kPer = kGuessSeg * 32 / 1024;
+    uint32_t raw[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const uint32_t e = q * 1024 + tid;
+        const uint64_t i = (e / 32) * stride + (e & 31);
+        raw[q] = e < segs * 32 && i < n ? __ldg(x + i) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const uint32_t e = q * 1024 + tid;
+        const uint64_t i = (e / 32) * stride + (e & 31);
+        const bool valid = e < segs * 32 && i < n;
+        const uint32_t dg = valid ? encode_f32_bits(raw[q], smallest != 0) >> (32 - d) : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xffffffffu, dg);
+        if (valid && (tid & 31) == __ffs(peers) - 1) atomicAdd(h + dg, static_cast<uint32_t>(__popc(peers)));
+    }
+    S = static_cast<uint32_t>(n < segs * 32 ? n : segs * 32);
+    __syncthreads();
+    // sample rank of k: ceil(k * S / n), then select_bin (descending cumulative scan)
+    const uint64_t ks0 = (k * S + n - 1) / n;
+    const uint64_t ks = ks0 > 0 ? ks0 : 1;
+    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+    unsigned long long sum = 0;
+    for (uint32_t i = 0; i < per; ++i) {
+        const uint32_t b = tid * per + i;
+        if (b < nb) sum += h[nb - 1 - b];
+    }
+    unsigned long long tot;
+    const unsigned long long before = block_excl_scan(sum, s_warp, &tot);
+    if (before < ks && before + sum >= ks) {
+        unsigned long long cum = before;
+        for (uint32_t i = 0; i < per; ++i) {
+            const uint32_t b = tid * per + i;
+            if (b >= nb) break;
+            const uint32_t c = h[nb - 1 - b];
+            if (cum + c >= ks) {
+                s_bin = nb - 1 - b;
+                s_cnt = c;
+                break;
+            }
+            cum += c;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const uint32_t fat = static_cast<double>(s_cnt) > tau * static_cast<double>(S) ? 1u : 0u;
+        const uint32_t a = fat ? __ldg(x + a_index) : 0u;
+        out[0] = fat;
+        out[1] = a;
+        out[2] = s_bin;
+        out[3] = 32 - d;
+        if (host_out) {
+            host_out[0] = fat;
+            host_out[1] = a;
+            __threadfence_system();
+        }
+    }
+}
+
+void launch_scale_guess(const uint32_t* x, uint64_t n, uint64_t k, uint32_t d, int smallest, double tau,
+                        uint64_t a_index, uint32_t* out, volatile uint32_t* host_out, cudaStream_t s) {
+    const size_t smem = (size_t(1) << d) * sizeof(uint32_t);
+    static DeviceOnce configured;
+    configured([&] {
+        cudaFuncSetAttribute(k_scale_guess, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    });
+    k_scale_guess<<<1, 1024, smem, s>>>(x, n, k, d, smallest, tau, a_index, out, host_out);
 }
 
 // ----------------------------------------------------------------------------------------

@@ -58,7 +58,7 @@ __device__ __forceinline__ void call_tail(const CallTail& t, uint32_t* s_flag) {
             *t.done_ctr = 0;
             const uint32_t seq = atomicAdd(t.seq_ctr, 1u) + 1;
             const volatile uint32_t* c = t.ctl;
-            for (int i = 0; i < 8; ++i) t.hflags[i] = c[i];
+            for (int i = 0; i < 15; ++i) t.hflags[i] = c[i];  // [8..9] tile counter, [10..13] trigger counts
             __threadfence_system();
             t.hflags[15] = seq;
             *s_flag = 1;
@@ -214,6 +214,7 @@ struct PlanArgs {         // per-row plan after the compaction (fused into k_com
     uint32_t dyn_per_cta;    // dynamic-tail tiles per CTA of the grid
     uint32_t contig;         // 1: contiguous tile runs per CTA (many-row batches), 0: interleaved
     uint32_t force_fail;     // test switch "force_exact": every row takes the exact path
+    uint32_t trig;           // count the speculative Adaptive trigger (k_scale_guess) into flags[10..13]
 };
 
 struct SortArgs {
@@ -333,6 +334,8 @@ void launch_philox_uniform(float* out, uint64_t n, uint64_t seed, uint64_t offse
                            cudaStream_t s);
 void launch_sample_rows(uint64_t rows, const void* vals, int fmt, const uint64_t* idx, uint64_t k, float top_p,
                         float temperature, const float* uniform, uint64_t* token, float* probs, cudaStream_t s);
+void launch_scale_guess(const uint32_t* x, uint64_t n, uint64_t k, uint32_t d, int smallest, double tau,
+                        uint64_t a_index, uint32_t* out, volatile uint32_t* host_out, cudaStream_t s);
 void launch_scale_decide(int mode, const unsigned long long* hist, uint32_t nbins, uint64_t n, uint64_t k,
                          double tau, const uint32_t* x, uint64_t a_index, uint32_t* out,
                          volatile uint32_t* host_out, cudaStream_t s);

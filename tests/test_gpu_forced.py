@@ -316,3 +316,32 @@ def test_concurrent_callers_share_one_handle(cuda):
     for x in th:
         x.join()
     assert not errors, errors
+
+
+# ---- Adaptive scaling: the sampled trigger guess and its exact verification ------------------------
+@pytest.mark.parametrize("order", [0, 1])
+def test_adaptive_guess_accepted_and_rejected(cuda, order):
+    # scaling.hpp:47-58 decides on the EXACT first-window histogram. The library guesses from a
+    # sample (k_scale_guess) and verifies with exact counts taken in the same streaming pass; a
+    # wrong guess reruns with the exact trigger pass (stats.passes == 1). Both must equal the
+    # reference bit for bit.
+    import torch
+    rtk = _rtk()
+    n, k = 1 << 22, 400
+    narrow = O.ref_generate(UNIFORM, n, 77, a=128.6, b=128.7)  # one fat bin: guess "scale", accepted
+    hidden = O.ref_generate(UNIFORM, n, 78)                     # top-k hidden between sample segments
+    stride = (n - 32) // 511
+    pos = np.array([s * stride + 4000 + j for s in range(511) for j in range(2)])
+    hidden[pos] = -1000.0 if order else 1000.0
+    balanced = O.ref_generate(UNIFORM, n, 79)                   # the k-th bin holds ~half the row
+    balanced[: n // 2 + 1] = np.float32(1.5) if order == 0 else np.float32(-1.5)
+    for name, x, want_passes in (("narrow", narrow, 0), ("hidden", hidden, 1), ("balanced", balanced, None)):
+        for tau in (0.5, 0.3):
+            wv, wi, wp, winfo = O.ref_scaled_topk(x, k, order, mode=2, tau=tau, seed=31, grid=CORES)
+            info = rtk.ScaleInfo()
+            r = rtk.scaled_topk(torch.from_numpy(x).to(cuda), k, rtk.SelectionOrder(order),
+                                policy=rtk.ScalePolicy(rtk.ScaleMode.Adaptive, tau, 31), info=info)
+            assert info.scaled == winfo["scaled"], (name, tau)
+            assert_same((r.values, r.indices, r.pivot), (wv, wi, wp), f"adaptive {name} tau={tau}")
+            if want_passes is not None:
+                assert rtk.last_stats().passes == want_passes, (name, rtk.last_stats())

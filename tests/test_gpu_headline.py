@@ -88,3 +88,5 @@ def test_c4_headline(c4, mode):
     assert info.scaled == winfo["scaled"]
     assert info.a_index == (winfo["a_index"] if winfo["scaled"] else 0)
     assert_same((r.values, r.indices, r.pivot), (wv, wi, wp), f"C4 mode={mode}")
+    if mode == 2:  # the sampled trigger guess was verified exact in the selection pass: no extra pass
+        assert rtk.last_stats().passes == 0
