@@ -1,9 +1,10 @@
 """Device time of one workload under the current RTK_* environment (rtk_bench_* C loops, L2
-flushed before each step): python tools/ab_env.py c1|c2|c3|c3b|c4 k [mode]."""
+flushed before each step except C2): python tools/ab_env.py c1|c2|c3|c3b|c4 k [mode]. RTK_PKG_ROOT
+selects another build (tools/build_variant.sh)."""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("RTK_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 
