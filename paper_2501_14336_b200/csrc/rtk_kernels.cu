@@ -641,9 +641,61 @@ __global__ void __launch_bounds__(kThreads, RTK_COMPACT_MINB) k_compact(Rows row
                 c_eq += ge - gt;
             }
         }
-        // pass 1: key transform + per-thread hit mask (bit u*8+i)
+        // pass 1: key transform + per-thread hit mask (bit u*8+i). Scaled keys (y = x - a_s): a
+        // plain fp32 subtraction per element and one NaN flag per thread; only a thread that
+        // produced a NaN re-derives those keys with the x86 NaN rule of sub_x86 (the element
+        // re-read from L2), instead of a NaN test per element
+        constexpr bool kSub = KM == kKmF32LScaled || KM == kKmF32SScaled || kAdapt;
+        constexpr bool kSm = KM == kKmF32SScaled || KM == kKmF32SAdapt;
         uint32_t mask = 0;
-        if (vlo == 0 && vhi == kTile) {
+        if constexpr (kSub) {
+            if (!kAdapt || in.scaled) {
+                bool anynan = false;
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                    for (int i = 0; i < kVec; ++i) {
+                        const float y = __fsub_rn(__uint_as_float(v[u][i]), in.a_s);
+                        anynan |= y != y;
+                        // the bits through an opaque move: otherwise the sign-flip encode is
+                        // rewritten as float negation (FADD -|y|), which canonicalises NaNs
+                        uint32_t yb;
+                        asm("mov.b32 %0, %1;" : "=r"(yb) : "f"(y));
+                        v[u][i] = encode_f32_bits(yb, kSm);
+                    }
+                if (anynan) {
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                        for (int i = 0; i < kVec; ++i) {
+                            const uint32_t e = kSm ? ~v[u][i] : v[u][i];  // encode(y) -> y
+                            const uint32_t yb = (e & 0x80000000u) ? (e ^ 0x80000000u) : ~e;
+                            const uint32_t l = (u * kThreads + threadIdx.x) * kVec + i;
+                            if ((yb & 0x7fffffffu) > 0x7f800000u && l >= vlo && l < vhi)
+                                v[u][i] = encode_f32_bits(sub_x86(__ldg(in.base + base_el + span0 + l), in.a_s), kSm);
+                        }
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                    for (int i = 0; i < kVec; ++i) v[u][i] = encode_f32_bits(v[u][i], kSm);
+            }
+            if (vlo == 0 && vhi == kTile) {
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                    for (int i = 0; i < kVec; ++i) mask |= static_cast<uint32_t>(v[u][i] >= tthr) << (u * kVec + i);
+            } else {
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                    for (int i = 0; i < kVec; ++i) {
+                        const uint32_t l = (u * kThreads + threadIdx.x) * kVec + i;
+                        mask |= static_cast<uint32_t>(v[u][i] >= tthr && l >= vlo && l < vhi) << (u * kVec + i);
+                    }
+            }
+        } else if (vlo == 0 && vhi == kTile) {
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
 #pragma unroll

@@ -1,53 +1,41 @@
-# Round-end evidence (1 GPU): full bench line (+ reference arm), ncu launch lists of the bench
-# configs, and full captures of the top kernels. Run under gpurun; outputs in gpurun_out/.
-cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out
-timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo "bench rc=$?"
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    --log-file gpurun_out/prof_launches.csv env RTK_MSD_Q=1 python tools/prof_topk.py 28 1048576 3 > /dev/null 2>&1; echo "launches rc=$?"
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    --log-file gpurun_out/prof_batch_launches.csv python -c "
-import torch, paper_2501_14336_b200 as rtk
-x=torch.randn(256,128256,device='cuda')
-for kb in (50, 4096, 128256): rtk.batch_topk_dense(x, kb)
-torch.cuda.synchronize()
-" > /dev/null 2>&1; echo "batch rc=$?"
-cat > /tmp/c4a.py <<'PY'
-import sys, os
-sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "."))
-import torch, paper_2501_14336_b200 as rtk
-from paper_2501_14336_b200 import rtk as R
-g = torch.Generator(device="cuda"); g.manual_seed(1)
-xa = (128.6 + 0.1 * torch.rand(1 << 26, device="cuda", generator=g)).float()
-for m in (0, 1, 2):
-    pol = R.ScalePolicy(mode=R.ScaleMode(m), trigger_fraction=0.5, seed=31)
-    for i in range(2): rtk.scaled_topk(xa, 1 << 16, policy=pol)
-torch.cuda.synchronize()
-PY
-MODE=2 RTK_MSD_Q=1 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    --log-file gpurun_out/prof_c4_launches.csv python /tmp/c4a.py > /dev/null 2>&1 || true
-ncu --set full --clock-control none --import-source on -k regex:"k_compact" -s 2 -c 1 \
-    -o gpurun_out/prof_compact -f python tools/prof_topk.py 28 1048576 3 > gpurun_out/prof_compact.log 2>&1; echo "compact rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"k_msd_cluster|k_sort_groups|k_sample_select" -s 3 -c 3 \
-    -o gpurun_out/prof_finish -f env RTK_MSD_Q=1 python tools/prof_topk.py 28 1048576 3 > gpurun_out/prof_finish.log 2>&1; echo "finish rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"k_rows_fused" -s 1 -c 2 \
-    -o gpurun_out/prof_rows -f python -c "
-import torch, paper_2501_14336_b200 as rtk
-x=torch.randn(256,128256,device='cuda')
-for kb in (50, 50, 4096, 4096): rtk.batch_topk_dense(x, kb)
-torch.cuda.synchronize()
-" > gpurun_out/prof_rows.log 2>&1; echo "rows rc=$?"
-# dense bf16 rows (k = vocab): the one-sweep LSD kernels
-cat > /tmp/lsd.py <<'PY'
-import os, sys
-sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "."))
-import torch, paper_2501_14336_b200 as rtk
-x = torch.randn(256, 128256, device="cuda").to(torch.bfloat16)
-for _ in range(2): rtk.batch_topk_dense(x, 128256)
-torch.cuda.synchronize()
-PY
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    --log-file gpurun_out/prof_lsd_launches.csv python /tmp/lsd.py > /dev/null 2>&1; echo "lsd launches rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"k_lsd_pass" -s 2 -c 1 \
-    -o gpurun_out/prof_lsd -f python /tmp/lsd.py > gpurun_out/prof_lsd.log 2>&1; echo "lsd rc=$?"
+# Round-2 evidence (1 GPU): GPU suite + smoke + bench line + reference arm, ncu launch lists of the
+# bench configs and full-capture summaries of the top kernels. Run under gpurun; outputs (text and
+# JSON only: gpurun returns at most 64 MiB) in gpurun_out/r2/.
+cd $GRAFT_REPO_ROOT; O=gpurun_out/r2; mkdir -p $O /tmp/ncu
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv,noheader > $O/gpu.txt
+lscpu | grep -E "Model name|^CPU\(s\)" >> $O/gpu.txt
+if [ -z "$SKIP_TESTS" ]; then
+timeout 1700 python -m pytest tests -m gpu -q --timeout=600 --timeout-method=thread > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -1 $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
+fi
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference_arm.json 2> $O/bench_ref.err; echo "ref rc=$?"
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum
+launches() { local name=$1; shift; timeout 600 ncu --metrics $M --clock-control none --csv --log-file $O/launches_$name.csv "$@" > /dev/null 2>&1; echo "launches $name rc=$?"; }
+launches c2_k2p20 env RTK_MSD_Q=1 python tools/prof_marks.py c2 1048576
+launches c2_k256 python tools/prof_marks.py c2 256
+launches c1 python tools/prof_marks.py c1 256
+launches c3_k50 python tools/prof_marks.py c3 50
+launches c3_k4096 python tools/prof_marks.py c3 4096
+launches c3_vocab python tools/prof_marks.py c3 128256
+launches c3_bf16_vocab env BF16=1 python tools/prof_marks.py c3 128256
+launches c4_off env MODE=0 RTK_MSD_Q=1 python tools/prof_marks.py c4
+launches c4_adaptive env MODE=2 RTK_MSD_Q=1 python tools/prof_marks.py c4
+cap() {  # name, kernel regex, skip, count, [env...] python args...
+  local name=$1 rx=$2 s=$3 c=$4; shift 4
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$rx" -s $s -c $c \
+    -o /tmp/ncu/$name -f "$@" > /tmp/ncu/$name.log 2>&1; echo "cap $name rc=$?"
+  python tools/ncu_summary.py /tmp/ncu/$name.ncu-rep 25 > $O/ncu_$name.txt 2>&1
+}
+cap compact "k_compact" 1 1 python tools/prof_marks.py c2 1048576
+cap sample_c2 "k_sample_select" 1 1 python tools/prof_marks.py c2 1048576
+cap sort_c2 "k_sort_groups" 1 1 python tools/prof_marks.py c2 1048576
+cap rows50 "k_rows_fused" 1 1 python tools/prof_marks.py c3 50
+cap rows4096 "k_rows_fused" 1 1 python tools/prof_marks.py c3 4096
+cap lsd "k_lsd_pass" 1 1 python tools/prof_marks.py c3 128256
+cap compact_c4a "k_compact" 1 1 env MODE=2 python tools/prof_marks.py c4
+# the shipped multi-cluster level-0 MSD (cooperative launch, grid barrier): application replay
+timeout 900 ncu --set full --replay-mode application --clock-control none --import-source on -k regex:"k_msd_cluster" -s 1 -c 1 \
+  -o /tmp/ncu/msd_q16 -f python tools/prof_marks.py c2 1048576 > /tmp/ncu/msd_q16.log 2>&1; echo "cap msd_q16 rc=$?"
+python tools/ncu_summary.py /tmp/ncu/msd_q16.ncu-rep 25 > $O/ncu_msd_q16.txt 2>&1
+tail -3 /tmp/ncu/msd_q16.log >> $O/ncu_msd_q16.txt
