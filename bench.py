@@ -231,7 +231,7 @@ def main():
     ap.add_argument("--sweep", type=str, default="256,16384", help="extra C2 k values")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--legs", type=str, default="c1,c3,c4,c5", help="secondary legs (N = 1)")
+    ap.add_argument("--legs", type=str, default="c1,c2dist,c3,c4,c5", help="secondary legs (N = 1)")
     ap.add_argument("--batch-ks", type=str, default="50,4096,128256")
     ap.add_argument("--batch-rows", type=int, default=256)
     ap.add_argument("--vocab", type=int, default=128256)
@@ -318,9 +318,13 @@ def single_gpu(args):
                "cpu_model": cpu_model(), "ms": t * 1e3,
                "sample": f"the same query and input (n=2^{args.logn}, k={k}): rtk::topk (oracle/_ref) "
                          f"grid_size={cores}, median of 3"}
-    del hp
+    if "c2dist" not in legs:
+        del hp
 
     out_legs = {}
+    if "c2dist" in legs:
+        del hp
+        out_legs["c2_distributions"] = leg_c2_dists(args, R, x, dev, peak, cores, do_cpu)
     if "c1" in legs:
         out_legs["c1"] = leg_c1(args, R, dev, flush, peak, cores, do_cpu)
     if "c3" in legs:
@@ -359,6 +363,31 @@ def single_gpu(args):
     print(json.dumps(out))
 
 
+def leg_c2_dists(args, R, x, dev, peak, cores, do_cpu):
+    """C2's other distributions: n = 2^28 Normal(0, 1) and Zipf(1.1) from the
+    reference's own generators (rtk_generate == rtk::generate, datagen.hpp:71-104), k = 2^20,
+    written over the headline's device buffer; the reference engine timed on the same input."""
+    from paper_2501_14336_b200 import report as REP
+    n, k = 1 << args.logn, args.k
+    res = {}
+    for kind, spec in (("normal", REP.DistributionSpec(kind="normal", a=0.0, b=1.0, seed=2, n=n)),
+                       ("zipf", REP.DistributionSpec(kind="zipf", s=1.1, seed=3, n=n))):
+        import torch
+        hx = REP.generate(spec)
+        x.copy_(torch.from_numpy(hx))
+        b = R.bench_topk(x, k, max(5, args.steps // 2), 3)
+        e = {"ms": b.median_ms, "host_ms": b.median_host_ms, "GBps": gbs(4 * n, k, b.median_ms),
+             "fraction_of_hbm_peak": gbs(4 * n, k, b.median_ms) / peak,
+             "config": f"n=2^{args.logn} rtk::generate {kind} seed {spec.seed}, k={k}"}
+        if do_cpu:
+            t = cpu_topk(hx, k, 1, cores)
+            e["cpu_baseline"] = {"ms": t * 1e3, "GBps": gbs(4 * n, k, t * 1e3), "cores": cores, "kind": "reference",
+                                 "sample": "same input, rtk::topk grid_size=cores, one call"}
+        res[kind] = e
+        del hx
+    return res
+
+
 def leg_c1(args, R, dev, flush, peak, cores, do_cpu):
     """C1 (BASELINE configs[0]): n = 2^20 Uniform[0,1), k = 256 — launch/latency-bound (4 MB);
     L2 flushed before every step outside the clocks."""
@@ -389,8 +418,9 @@ def leg_c3(args, R, dev, flush, peak, cores, do_cpu):
     hl = np.random.default_rng(3).standard_normal((B, V), dtype=np.float32)
     logits = torch.from_numpy(hl).to(dev)
     lb = logits.to(torch.bfloat16)
-    res = {"config": f"{B} x {V} PCG64(3) N(0,1) fp32 logits (bf16: the same rounded); L2 flushed before "
-                     "each step", "f32": {}, "bf16": {}, "sampling": {}}
+    res = {"config": f"{B} x {V} PCG64(3) N(0,1) fp32 logits (bf16: the same rounded); peaked: rtk::generate "
+                     "Peaked mass 0.8, modes 1 + t % 2, seed 100 + t per row; L2 flushed before each step",
+           "f32": {}, "bf16": {}, "sampling": {}}
     for kb in [min(int(v), V) for v in args.batch_ks.split(",") if v]:
         b = R.bench_batch_dense(logits, kb, max(5, args.steps // 2), 3, flush)
         byts = B * (4 * V + 12 * kb)
@@ -410,6 +440,24 @@ def leg_c3(args, R, dev, flush, peak, cores, do_cpu):
                                 "queries_per_s": B / (bh.median_ms * 1e-3),
                                 "effective_GBps": byts / (bh.median_ms * 1e-3) / 1e9,
                                 "fraction_of_hbm_peak": byts / (bh.median_ms * 1e-3) / 1e9 / peak}
+    # Peaked rows (DistKind::Peaked, mass 0.8, modes 1-2, datagen.hpp:93-104)
+    from paper_2501_14336_b200 import report as REP
+    hp = np.stack([REP.generate(REP.DistributionSpec(kind="peaked", mass=0.8, modes=1 + t % 2, seed=100 + t, n=V))
+                   for t in range(B)])
+    peaked = torch.from_numpy(hp).to(dev)
+    res["peaked"] = {}
+    for kb in [min(int(v), V) for v in args.batch_ks.split(",") if v]:
+        b = R.bench_batch_dense(peaked, kb, max(5, args.steps // 2), 3, flush)
+        byts = B * (4 * V + 12 * kb)
+        e = {"ms": b.median_ms, "queries_per_s": B / (b.median_ms * 1e-3),
+             "fraction_of_hbm_peak": byts / (b.median_ms * 1e-3) / 1e9 / peak}
+        if do_cpu and kb <= 8192:
+            t, _ = _timed(lambda: O.ref_batch_topk(hp.reshape(-1), [i * V for i in range(B)], [V] * B, [kb] * B,
+                                                   0, 12, cores), 1)
+            e["cpu_baseline"] = {"ms": t * 1e3, "queries_per_s": B / t, "cores": cores, "kind": "reference",
+                                 "sample": "same rows, rtk::batch_topk grid_size=cores, one call"}
+        res["peaked"][str(kb)] = e
+    del peaked
     # LLM sampling consumer: top-k -> softmax -> top-p -> one draw per row
     u = torch.rand(B, device=dev, generator=torch.Generator(device=dev).manual_seed(4))
     for kb, tp in ((50, 0.9), (4096, 0.95)):

@@ -41,7 +41,7 @@ struct RowSel {
     unsigned int pos;            // low bit of the next digit
     unsigned int status;         // 0 active, 1 resolved, 2 rank error
     unsigned int ticket;         // CTAs that finished this pass
-    unsigned int pad;
+    unsigned int passes;         // digit passes this row took
 };
 
 // Per-launch row list (device arrays). Launch row j maps to state row rid[j].

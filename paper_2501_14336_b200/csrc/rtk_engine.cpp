@@ -1106,9 +1106,11 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
         ++stats.kernel_launches;
     }
     check(cudaMemsetAsync(ghist_.p, 0, 8ull * kBins * R, s), "memset");
-    std::vector<RowSel> st(R);
-    for (int pass = 0; pass < 6 && !active.empty(); ++pass) {
-        const int RA = static_cast<int>(active.size());
+    // Device-driven passes (radix_select's loop, engine.hpp:293-312): the at most six digit
+    // windows of the 64-bit composite are launched back to back with no host round trip; each
+    // pass skips rows that already resolved (RowSel::status, set by the pass's last CTA with the
+    // early stop count_ge <= target), so only one readback follows all of them.
+    {
         std::vector<uint64_t> off, len, tiles{0};
         std::vector<uint32_t> lead;
         for (uint32_t r : active) {
@@ -1116,34 +1118,32 @@ void Engine::fallback(const uint32_t* d_base, const InputSrc& src, const std::ve
             len.push_back(rows[r].n);
             lead.push_back(static_cast<uint32_t>((base_words + rows[r].in_off) & 7));
             tiles.push_back(tiles.back() + ceil_div(lead.back() + rows[r].n, kTile));
-            stats.elements_scanned += rows[r].n;
         }
         Plan P;
         const size_t o_rid = P.add(active), o_off = P.add(off), o_len = P.add(len),
                      o_lead = P.add(lead), o_tile = P.add(tiles);
         uint8_t* D = upload(P, s);
-        Rows rr{RA, at<uint32_t>(D, o_rid), at<uint64_t>(D, o_off), at<uint64_t>(D, o_len),
+        Rows rr{static_cast<int>(active.size()), at<uint32_t>(D, o_rid), at<uint64_t>(D, o_off), at<uint64_t>(D, o_len),
                 at<uint32_t>(D, o_lead), at<uint64_t>(D, o_tile)};
-        launch_radix_pass(0, tiles.back(), rr, src, nullptr, sel_.as<RowSel>(),
-                          ghist_.as<unsigned long long>(), s);
-        ++stats.passes;
-        ++stats.kernel_launches;
-        for (uint32_t r : active) ++row_passes_[r];
-        check(cudaMemcpyAsync(st.data(), sel_.p, sizeof(RowSel) * R, cudaMemcpyDeviceToHost, s), "d2h");
-        sync(s, "fallback pass");
-        std::vector<uint32_t> still;
-        for (uint32_t r : active) {
-            if (st[r].status == 2) throw Error{RTK_INVARIANT_VIOLATION, "select_bin: rank outside histogram total"};
-            if (st[r].status == 0) still.push_back(r);
+        for (int pass = 0; pass < 6; ++pass) {
+            launch_radix_pass(0, tiles.back(), rr, src, nullptr, sel_.as<RowSel>(), ghist_.as<unsigned long long>(), s);
+            ++stats.kernel_launches;
         }
-        active.swap(still);
     }
-    if (!active.empty()) throw Error{RTK_INVARIANT_VIOLATION, "radix select did not resolve"};
+    std::vector<RowSel> st(R);
+    std::vector<uint64_t> T(R);
+    check(cudaMemcpyAsync(st.data(), sel_.p, sizeof(RowSel) * R, cudaMemcpyDeviceToHost, s), "d2h");
+    check(cudaMemcpyAsync(T.data(), T_.p, 8 * R, cudaMemcpyDeviceToHost, s), "d2h");
+    sync(s, "exact path passes");
+    for (uint32_t r : active) {
+        if (st[r].status == 2) throw Error{RTK_INVARIANT_VIOLATION, "select_bin: rank outside histogram total"};
+        if (st[r].status != 1) throw Error{RTK_INVARIANT_VIOLATION, "radix select did not resolve"};
+        stats.passes += st[r].passes;
+        stats.elements_scanned += rows[r].n * st[r].passes;
+        row_passes_[r] += st[r].passes;
+    }
 
     // thresholds are full composites now; candidates get fresh regions at the buffer end
-    std::vector<uint64_t> T(R);
-    check(cudaMemcpyAsync(T.data(), T_.p, 8 * R, cudaMemcpyDeviceToHost, s), "d2h");
-    sync(s, "T");
     std::vector<uint64_t> expect(R, 0);
     std::vector<uint64_t> off, len, tiles{0};
     std::vector<uint32_t> lead;

@@ -49,7 +49,7 @@ __global__ void k_init_sel(int R, const uint32_t* rid, const uint64_t* k, const 
     s.pos = 53;
     s.status = 0;
     s.ticket = 0;
-    s.pad = 0;
+    s.passes = 0;
     sel[rid[j]] = s;
 }
 
@@ -99,6 +99,7 @@ __device__ void select_in_block(RowSel* sp, unsigned long long* gh) {
         } else {
             const unsigned int pos = sp->pos;
             const unsigned long long bin = s_res[0];
+            ++sp->passes;
             sp->prefix |= bin << pos;
             sp->above += s_res[1];
             sp->k_rem = k_rem - s_res[1];
