@@ -205,11 +205,16 @@ def c5_config(args, world):
 
 
 # ---- self-launch for --gpus N ------------------------------------------------------------------
-def self_launch(args) -> int:
+def _free_port() -> int:
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
+    return port
+
+
+def self_launch(args) -> int:
+    port = _free_port()
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
@@ -235,6 +240,8 @@ def main():
     ap.add_argument("--batch-ks", type=str, default="50,4096,128256")
     ap.add_argument("--batch-rows", type=int, default=256)
     ap.add_argument("--vocab", type=int, default=128256)
+    ap.add_argument("--sharded-1gpu", action="store_true",
+                    help="run the N > 1 code path (C5 shards, rtk_topk_sharded over NCCL) with one rank")
     args = ap.parse_args()
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
@@ -248,7 +255,12 @@ def main():
     if args.impl == "reference":
         reference_arm(args, world, rank)
         return
-    if world > 1:
+    if world > 1 or args.sharded_1gpu:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(_free_port()))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         multi_gpu(args, rank, world, local)
     else:
         single_gpu(args)

@@ -110,3 +110,18 @@ def test_cpp_header_compiles_against_the_library(tmp_path):
                         "-L", os.path.join(ROOT, "paper_2501_14336_b200"), "-lrtk_b200", "-L", ref, "-lrtk_ref"],
                        capture_output=True, text=True, timeout=300)
     assert p.returncode == 0, p.stderr[-3000:]
+
+
+def test_bench_reference_arm_contract():
+    # bench.py --impl reference: one JSON line with the contract's keys (tiny workload on CPU)
+    import json
+    import sys
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--logn", "16",
+                        "--k", "256", "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    d = json.loads(p.stdout.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "higher_is_better", "config",
+                "cpu_baseline", "e2e"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "reference"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["config"]["n"] == 1 << 16

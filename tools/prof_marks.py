@@ -1,5 +1,5 @@
 """Per-phase device times (RTK_PROFILE=1 event marks, printed by the engine to stderr) of one
-workload: python tools/prof_marks.py c2|c1|c3|c4 [k] — run with RTK_PROFILE=1 (and any other RTK_*
+workload: python tools/prof_marks.py c2|c1|c3|c4|samp [k] — run with RTK_PROFILE=1 (and any other RTK_*
 switch) in the environment."""
 import os
 import sys
@@ -25,6 +25,11 @@ elif which == "c3":
         x = x.to(torch.bfloat16)
     for _ in range(3):
         rtk.batch_topk_dense(x, k or 50)
+elif which == "samp":  # the LLM sampling consumer on the C3 logits (top-k -> softmax -> top-p -> draw)
+    x = torch.from_numpy(np.random.default_rng(3).standard_normal((256, 128256), dtype=np.float32)).to(dev)
+    u = torch.rand(256, device=dev)
+    for _ in range(3):
+        R.topk_sample(x, k or 50, top_p=0.9, uniform=u)
 elif which == "c4":
     n = 1 << 26
     x = torch.from_numpy((np.float32(128.6) + np.float32(0.1) * np.random.default_rng(5).random(n, dtype=np.float32))).to(dev)

@@ -10,6 +10,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 fi
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference_arm.json 2> $O/bench_ref.err; echo "ref rc=$?"
+NCCL_DEBUG=INFO timeout 600 python bench.py --sharded-1gpu --steps 10 --warmup 3 > $O/bench_sharded_1gpu.json 2> $O/bench_sharded.err; echo "sharded rc=$?"
+grep -E "NCCL INFO (comm|nranks|Init)" $O/bench_sharded.err | head -5 > $O/nccl_info.txt
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum
 launches() { local name=$1; shift; timeout 600 ncu --metrics $M --clock-control none --csv --log-file $O/launches_$name.csv "$@" > /dev/null 2>&1; echo "launches $name rc=$?"; }
 launches c2_k2p20 env RTK_MSD_Q=1 python tools/prof_marks.py c2 1048576
@@ -34,8 +36,11 @@ cap rows50 "k_rows_fused" 1 1 python tools/prof_marks.py c3 50
 cap rows4096 "k_rows_fused" 1 1 python tools/prof_marks.py c3 4096
 cap lsd "k_lsd_pass" 1 1 python tools/prof_marks.py c3 128256
 cap compact_c4a "k_compact" 1 1 env MODE=2 python tools/prof_marks.py c4
-# the shipped multi-cluster level-0 MSD (cooperative launch, grid barrier): application replay
+cap radix_exact "k_radix_pass" 1 1 env RTK_FORCE_EXACT=1 python tools/prof_marks.py c1 256
+cap sample_rows "k_sample_rows" 1 1 python tools/prof_marks.py samp 50
+# the shipped multi-cluster level-0 MSD (cooperative launch, grid barrier): application replay,
+# no graph capture (every call launches it directly)
 timeout 900 ncu --set full --replay-mode application --clock-control none --import-source on -k regex:"k_msd_cluster" -s 1 -c 1 \
-  -o /tmp/ncu/msd_q16 -f python tools/prof_marks.py c2 1048576 > /tmp/ncu/msd_q16.log 2>&1; echo "cap msd_q16 rc=$?"
+  -o /tmp/ncu/msd_q16 -f env RTK_GRAPHS=0 python tools/prof_marks.py c2 1048576 > /tmp/ncu/msd_q16.log 2>&1; echo "cap msd_q16 rc=$?"
 python tools/ncu_summary.py /tmp/ncu/msd_q16.ncu-rep 25 > $O/ncu_msd_q16.txt 2>&1
 tail -3 /tmp/ncu/msd_q16.log >> $O/ncu_msd_q16.txt
