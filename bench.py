@@ -217,6 +217,7 @@ def self_launch(args) -> int:
     port = _free_port()
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries the one JSON line only
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
     return subprocess.run(cmd, env=env).returncode

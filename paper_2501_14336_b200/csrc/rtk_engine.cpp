@@ -1298,8 +1298,7 @@ void Engine::remap(uint64_t k, const uint64_t* d_cand_idx, const std::vector<uin
     uint8_t* D = upload(P, s);
     launch_remap_idx(k, d_cand_idx, static_cast<uint32_t>(block_start.size()), at<uint64_t>(D, o_bs),
                      at<uint64_t>(D, o_sb), d_idx, s);
-    sync(s, "remap");
-    release_retired();
+    check(cudaGetLastError(), "remap launch");  // stream-ordered: no host synchronisation
 }
 
 }  // namespace rtk_b200

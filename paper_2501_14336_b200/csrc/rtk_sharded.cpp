@@ -122,6 +122,14 @@ void topk_sharded(Engine* const* engines, ShardWork* const* work, void* const* c
         nccl_check(api.CommUserRank(static_cast<ncclComm_t>(comms[i]), &rank[i]), "ncclCommUserRank");
         if (cnt != world) throw Error{RTK_INVALID_ARGUMENT, "topk_sharded: communicator size != number of shards"};
     }
+    if (world == 1) {  // one rank: the shard is the query, its top-k the result (no exchange)
+        DeviceGuard dg(engines[0]->device());
+        engines[0]->run(static_cast<const uint32_t*>(d_shards[0]), dtype, order, false, 0.0f, false,
+                        {RowReq{0, shard_n[0], k, 0}}, static_cast<uint32_t*>(d_out_vals[0]), d_out_idx[0],
+                        static_cast<uint32_t*>(d_out_pivots ? d_out_pivots[0] : nullptr),
+                        static_cast<cudaStream_t>(streams ? streams[0] : nullptr));
+        return;
+    }
     // 1. local top-k of every local shard into its send slot (values | u64 local indices)
     for (int i = 0; i < L; ++i) {
         const int r = rank[i];

@@ -10,7 +10,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 fi
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference_arm.json 2> $O/bench_ref.err; echo "ref rc=$?"
-NCCL_DEBUG=INFO timeout 600 python bench.py --sharded-1gpu --steps 10 --warmup 3 > $O/bench_sharded_1gpu.json 2> $O/bench_sharded.err; echo "sharded rc=$?"
+NCCL_DEBUG=INFO NCCL_DEBUG_FILE=/dev/stderr timeout 600 python bench.py --sharded-1gpu --steps 10 --warmup 3 > $O/bench_sharded_1gpu.json 2> $O/bench_sharded.err; echo "sharded rc=$?"
 grep -E "NCCL INFO (comm|nranks|Init)" $O/bench_sharded.err | head -5 > $O/nccl_info.txt
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum
 launches() { local name=$1; shift; timeout 600 ncu --metrics $M --clock-control none --csv --log-file $O/launches_$name.csv "$@" > /dev/null 2>&1; echo "launches $name rc=$?"; }
