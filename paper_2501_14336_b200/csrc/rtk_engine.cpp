@@ -117,6 +117,7 @@ Engine::~Engine() {
     if (hcount_) cudaFreeHost(hcount_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
+    if (pin_ev_) cudaEventDestroy(pin_ev_);
     for (DevBuf* b : {&arena_, &sel_, &T_, &count_, &kmin_, &kmax_, &kor_, &ghist_, &samples_, &cand_a_,
                       &cand_b_, &seg_hist_, &gcursor_, &bstart_, &dcap_, &dcoff_, &ctl_, &row_fail_, &groups_, &slots0_, &slotsA_, &slotsB_, &done_, &seg_ticket_, &wgroups_, &ctot_, &sig_, &io_in, &io_vals, &io_idx,
                       &io_piv, &io_aux, &adapt_buf_, &scale_hist_, &scale_plan_})
@@ -124,6 +125,10 @@ Engine::~Engine() {
 }
 
 uint8_t* Engine::upload(const Plan& p, cudaStream_t s) {
+    if (pin_ev_pending_) {  // a stream-ordered remap's plan copy may still read the pinned staging
+        check(cudaEventSynchronize(pin_ev_), "remap plan copy");
+        pin_ev_pending_ = false;
+    }
     const size_t need = (p.bytes.size() + 255) & ~size_t(255);
     if (arena_used_ + need > arena_.cap) {
         // earlier plan regions may still be referenced by queued kernels and by pointers the
@@ -1298,7 +1303,12 @@ void Engine::remap(uint64_t k, const uint64_t* d_cand_idx, const std::vector<uin
     uint8_t* D = upload(P, s);
     launch_remap_idx(k, d_cand_idx, static_cast<uint32_t>(block_start.size()), at<uint64_t>(D, o_bs),
                      at<uint64_t>(D, o_sb), d_idx, s);
-    check(cudaGetLastError(), "remap launch");  // stream-ordered: no host synchronisation
+    check(cudaGetLastError(), "remap launch");
+    // stream-ordered, no host synchronisation: the next plan upload waits for this one's pinned
+    // staging to be consumed before it rewrites it (upload())
+    if (!pin_ev_) check(cudaEventCreateWithFlags(&pin_ev_, cudaEventDisableTiming), "event");
+    check(cudaEventRecord(pin_ev_, s), "event");
+    pin_ev_pending_ = true;
 }
 
 }  // namespace rtk_b200

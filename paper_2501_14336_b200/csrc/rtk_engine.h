@@ -283,6 +283,8 @@ private:
     DevBuf arena_;
     size_t arena_used_ = 0;
     std::vector<DevBuf> retired_;
+    cudaEvent_t pin_ev_ = nullptr;  // recorded after a stream-ordered remap's plan upload
+    bool pin_ev_pending_ = false;
     uint8_t* pin_ = nullptr;       // pinned staging for plan uploads
     size_t pin_cap_ = 0, pin_used_ = 0;
     std::vector<uint8_t*> retired_pinned_;
