@@ -36,7 +36,7 @@ constexpr int kLsdWarps = kLsdThreads / 32;
 #define RTK_LSD_ITEMS 16
 #endif
 #ifndef RTK_LSD_MINB
-#define RTK_LSD_MINB 3
+#define RTK_LSD_MINB 4
 #endif
 constexpr int kLsdItems = RTK_LSD_ITEMS;
 constexpr int kLsdTile = kLsdThreads * kLsdItems;  // 4096 elements
