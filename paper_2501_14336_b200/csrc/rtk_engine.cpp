@@ -81,6 +81,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_GRAPH_EVENTS")) no_graph_events_ = *g == '0';
     if (const char* g = std::getenv("RTK_PREFETCH_MB")) prefetch_mb_ = std::max(0, std::atoi(g));
     if (const char* g = std::getenv("RTK_NO_FUSED")) no_fused_ = *g && *g != '0';
+    if (const char* g = std::getenv("RTK_NO_RCLUSTER")) no_rcluster_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_NO_DENSE")) no_dense_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_SPARSE_MAX")) sparse_max_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_SPARSE_SEL")) sparse_sel_ = std::atoi(g);
@@ -465,11 +466,18 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     // K6 routing: short rows with small k finish in one CTA each (k_rows_fused); the rest take
     // the general multi-CTA pipeline (sampled threshold -> k_compact -> MSD -> sort groups)
     std::vector<uint32_t> grow, frow[2];
+    bool row_cluster = false;  // the one row goes to k_row_cluster (frow[1] holds it)
     std::vector<uint64_t> f_off[2], f_len[2], f_k[2];
     // returns -1 (general path), 0 (large-buffer fused variant) or 1 (small-buffer variant)
     auto fused_class = [&](const RowReq& q) {
         if (no_fused_ || force_exact_) return -1;
         if (q.k == 0 || q.k > rows_fused_kmax(false)) return -1;
+        if (R == 1 && !no_rcluster_ && !trig_count_ && q.n > (uint64_t(1) << 18) && q.n <= (uint64_t(1) << 21) &&
+            q.k <= row_cluster_kmax()) {  // one long query: a 16-CTA cluster (k_row_cluster)
+            const double rr = static_cast<double>(q.k) * 4096.0 / static_cast<double>(q.n);
+            const double rp = std::ceil(rr + 4.0 * std::sqrt(rr) + 3.0);
+            if (static_cast<double>(q.n) / 4096.0 * (rp + 5.0 * std::sqrt(rp)) <= 8192.0) return 2;
+        }
         if (q.n > (uint64_t(1) << 18) && R < 64) return -1;  // long rows want many CTAs
         for (int small = 1; small >= 0; --small) {
             if (q.k > rows_fused_kmax(small)) continue;
@@ -496,7 +504,11 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
         row_k[r] = q.k;
         row_out[r] = q.out_off;
         row_in[r] = q.in_off;
-        const int fc = fused_class(q);
+        int fc = fused_class(q);
+        if (fc == 2) {
+            row_cluster = true;
+            fc = 1;
+        }
         if (fc >= 0) {
             frow[fc].push_back(r);
             f_off[fc].push_back(q.in_off);
@@ -680,7 +692,8 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
             cudaMemsetAsync(trace_.p, 0, nfr * 16 * sizeof(unsigned long long), s);
             fa.trace = trace_.as<unsigned long long>();
         }
-        launch_rows_fused(static_cast<int>(nfr), fa, v == 1, s);
+        if (v == 1 && row_cluster) launch_row_cluster(fa, s);
+        else launch_rows_fused(static_cast<int>(nfr), fa, v == 1, s);
         ++stats.kernel_launches;
         if (rows_trace_) report_rows_trace(nfr, s);
         if (fa.tail.hflags) {

@@ -255,6 +255,7 @@ private:
     std::vector<uint64_t> row_passes_;
     uint32_t level0_bits() const { return force_deep_ ? 6u : static_cast<uint32_t>(msd_max_bits_); }
     bool no_fused_ = false;
+    bool no_rcluster_ = false;  // RTK_NO_RCLUSTER=1: single long rows take the general path
     bool no_dense_ = false;
     int sparse_max_ = 96;            // RTK_SPARSE_MAX (k_compact sparse-hit path threshold)
     int lsd_mode_ = 2;               // RTK_LSD: dense rows' LSD sort: 0 off (MSD + bucket sorts), 1 16-bit keys, 2 all

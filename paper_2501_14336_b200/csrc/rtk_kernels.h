@@ -327,6 +327,9 @@ struct LsdArgs {  // dense rows: segmented one-sweep LSD radix sort (rtk_lsd.cu)
 uint32_t lsd_tile();
 void launch_lsd(uint64_t tiles, const LsdArgs& a, cudaStream_t s);
 void launch_rows_fused(int R, const RowsFusedArgs& a, bool small, cudaStream_t s);
+// one long row (2^18 < n <= 2^21, k <= row_cluster_kmax()) on one 16-CTA cluster (rtk_rows.cu)
+void launch_row_cluster(const RowsFusedArgs& a, cudaStream_t s);
+uint32_t row_cluster_kmax();
 uint32_t rows_fused_kmax(bool small);
 uint32_t rows_fused_cand(bool small);
 uint32_t rows_fused_sample(bool small);

@@ -11,6 +11,7 @@
 // buffer is flagged and rerun by the host on the general multi-CTA path; correctness never
 // depends on the sample. The reference's per-task semantics (batch.hpp:284-291: each task
 // equals rtk::topk on its view) hold row by row.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "rtk_device.cuh"
@@ -743,6 +744,313 @@ static void rows_variant(int R, const RowsFusedArgs& a, cudaStream_t s) {
         default: rows_km<kKmU32S, CAND, STAGES, SAMPLE, UU>(R, a, s); break;
     }
 }
+
+// ---- one long row on a cluster (K6 for single queries, BASELINE C1) ----------------------------
+// A single query with 2^18 < n <= 2^21 and k <= 512 is owned by ONE thread-block cluster of
+// kRcCs CTAs instead of the four-kernel general path (sample, compaction, MSD, sort): CTA 0
+// selects the sample threshold T (the one-CTA kernel's stratified sample + in-CTA radix select)
+// while the other CTAs pull their contiguous slices into L2; after a cluster barrier every CTA
+// streams its slice once and appends K >= T to CTA 0's shared candidate buffer through
+// distributed shared memory (one remote atomic per warp, remote stores of the hits); after a
+// second barrier CTA 0 selects exactly k (in-CTA radix select) and sorts them (one warp, in
+// registers). A missed sample or an overflow flags the row for the exact path, as k_rows_fused.
+// Sorts buf[0, m) (m <= kRowThreads, distinct composites) descending into out[0, m) by rank:
+// element i lands at #{j : buf[j] > buf[i]}. P = kRowThreads / pow2ceil(m) threads share one
+// element, each counting over j = part (mod P) — consecutive words, no bank conflicts — and
+// combine by shuffles. One smem broadcast read per comparison, no barrier per stage.
+__device__ __forceinline__ void rank_sort_desc(const unsigned long long* buf, uint32_t m,
+                                               unsigned long long* out) {
+    uint32_t n2 = 1;
+    while (n2 < m) n2 <<= 1;
+    const uint32_t P = n2 >= kRowThreads ? 1u : kRowThreads / n2;  // <= 512, power of two
+    const uint32_t Pw = P > 32 ? 32u : P;                           // lanes combined per element
+    const uint32_t tid = threadIdx.x;
+    const uint32_t i = tid / Pw, part = tid % Pw;
+    const unsigned long long me = i < m ? buf[i] : 0ull;
+    uint32_t cnt = 0;
+    if (i < m) {
+        uint32_t j = part;
+        for (; j + 7 * Pw < m; j += 8 * Pw) {
+            unsigned long long b[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) b[q] = buf[j + q * Pw];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) cnt += b[q] > me;
+        }
+        for (; j < m; j += Pw) cnt += buf[j] > me;
+    }
+    for (uint32_t d = 1; d < Pw; d <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+    if (i < m && part == 0) out[cnt] = me;
+    __syncthreads();
+}
+
+constexpr int kRcCs = 16;
+constexpr int kRcCand = 8192;
+constexpr int kRcSample = 4096;
+constexpr int kRcU = 8;  // 16-byte loads in flight per thread in the streaming pass
+
+template <int KM>
+__global__ void __cluster_dims__(kRcCs, 1, 1) __launch_bounds__(kRowThreads, 1) k_row_cluster(RowsFusedArgs a) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ unsigned long long cand[];  // kRcCand; CTA 0's is the row's candidate buffer
+    __shared__ uint32_t hist[kBins];
+    __shared__ uint32_t s_w[kRowWarps];
+    __shared__ unsigned long long s_res[3];
+    __shared__ uint32_t s_m;
+    __shared__ unsigned long long s_T;
+    __shared__ uint32_t s_tail;
+    resolve_src(a.in);
+    const uint32_t crank = cluster.block_rank();
+    int ntr = 0;
+    auto stamp = [&]() {  // RTK_ROWS_TRACE: CTA 0's phase ends (globaltimer)
+        if (a.trace && crank == 0 && threadIdx.x == 0 && ntr < 15) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            a.trace[ntr++] = t;
+        }
+    };
+    stamp();
+    const int tid = threadIdx.x, lane = tid & 31;
+    const unsigned full = 0xffffffffu;
+    const uint32_t r = a.rid[0];
+    const uint64_t n = a.len[0], off = a.off[0], k = a.k[0];
+    constexpr int EB = km_is16<KM>() ? 2 : 4;
+    const char* rowb = reinterpret_cast<const char*>(a.in.base) + off * EB;
+    auto ld = [&](uint64_t i) -> uint32_t {
+        if constexpr (EB == 2) return __ldg(reinterpret_cast<const unsigned short*>(rowb) + i);
+        else return __ldg(reinterpret_cast<const uint32_t*>(rowb) + i);
+    };
+    // 16-byte vectors over the aligned body [a0, a1) of the row, split evenly over the CTAs; the
+    // < VE elements before a0 and after a1 go to the last CTA's first threads
+    constexpr int VE = 16 / EB;
+    const uintptr_t rb = reinterpret_cast<uintptr_t>(rowb);
+    const uint64_t a0 = min(n, static_cast<uint64_t>(((16 - (rb & 15)) & 15) / EB));
+    const uint64_t nv = (n - a0) / VE;
+    const uint64_t a1 = a0 + nv * VE;
+    const uint64_t vper = (nv + kRcCs - 1) / kRcCs;
+    const uint64_t v0 = min(nv, crank * vper), v1 = min(nv, v0 + vper);
+    const uint4* vrow = reinterpret_cast<const uint4*>(rowb + a0 * EB);
+    if (tid == 0) s_m = 0;
+    if (tid < 64) {  // L2 prefetch of this CTA's slice: 64 threads x 16 KB bulk prefetches
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(vrow + v0), hi = reinterpret_cast<uintptr_t>(vrow + v1);
+        for (uintptr_t p = lo + static_cast<uintptr_t>(tid) * 16384; p < hi; p += 64 * 16384) {
+            const uint32_t bytes = static_cast<uint32_t>(hi - p < 16384 ? hi - p : 16384);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+        }
+    }
+    // ---- 1. threshold on CTA 0 (stratified sample, in-CTA radix select of the r'-th) ----------
+    if (crank == 0) {
+        const uint64_t nseg = kRcSample / 32;
+        const uint64_t stride_fp = ((n - 32) << 16) / (nseg - 1);
+        uint32_t raw[kRcSample / kRowThreads];
+#pragma unroll
+        for (int q = 0; q < kRcSample / kRowThreads; ++q) {
+            const int e = q * kRowThreads + tid;
+            raw[q] = ld(((static_cast<uint64_t>(e / 32) * stride_fp) >> 16) + (e & 31));
+        }
+#pragma unroll
+        for (int q = 0; q < kRcSample / kRowThreads; ++q) {
+            const int e = q * kRowThreads + tid;
+            const uint64_t idx = ((static_cast<uint64_t>(e / 32) * stride_fp) >> 16) + (e & 31);
+            cand[e] = composite(key_of<KM>(raw[q], a.in), idx);
+        }
+        __syncthreads();
+        const double rr = static_cast<double>(k) * kRcSample / static_cast<double>(n);
+        const uint64_t rp = static_cast<uint64_t>(ceil(rr + 4.0 * sqrt(rr) + 3.0));
+        uint64_t cge;
+        const uint64_t rpc = rp < kRcSample ? rp : kRcSample;
+        const unsigned long long T = cta_radix_select(cand, kRcSample, rpc, rpc, hist, s_w, s_res, &cge, km_is16<KM>());
+        if (tid == 0) s_T = T;
+        stamp();
+    }
+    cluster.sync();
+    stamp();
+    // ---- 2. stream the slice, hits to CTA 0 through DSMEM ------------------------------------
+    const unsigned long long T = *cluster.map_shared_rank(&s_T, 0);
+    const uint32_t thi = static_cast<uint32_t>(T >> 32);
+    const uint64_t eT = ~static_cast<uint32_t>(T);  // T's element index
+    uint32_t* m0 = cluster.map_shared_rank(&s_m, 0);
+    unsigned long long* cand0 = cluster.map_shared_rank(cand, 0);
+    // one warp's hits (bit i of mask: element e_of(i) with key[i]) appended to CTA 0's buffer
+    auto append = [&](const auto& key, uint32_t mask, auto e_of) {
+        constexpr int NK = sizeof(key) / sizeof(key[0]);
+        const uint32_t c = __popc(mask);
+        uint32_t inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(full, inc, d);
+            if (lane >= d) inc += o;
+        }
+        const uint32_t wtot = __shfl_sync(full, inc, 31);
+        uint32_t wbase = 0;
+        if (lane == 31) wbase = atomicAdd(m0, wtot);
+        wbase = __shfl_sync(full, wbase, 31);
+        uint32_t o = wbase + inc - c;
+#pragma unroll
+        for (int i = 0; i < NK; ++i)
+            if ((mask >> i) & 1u) {
+                if (o < static_cast<uint32_t>(kRcCand)) cand0[o] = composite(key[i], e_of(i));
+                ++o;
+            }
+    };
+    constexpr int NE = kRcU * VE;  // elements per thread per step (32)
+    for (uint64_t vb = v0; vb < v1; vb += static_cast<uint64_t>(kRcU) * kRowThreads) {
+        uint4 w[kRcU];
+#pragma unroll
+        for (int u = 0; u < kRcU; ++u) {
+            const uint64_t v = vb + static_cast<uint64_t>(u) * kRowThreads + tid;
+            w[u] = v < v1 ? __ldg(vrow + v) : make_uint4(0u, 0u, 0u, 0u);
+        }
+        uint32_t key[NE];
+        uint32_t mask = 0;
+        // ties at T's key (index eT) are hits iff their index <= eT: decided once for the whole
+        // step unless the step's index range straddles eT (at most one step per row)
+        const uint64_t lo_e = a0 + vb * VE, hi_e = a0 + (vb + static_cast<uint64_t>(kRcU) * kRowThreads) * VE - 1;
+        if (hi_e <= eT || lo_e > eT) {
+            const bool tie_in = hi_e <= eT;
+            if (!tie_in && thi == 0xffffffffu) continue;  // nothing above T's key
+            const uint32_t ge = tie_in ? thi : thi + 1;
+#pragma unroll
+            for (int u = 0; u < kRcU; ++u) {
+                const bool ok = vb + static_cast<uint64_t>(u) * kRowThreads + tid < v1;
+                const uint32_t wd[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+                for (int j = 0; j < VE; ++j) {
+                    const uint32_t rawk = EB == 2 ? (wd[j / 2] >> (16 * (j & 1))) & 0xffffu : wd[j];
+                    const int i = u * VE + j;
+                    key[i] = key_of<KM>(rawk, a.in);
+                    mask |= static_cast<uint32_t>(ok && key[i] >= ge) << i;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < kRcU; ++u) {
+                const uint64_t v = vb + static_cast<uint64_t>(u) * kRowThreads + tid;
+                const uint32_t wd[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+                for (int j = 0; j < VE; ++j) {
+                    const uint32_t rawk = EB == 2 ? (wd[j / 2] >> (16 * (j & 1))) & 0xffffu : wd[j];
+                    const int i = u * VE + j;
+                    key[i] = key_of<KM>(rawk, a.in);
+                    mask |= static_cast<uint32_t>(v < v1 && composite(key[i], a0 + v * VE + j) >= T) << i;
+                }
+            }
+        }
+        if (!__any_sync(full, mask)) continue;
+        append(key, mask, [&](int i) {
+            return a0 + (vb + static_cast<uint64_t>(i / VE) * kRowThreads + tid) * VE + (i % VE);
+        });
+    }
+    if (crank == kRcCs - 1 && tid < 32) {  // head [0, a0) and tail [a1, n): < 2 VE elements
+        const uint64_t nh = a0, nt = n - a1;
+        const bool in = static_cast<uint64_t>(lane) < nh + nt;
+        const uint64_t e = lane < nh ? lane : a1 + (lane - nh);
+        uint32_t key[1];
+        key[0] = in ? key_of<KM>(ld(e), a.in) : 0u;
+        const uint32_t mask = static_cast<uint32_t>(in && composite(key[0], e) >= T);
+        if (__any_sync(full, mask)) append(key, mask, [&](int) { return e; });
+    }
+    stamp();
+    cluster.sync();
+    stamp();
+    // ---- 3. CTA 0: exactly k, sorted, written -------------------------------------------------
+    if (crank == 0) {
+        const uint32_t m = s_m;
+        if (m < k || m > static_cast<uint32_t>(kRcCand)) {  // sample missed / overflow: exact path
+            if (tid == 0) {
+                a.row_fail[r] = 1;
+                atomicOr(a.flags, kFlagFail);
+            }
+        } else {
+            if (m > k) {
+                uint64_t cge;
+                const unsigned long long T2 = cta_radix_select(cand, m, k, k, hist, s_w, s_res, &cge, km_is16<KM>());
+                constexpr int PT = kRcCand / kRowThreads;
+                unsigned long long keep[PT];
+                uint32_t km = 0;
+#pragma unroll
+                for (int q = 0; q < PT; ++q) {
+                    const uint32_t i = q * kRowThreads + tid;
+                    keep[q] = i < m ? cand[i] : 0ull;
+                    km |= static_cast<uint32_t>(i < m && keep[q] >= T2) << q;
+                }
+                if (tid == 0) s_m = 0;
+                __syncthreads();
+                const uint32_t c = __popc(km);
+                uint32_t inc = c;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o2 = __shfl_up_sync(full, inc, d);
+                    if (lane >= d) inc += o2;
+                }
+                const uint32_t wtot = __shfl_sync(full, inc, 31);
+                uint32_t wbase = 0;
+                if (lane == 31 && wtot) wbase = atomicAdd(&s_m, wtot);
+                wbase = __shfl_sync(full, wbase, 31);
+                uint32_t o = wbase + inc - c;
+#pragma unroll
+                for (int q = 0; q < PT; ++q)
+                    if ((km >> q) & 1u) cand[o++] = keep[q];
+                __syncthreads();
+            }
+            stamp();
+            const uint32_t kk = static_cast<uint32_t>(k);
+            unsigned long long* sorted = cand + kRcCand / 2;
+            rank_sort_desc(cand, kk, sorted);
+            stamp();
+            const uint64_t oo = a.row_out_off[r];
+            for (uint32_t p = tid; p < kk; p += kRowThreads) {
+                const unsigned long long K = sorted[p];
+                const uint32_t kv = static_cast<uint32_t>(K >> 32);
+                const uint32_t idx = ~static_cast<uint32_t>(K);
+                uint32_t val;
+                if (a.in.scaled) val = ld(idx);
+                else if (a.in.dtype == kF32) val = decode_f32_bits(kv, a.in.smallest);
+                else if (a.in.dtype == kF16) val = decode_f16_bits(kv, a.in.smallest);
+                else val = a.in.smallest ? ~kv : kv;
+                store_val(a.out_vals, a.in.dtype, oo + p, val);
+                a.out_idx[oo + p] = idx;
+                if (p == kk - 1 && a.pivots) store_val(a.pivots, a.in.dtype, r, val);
+            }
+        }
+    }
+    stamp();
+    if (a.trace && crank == 0 && threadIdx.x == 0) {
+        uint32_t sm;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+        a.trace[15] = sm;
+    }
+    call_tail(a.tail, &s_tail);
+}
+
+template <int KM>
+static void row_cluster_km(const RowsFusedArgs& a, cudaStream_t s) {
+    constexpr size_t smem = kRcCand * sizeof(unsigned long long);
+    static DeviceOnce configured;
+    configured([&] {
+        cudaFuncSetAttribute(k_row_cluster<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaFuncSetAttribute(k_row_cluster<KM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    });
+    k_row_cluster<KM><<<kRcCs, kRowThreads, smem, s>>>(a);
+}
+
+void launch_row_cluster(const RowsFusedArgs& a, cudaStream_t s) {
+    switch (key_mode(a.in.dtype, a.in.smallest, a.in.scaled, a.in.adapt)) {
+        case kKmF32L: row_cluster_km<kKmF32L>(a, s); break;
+        case kKmF32S: row_cluster_km<kKmF32S>(a, s); break;
+        case kKmF32LScaled: row_cluster_km<kKmF32LScaled>(a, s); break;
+        case kKmF32SScaled: row_cluster_km<kKmF32SScaled>(a, s); break;
+        case kKmU32L: row_cluster_km<kKmU32L>(a, s); break;
+        case kKmF16L: row_cluster_km<kKmF16L>(a, s); break;
+        case kKmF32LAdapt: row_cluster_km<kKmF32LAdapt>(a, s); break;
+        case kKmF32SAdapt: row_cluster_km<kKmF32SAdapt>(a, s); break;
+        case kKmF16S: row_cluster_km<kKmF16S>(a, s); break;
+        default: row_cluster_km<kKmU32S>(a, s); break;
+    }
+}
+
+uint32_t row_cluster_kmax() { return kRowKMaxS; }
 
 // small = rows whose k and expected candidate count fit the small-buffer variant
 void launch_rows_fused(int R, const RowsFusedArgs& a, bool small, cudaStream_t s) {

@@ -1,5 +1,5 @@
 """Device time of one workload under the current RTK_* environment (rtk_bench_* C loops, L2
-flushed before each step except C2): python tools/ab_env.py c1|c2|c3|c3b|c4 k [mode]. RTK_PKG_ROOT
+flushed before each step except C2): python tools/ab_env.py tiny|c1|c2|c3|c3b|c4 k [mode]. RTK_PKG_ROOT
 selects another build (tools/build_variant.sh)."""
 import os
 import sys
@@ -13,7 +13,10 @@ from paper_2501_14336_b200 import rtk as R
 which, k = sys.argv[1], int(sys.argv[2])
 dev = torch.device("cuda", 0)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-if which in ("c1", "c2"):
+if which == "tiny":  # the fixed per-call cost: one 1000-element row (one CTA)
+    x = torch.from_numpy(np.random.default_rng(1).random(1000, dtype=np.float32)).to(dev)
+    b = R.bench_topk(x, k, 20, 5, flush=flush)
+elif which in ("c1", "c2"):
     n = 1 << (20 if which == "c1" else 28)
     x = torch.from_numpy(np.random.default_rng(1).random(n, dtype=np.float32)).to(dev)
     b = R.bench_topk(x, k, 20, 5, flush=flush if which == "c1" else None)  # C2: 1 GiB > L2
