@@ -36,6 +36,7 @@ cap rows50 "k_rows_fused" 1 1 python tools/prof_marks.py c3 50
 cap rows4096 "k_rows_fused" 1 1 python tools/prof_marks.py c3 4096
 cap lsd "k_lsd_pass" 1 1 python tools/prof_marks.py c3 128256
 cap compact_c4a "k_compact" 1 1 env MODE=2 python tools/prof_marks.py c4
+cap row_cluster "k_row_cluster" 1 1 python tools/prof_marks.py c1 256
 cap radix_exact "k_radix_pass" 1 1 env RTK_FORCE_EXACT=1 python tools/prof_marks.py c1 256
 cap sample_rows "k_sample_rows" 1 1 python tools/prof_marks.py samp 50
 # the shipped multi-cluster level-0 MSD (cooperative launch, grid barrier): application replay,
