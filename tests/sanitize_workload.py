@@ -24,8 +24,10 @@ def check(got, x, k, order=0, what=""):
 def main():
     dev = torch.device("cuda", 0)
     rng = np.random.default_rng(17)
-    # (1 << 22, 1 << 19): the one-huge-row level-0 MSD over Q co-resident clusters (grid barrier)
-    for n, k in [(3000, 7), (1 << 16, 256), (1 << 17, 50000), (1 << 20, 4096), (1 << 22, 1 << 19)]:
+    # (1 << 22, 1 << 19): the one-huge-row level-0 MSD over Q co-resident clusters (grid barrier);
+    # (1 << 20, 256), (1 << 19 + 5, 512): the single-query cluster kernel (k_row_cluster, DSMEM)
+    for n, k in [(3000, 7), (1 << 16, 256), (1 << 17, 50000), (1 << 20, 4096), (1 << 22, 1 << 19),
+                 (1 << 20, 256), ((1 << 19) + 5, 512)]:
         x = rng.standard_normal(n).astype(np.float32)
         for order in (0, 1):
             check(rtk.topk(torch.from_numpy(x).to(dev), k, rtk.SelectionOrder(order)), x, k, order, f"topk {n} {k}")
