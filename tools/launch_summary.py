@@ -15,7 +15,7 @@ for path in sys.argv[1:]:
     ids = sorted(d)
     # the last call = the launches after the last k_sample_select / k_rows_fused / first kernel of a call
     starts = [i for i in ids if any(s in d[i]["k"] for s in ("k_sample_select", "k_rows_fused", "k_lsd_hist",
-                                                               "k_scale_guess", "k_init_sel"))]
+                                                               "k_scale_guess", "k_init_sel", "k_row_cluster"))]
     first = starts[-1] if starts else ids[0]
     if "k_scale_guess" not in d[first]["k"] and any("k_scale_guess" in d[i]["k"] for i in ids if i < first):
         first = max(i for i in ids if i < first and "k_scale_guess" in d[i]["k"])
