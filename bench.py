@@ -131,6 +131,27 @@ def _timed(fn, reps):
     return statistics.median(ts), ts
 
 
+def torch_topk_ms(fn, steps, flush=None):
+    """Median device time (CUDA events on torch's current stream) of fn() — torch.topk as a timing
+    competitor; its ties are not ordered by index, so it is not a parity oracle."""
+    import statistics
+    import torch
+    for _ in range(3):
+        fn()
+    ts = []
+    for _ in range(steps):
+        if flush is not None:
+            flush.fill_(1)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
 def cpu_topk(x, k, reps, cores):
     import oracle as O
     t, _ = _timed(lambda: O.ref_topk(x, k, 0, 12, cores), reps)
@@ -237,6 +258,7 @@ def main():
     ap.add_argument("--sweep", type=str, default="256,16384", help="extra C2 k values")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-torch-topk", action="store_true", help="skip the torch.topk timing competitor")
     ap.add_argument("--legs", type=str, default="c1,c2dist,c3,c4,c5", help="secondary legs (N = 1)")
     ap.add_argument("--batch-ks", type=str, default="50,4096,128256")
     ap.add_argument("--batch-rows", type=int, default=256)
@@ -312,6 +334,15 @@ def single_gpu(args):
         sweep[str(kk)] = {"ms": bk.median_ms, "host_ms": bk.median_host_ms, "GBps": gbs(4 * n, kk, bk.median_ms),
                           "fraction_of_hbm_peak": gbs(4 * n, kk, bk.median_ms) / peak}
 
+    # ---- torch.topk on the same device-resident inputs (timing competitor) -------
+    competitor = {"note": "torch.topk(sorted=True) on the same tensors, CUDA events, median; ours = this bench's "
+                          "median for the same config"}
+    if not args.no_torch_topk:
+        for kk in [k] + [int(v) for v in args.sweep.split(",") if v]:
+            tm = torch_topk_ms(lambda: torch.topk(x, kk, sorted=True), max(5, args.steps // 2))
+            ours = med if kk == k else sweep[str(kk)]["ms"]
+            competitor[f"c2_k{kk}"] = {"ms": tm, "ours_ms": ours, "speedup": tm / ours}
+
     # ---- e2e through the host entry point (pinned host input, copies inside) ------------------
     hp = torch.from_numpy(hx).pin_memory().numpy()
     R.topk(hp, k)
@@ -340,8 +371,12 @@ def single_gpu(args):
         out_legs["c2_distributions"] = leg_c2_dists(args, R, x, dev, peak, cores, do_cpu)
     if "c1" in legs:
         out_legs["c1"] = leg_c1(args, R, dev, flush, peak, cores, do_cpu)
+        if not args.no_torch_topk:
+            competitor["c1"] = out_legs["c1"].pop("torch_topk")
     if "c3" in legs:
         out_legs["c3"] = leg_c3(args, R, dev, flush, peak, cores, do_cpu)
+        if not args.no_torch_topk:
+            competitor["c3"] = out_legs["c3"].pop("torch_topk")
     if "c4" in legs:
         out_legs["c4"] = leg_c4(args, R, dev, peak, cores, do_cpu)
     if "c5" in legs:
@@ -372,7 +407,7 @@ def single_gpu(args):
                      "first and after its last device operation of the call; host_ms = steady_clock around "
                      "each rtk_topk call (returns after the device's completion signal)",
            "step_ms_all": b.device_ms, "host_ms_all": b.host_ms,
-           "k_sweep": sweep, "legs": out_legs}
+           "k_sweep": sweep, "legs": out_legs, "torch_topk": competitor}
     print(json.dumps(out))
 
 
@@ -417,6 +452,9 @@ def leg_c1(args, R, dev, flush, peak, cores, do_cpu):
         t = cpu_topk(hx, k, 5, cores)
         leg["cpu_baseline"] = {"ms": t * 1e3, "GBps": gbs(4 * n, k, t * 1e3), "cores": cores, "kind": "reference",
                                "sample": "same input, rtk::topk grid_size=cores, median of 5"}
+    if not args.no_torch_topk:
+        tm = torch_topk_ms(lambda: torch.topk(x, k, sorted=True), max(10, args.steps), flush)
+        leg["torch_topk"] = {"ms": tm, "ours_ms": b.median_ms, "speedup": tm / b.median_ms}
     return leg
 
 
@@ -447,12 +485,19 @@ def leg_c3(args, R, dev, flush, peak, cores, do_cpu):
             e["cpu_baseline"] = {"ms": t * 1e3, "queries_per_s": B / t, "cores": cores, "kind": "reference",
                                  "sample": f"same logits, rtk::batch_topk grid_size=cores, median of {reps}"}
         res["f32"][str(kb)] = e
+        if not args.no_torch_topk:
+            tm = torch_topk_ms(lambda: torch.topk(logits, kb, dim=1, sorted=True), max(5, args.steps // 2), flush)
+            res.setdefault("torch_topk", {})[f"f32_k{kb}"] = {"ms": tm, "ours_ms": b.median_ms,
+                                                              "speedup": tm / b.median_ms}
         bh = R.bench_batch_dense(lb, kb, max(5, args.steps // 2), 3, flush)
         byts = B * (2 * V + 10 * kb)
         res["bf16"][str(kb)] = {"ms": bh.median_ms, "host_ms": bh.median_host_ms,
                                 "queries_per_s": B / (bh.median_ms * 1e-3),
                                 "effective_GBps": byts / (bh.median_ms * 1e-3) / 1e9,
                                 "fraction_of_hbm_peak": byts / (bh.median_ms * 1e-3) / 1e9 / peak}
+        if not args.no_torch_topk:
+            tm = torch_topk_ms(lambda: torch.topk(lb, kb, dim=1, sorted=True), max(5, args.steps // 2), flush)
+            res["torch_topk"][f"bf16_k{kb}"] = {"ms": tm, "ours_ms": bh.median_ms, "speedup": tm / bh.median_ms}
     # Peaked rows (DistKind::Peaked, mass 0.8, modes 1-2, datagen.hpp:93-104)
     from paper_2501_14336_b200 import report as REP
     hp = np.stack([REP.generate(REP.DistributionSpec(kind="peaked", mass=0.8, modes=1 + t % 2, seed=100 + t, n=V))

@@ -89,6 +89,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_LSD")) lsd_mode_ = std::strcmp(g, "16") == 0 ? 1 : std::strcmp(g, "off") == 0 ? 0 : 2;
     if (const char* g = std::getenv("RTK_ROWS_PF")) rows_pf_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_ROWS_TRACE")) rows_trace_ = *g && *g != '0';
+    if (const char* g = std::getenv("RTK_LSD_TRACE")) lsd_trace_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_MSD_CS")) msd_cs_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_TILE_CONTIG")) tile_contig_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_DENSE_BITS")) dense_bits_ = static_cast<uint32_t>(std::atoi(g));
@@ -748,8 +749,40 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
             set_clean(la.tail, R);
             clean_rows_ = R;
         }
+        if (lsd_trace_) {
+            lsd_trace_buf_.ensure(8ull * 8 * 4 * tiles);
+            check(cudaMemsetAsync(lsd_trace_buf_.p, 0, 8ull * 8 * 4 * tiles, s), "memset");
+            la.trace = lsd_trace_buf_.as<unsigned long long>();
+        }
         launch_lsd(tiles, la, s);
         check(cudaGetLastError(), "lsd launch");
+        if (lsd_trace_) {  // per pass: phase durations (p10/p50/p90 us) and the pass span
+            std::vector<unsigned long long> tv(8ull * 4 * tiles);
+            check(cudaStreamSynchronize(s), "sync");
+            check(cudaMemcpy(tv.data(), lsd_trace_buf_.p, 8 * tv.size(), cudaMemcpyDeviceToHost), "trace");
+            for (uint32_t p = 0; p < la.npass; ++p) {
+                std::vector<double> ph[6];
+                unsigned long long t0 = ~0ull, t1 = 0;
+                for (uint64_t t = 0; t < tiles; ++t) {
+                    const unsigned long long* e = tv.data() + (p * tiles + t) * 8;
+                    if (!e[0] || !e[4]) continue;
+                    const int last = e[5] ? 5 : 4;
+                    t0 = std::min(t0, e[0]);
+                    t1 = std::max(t1, e[last]);
+                    for (int i = 1; i <= last; ++i) ph[i - 1].push_back((e[i] - e[i - 1]) * 1e-3);
+                    ph[5].push_back((e[last] - e[0]) * 1e-3);
+                }
+                std::fprintf(stderr, "[rtk lsd trace] pass %u span %.1f us; phase us p10/p50/p90:", p, (t1 - t0) * 1e-3);
+                const char* nm[6] = {"rank", "lookback", "scan", "reorder", "store", "tile"};
+                for (int i = 0; i < 6; ++i) {
+                    auto& v = ph[i];
+                    if (v.empty()) continue;
+                    std::sort(v.begin(), v.end());
+                    std::fprintf(stderr, " %s %.2f/%.2f/%.2f", nm[i], v[v.size() / 10], v[v.size() / 2], v[v.size() * 9 / 10]);
+                }
+                std::fprintf(stderr, "\n");
+            }
+        }
         stats.kernel_launches += 1 + la.npass;
         ++expected_seq_;
         sig_pending_ = true;

@@ -163,6 +163,8 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned full = 0xffffffffu;
     const unsigned lt = (1u << lane) - 1u;
+    unsigned long long t_start = 0;
+    if (a.trace && tid == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_start));
     if (tid == 0) s_t = atomicAdd(a.ctr + pass, 1u);
     for (int i = tid; i < kLsdWarps * 256; i += kLsdThreads) {
         (&s_cnt[0][0])[i] = 0;
@@ -172,6 +174,21 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
     }
     __syncthreads();
     const uint64_t t = s_t;
+    unsigned long long* tr = a.trace ? a.trace + (static_cast<uint64_t>(pass) * a.tile_start[a.R] + t) * 8 : nullptr;
+    int ntr = 1;
+    auto stamp = [&]() {
+        if (tr && tid == 0) {
+            unsigned long long x;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(x));
+            tr[ntr++] = x;
+        }
+    };
+    if (tr && tid == 0) {
+        tr[0] = t_start;
+        uint32_t sm;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+        tr[7] = sm;
+    }
     const int j = lsd_row_of_tile(a, t);
     const uint64_t t0 = a.tile_start[j];
     const uint64_t n = a.len[j];
@@ -237,6 +254,7 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
         __syncwarp();
     }
     __syncthreads();
+    stamp();  // [1] loaded + ranked
     // thread d: warp offsets of digit d, the tile's count of d, look-back, bases
     const uint32_t d = tid;
     uint32_t tc = 0;
@@ -277,6 +295,7 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
         }
         __stcg(st, ep | kLsdPrefix | (excl + tc));  // flag and count in one 64-bit word: no fence
     }
+    if (tr && tid == 0) stamp();  // [2] own digit's look-back done (thread 0 = digit 0)
     uint32_t tot;
     const uint32_t rowbase = lsd_block_scan(hrow, s_w, &tot);
     const uint32_t dstart = lsd_block_scan(tc, s_w, &tot);
@@ -285,6 +304,7 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
 #pragma unroll
     for (int w = 0; w < kLsdWarps; ++w) s_cnt[w][d] += dstart;  // warp offsets -> tile positions
     __syncthreads();
+    stamp();  // [3] all look-backs + scans
     // reorder the tile by digit (stable) in shared memory
 #pragma unroll
     for (int i = 0; i < kLsdItems; ++i) {
@@ -295,6 +315,7 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
         }
     }
     __syncthreads();
+    stamp();  // [4] reordered in smem
     // coalesced runs: tile-sorted position q -> row position gbase[d] + (q - dstart[d])
     if (!LAST) {
         unsigned long long* dst = a.dst + a.buf_off[j];
@@ -303,6 +324,7 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
             const uint32_t dd = digit(K);
             __stcs(dst + (s_gbase[dd] + q), K);
         }
+        stamp();  // [5] stores issued
     } else {
         const uint64_t k = a.k[j], oo = a.out_off[j];
         for (uint32_t q = tid; q < cnt; q += kLsdThreads) {
