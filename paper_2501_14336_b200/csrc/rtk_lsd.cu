@@ -41,6 +41,9 @@ constexpr int kLsdWarps = kLsdThreads / 32;
 constexpr int kLsdItems = RTK_LSD_ITEMS;
 constexpr int kLsdTile = kLsdThreads * kLsdItems;  // 4096 elements
 constexpr int kLsdHistThreads = 512;
+#ifndef RTK_LSD_LBW
+#define RTK_LSD_LBW 1  // look-back window: predecessor words loaded per L2 round trip
+#endif
 #ifndef RTK_LSD_BALLOT
 #define RTK_LSD_BALLOT 0
 #endif
@@ -225,16 +228,19 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
         }
     }
     // stable warp-local ranks in (round, lane) order
-    uint32_t rk[kLsdItems];
+    uint32_t rk2[kLsdItems / 2];  // warp-local ranks (< 2^12), two per register
 #pragma unroll
     for (int i = 0; i < kLsdItems; ++i) {
         const uint32_t e = warp * (kLsdItems * 32) + i * 32 + lane;
         const bool valid = e < cnt;
         const uint32_t d = digit(c[i]);
-#if RTK_LSD_BALLOT
+#if RTK_LSD_BALLOT == 1
         // ballot multisplit (8 ballots)
         unsigned peers = warp_peers8(d);
         if (!full_tile) peers &= __ballot_sync(full, valid);
+#elif RTK_LSD_BALLOT == 2
+        // one match.any per item (invalid lanes get unique keys)
+        const unsigned peers = __match_any_sync(full, valid ? d : 256u + lane);
 #else
         // peers through a shared-memory bitmask per (warp, digit): each lane ORs its bit in, reads
         // the mask back; the lowest peer clears it below (one shared atomic instead of 8 ballots)
@@ -243,7 +249,8 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
         const unsigned peers = valid ? s_match[warp][d] : 0u;
 #endif
         const uint32_t b0 = s_cnt[warp][d];
-        rk[i] = b0 + __popc(peers & lt);
+        const uint32_t r = b0 + __popc(peers & lt);
+        if (i & 1) rk2[i / 2] |= r << 16; else rk2[i / 2] = r;
         __syncwarp();
         if (valid && (peers & lt) == 0) {
             s_cnt[warp][d] = b0 + __popc(peers);
@@ -271,9 +278,9 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
         __stcg(st, ep | kLsdPrefix | tc);
     } else {
         __stcg(st, ep | kLsdAgg | tc);
-        // windowed look-back: the next 8 predecessors' words are loaded at once (one L2 round
+        // windowed look-back: the next W predecessors' words are loaded at once (one L2 round
         // trip per window instead of per tile), then consumed nearest-first until a prefix
-        constexpr int W = 8;
+        constexpr int W = RTK_LSD_LBW;
         const long long first = static_cast<long long>(t0);
         long long q = static_cast<long long>(t) - 1;
         bool done = false;
@@ -311,7 +318,7 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
         const uint32_t e = warp * (kLsdItems * 32) + i * 32 + lane;
         if (e < cnt) {
             const uint32_t dd = digit(c[i]);
-            s_tile[s_cnt[warp][dd] + rk[i]] = c[i];
+            s_tile[s_cnt[warp][dd] + ((rk2[i / 2] >> (16 * (i & 1))) & 0xFFFFu)] = c[i];
         }
     }
     __syncthreads();

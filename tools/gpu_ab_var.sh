@@ -1,6 +1,8 @@
-# same-box A/B of library variants under ab/ (plus the in-tree build) on C2: tools/gpu_ab_var.sh v1 v2 ...
-cd $GRAFT_REPO_ROOT
-for round in 1 2; do
-  python tools/ab_c2.py $GRAFT_REPO_ROOT
-  for v in "$@"; do python tools/ab_c2.py $GRAFT_REPO_ROOT/ab/$v; done
-done
+#!/bin/bash
+# same-box A/B: ab/<variant> builds (tools/build_variant.sh) and the working tree; args: variants -- workloads
+vars=(); while [ "$1" != "--" ]; do vars+=("$1"); shift; done; shift
+for rep in 1 2; do
+for w in "$@"; do
+  for v in "${vars[@]}"; do RTK_PKG_ROOT=ab/$v timeout 120 python tools/ab_env.py $w | sed "s/^/$v /"; done
+  timeout 120 python tools/ab_env.py $w | sed 's/^/NEW  /'
+done; done
