@@ -985,7 +985,8 @@ __global__ void __cluster_dims__(kRcCs, 1, 1) __launch_bounds__(kRowThreads, 1) 
         } else {
             if (m > k) {
                 uint64_t cge;
-                const unsigned long long T2 = cta_radix_select(cand, m, k, k, hist, s_w, s_res, &cge, km_is16<KM>());
+                // the candidates of one long query span a narrow key range: skip constant windows
+                const unsigned long long T2 = cta_radix_select(cand, m, k, k, hist, s_w, s_res, &cge, true);
                 constexpr int PT = kRcCand / kRowThreads;
                 unsigned long long keep[PT];
                 uint32_t km = 0;
