@@ -340,9 +340,19 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     if (n > static_cast<uint64_t>(kRowCand)) {
         const uint64_t nseg = kRowSample / 32;
         const uint64_t stride_fp = ((n - 32) << 16) / (nseg - 1);
-        for (int e = tid; e < kRowSample; e += kRowThreads) {
+        // every sample load issued before the first is used (one memory round trip)
+        constexpr int SQ = kRowSample / kRowThreads;
+        uint32_t raw[SQ];
+#pragma unroll
+        for (int q = 0; q < SQ; ++q) {
+            const int e = q * kRowThreads + tid;
+            raw[q] = ld(((static_cast<uint64_t>(e / 32) * stride_fp) >> 16) + (e & 31));
+        }
+#pragma unroll
+        for (int q = 0; q < SQ; ++q) {
+            const int e = q * kRowThreads + tid;
             const uint64_t idx = ((static_cast<uint64_t>(e / 32) * stride_fp) >> 16) + (e & 31);
-            cand[e] = composite(make_key(a.in, ld(idx)), idx);
+            cand[e] = composite(make_key(a.in, raw[q]), idx);
         }
         __syncthreads();
         const double rr = static_cast<double>(k) * kRowSample / static_cast<double>(n);
