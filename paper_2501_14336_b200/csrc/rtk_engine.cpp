@@ -90,6 +90,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_ROWS_PF")) rows_pf_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_ROWS_TRACE")) rows_trace_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_LSD_TRACE")) lsd_trace_ = *g && *g != '0';
+    if (const char* g = std::getenv("RTK_LSD_RR")) lsd_rr_ = *g != '0';
     if (const char* g = std::getenv("RTK_MSD_CS")) msd_cs_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_TILE_CONTIG")) tile_contig_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_DENSE_BITS")) dense_bits_ = static_cast<uint32_t>(std::atoi(g));
@@ -592,6 +593,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
     // (RTK_LSD=off: the MSD + bucket-sort path; RTK_LSD=16: 16-bit keys only)
     const bool lsd = dense && (lsd_mode_ == 2 || (lsd_mode_ == 1 && dtype == kF16));
     std::vector<uint64_t> l_tile{0}, l_len, l_in, l_buf, l_k, l_out;
+    std::vector<uint32_t> l_order;
     uint64_t l_total = 0;
     if (lsd) {
         for (uint32_t r : grow) {
@@ -604,11 +606,23 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
             l_k.push_back(q.k);
             l_out.push_back(q.out_off);
         }
+        // claim order of the LSD tiles: round-robin over the rows (tile 0 of every row, then tile
+        // 1, ...), so a tile's predecessor in its row was claimed ~R claims earlier and has
+        // usually published its inclusive prefix by the time the tile looks back
+        if (lsd_rr_) {
+            const size_t NR = l_len.size();
+            uint64_t maxt = 0;
+            for (size_t j = 0; j < NR; ++j) maxt = std::max(maxt, l_tile[j + 1] - l_tile[j]);
+            l_order.reserve(l_tile.back());
+            for (uint64_t t = 0; t < maxt; ++t)
+                for (size_t j = 0; j < NR; ++j)
+                    if (l_tile[j] + t < l_tile[j + 1]) l_order.push_back(static_cast<uint32_t>(l_tile[j] + t));
+        }
     }
     Plan P;
     const size_t o_dslots = P.add(dslots);
     const size_t o_ltile = P.add(l_tile), o_llen = P.add(l_len), o_lin = P.add(l_in), o_lbuf = P.add(l_buf),
-                 o_lk = P.add(l_k), o_lout = P.add(l_out);
+                 o_lk = P.add(l_k), o_lout = P.add(l_out), o_lord = P.add(l_order);
     const size_t o_rid = P.add(rid), o_off = P.add(off), o_len = P.add(len), o_lead = P.add(lead),
                  o_tile = P.add(tile_start), o_coff = P.add(cand_off), o_cap = P.add(cap),
                  o_k = P.add(row_k), o_out = P.add(row_out), o_in = P.add(row_in),
@@ -727,6 +741,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
         LsdArgs la{};
         la.R = NR;
         la.tile_start = at<uint64_t>(D, o_ltile);
+        la.order = l_order.empty() ? nullptr : at<uint32_t>(D, o_lord);
         la.len = at<uint64_t>(D, o_llen);
         la.in_off = at<uint64_t>(D, o_lin);
         la.buf_off = at<uint64_t>(D, o_lbuf);

@@ -267,6 +267,7 @@ private:
     int tile_contig_ = -1;          // RTK_TILE_CONTIG: force k_compact's tile order (-1: by row count)
     int msd_cs_ = 0;                // RTK_MSD_CS: force the level-0 MSD cluster size
     int rows_pf_ = 0;               // L2 prefetch distance of the per-row ring (RTK_ROWS_PF)
+    bool lsd_rr_ = true;            // RTK_LSD_RR=0: LSD tiles claimed row by row (no round-robin order)
     bool lsd_trace_ = false;        // RTK_LSD_TRACE: per-tile phase timestamps of k_lsd_pass
     DevBuf lsd_trace_buf_;
     bool rows_trace_ = false;       // per-CTA phase timestamps of k_rows_fused (RTK_ROWS_TRACE)

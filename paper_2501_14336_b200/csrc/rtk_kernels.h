@@ -324,6 +324,7 @@ struct LsdArgs {  // dense rows: segmented one-sweep LSD radix sort (rtk_lsd.cu)
     uint32_t npass;               // 4 (32-bit keys) or 2 (16-bit keys: low half constant)
     uint32_t shift0;              // 0 or 16
     unsigned long long* trace;    // RTK_LSD_TRACE: [pass][tile][8] phase timestamps, nullable
+    const uint32_t* order;        // claim index -> row-major tile id (round-robin over rows), nullable
 };
 uint32_t lsd_tile();
 void launch_lsd(uint64_t tiles, const LsdArgs& a, cudaStream_t s);

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
 #endif
     }
     __syncthreads();
-    const uint64_t t = s_t;
+    const uint64_t t = a.order ? a.order[s_t] : s_t;  // row-major tile id
     unsigned long long* tr = a.trace ? a.trace + (static_cast<uint64_t>(pass) * a.tile_start[a.R] + t) * 8 : nullptr;
     int ntr = 1;
     auto stamp = [&]() {
