@@ -30,7 +30,10 @@
 
 namespace rtk_b200 {
 
-constexpr int kLsdThreads = 256;
+#ifndef RTK_LSD_THREADS
+#define RTK_LSD_THREADS 256
+#endif
+constexpr int kLsdThreads = RTK_LSD_THREADS;  // >= 256: thread d < 256 owns digit d
 constexpr int kLsdWarps = kLsdThreads / 32;
 #ifndef RTK_LSD_ITEMS
 #define RTK_LSD_ITEMS 16
@@ -198,7 +201,7 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
     const uint64_t e0 = (t - t0) * kLsdTile;
     const uint32_t cnt = static_cast<uint32_t>(n - e0 < kLsdTile ? n - e0 : kLsdTile);
     const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(a.ctr + 4) * 4u + pass + 1u;
-    const uint32_t hrow = __ldcg(a.hist + j * 1024 + pass * 256 + tid);  // consumed after the look-back
+    const uint32_t hrow = tid < 256 ? __ldcg(a.hist + j * 1024 + pass * 256 + tid) : 0u;  // used after the look-back
     const bool full_tile = cnt == kLsdTile;
     (void)full_tile;
     (void)full;
@@ -264,7 +267,8 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
     stamp();  // [1] loaded + ranked
     // thread d: warp offsets of digit d, the tile's count of d, look-back, bases
     const uint32_t d = tid;
-    uint32_t tc = 0;
+    uint32_t tc = 0, excl = 0;
+    if (kLsdThreads == 256 || d < 256) {
 #pragma unroll
     for (int w = 0; w < kLsdWarps; ++w) {
         const uint32_t v = s_cnt[w][d];
@@ -273,7 +277,6 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
     }
     unsigned long long* st = a.status + t * 256 + d;
     const unsigned long long ep = static_cast<unsigned long long>(epoch) << 32;
-    uint32_t excl = 0;
     if (t == t0) {
         __stcg(st, ep | kLsdPrefix | tc);
     } else {
@@ -302,14 +305,17 @@ __global__ void __launch_bounds__(kLsdThreads, RTK_LSD_MINB) k_lsd_pass(LsdArgs 
         }
         __stcg(st, ep | kLsdPrefix | (excl + tc));  // flag and count in one 64-bit word: no fence
     }
+    }
     if (tr && tid == 0) stamp();  // [2] own digit's look-back done (thread 0 = digit 0)
     uint32_t tot;
     const uint32_t rowbase = lsd_block_scan(hrow, s_w, &tot);
     const uint32_t dstart = lsd_block_scan(tc, s_w, &tot);
     // tile-sorted position q of digit d goes to row position q + (rowbase + excl - dstart)
-    s_gbase[d] = rowbase + excl - dstart;
+    if (kLsdThreads == 256 || d < 256) {
+        s_gbase[d] = rowbase + excl - dstart;
 #pragma unroll
-    for (int w = 0; w < kLsdWarps; ++w) s_cnt[w][d] += dstart;  // warp offsets -> tile positions
+        for (int w = 0; w < kLsdWarps; ++w) s_cnt[w][d] += dstart;  // warp offsets -> tile positions
+    }
     __syncthreads();
     stamp();  // [3] all look-backs + scans
     // reorder the tile by digit (stable) in shared memory
