@@ -557,7 +557,11 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
             g.nseg.push_back(ns / 32);
             g.k.push_back(rp);
             g.target.push_back(rp + rp / 10 + 8);
-            if (grp) g.cs = std::max<int>(g.cs, static_cast<int>(std::min<uint64_t>(16, ns / 4096)));
+            if (grp) {  // a power of two: the sample kernel splits its 2048 bins into cs equal slices
+                int cs = 1;
+                while (cs * 2 <= 16 && static_cast<uint64_t>(cs * 2) * 4096 <= ns) cs *= 2;
+                g.cs = std::max<int>(g.cs, cs);
+            }
             g.per_cta = std::max<uint32_t>(g.per_cta, static_cast<uint32_t>(ns / g.cs));
         } else {
             cap[r] = q.n;

@@ -529,3 +529,16 @@ def test_bench_helpers_time_the_same_call(cuda):
     got = R.scaled_topk(x, 4096, policy=pol)
     want = O.ref_scaled_topk(x.cpu().numpy(), 4096, 0, mode=2, tau=0.5, seed=31)
     assert np.array_equal(got.indices.cpu().numpy().astype(np.uint64), np.asarray(want[1], dtype=np.uint64))
+
+
+@pytest.mark.parametrize("n", [6911791, 3 * (1 << 20) + 5, (1 << 22) + (1 << 21) - 3])
+def test_sample_cluster_sizes(cuda, n):
+    # huge rows whose stratified sample (n/128 elements) is not a power of two: the sample
+    # kernel's cluster must still be a power of two (its 2048 bins split into equal slices);
+    # found by tests/test_gpu_fuzz.py (n = 6911791: 13 CTAs before the fix, misaligned DSMEM)
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(n).astype(np.float32)
+    for k, order in [(398, 1), (1000, 0), (70000, 0)]:
+        assert_same(gpu_topk(x, k, order, cuda), O.ref_topk(x, k, order, grid=8), f"n={n} k={k}")
+        u = x.view(np.uint32)
+        assert_same(gpu_topk(u, k, order, cuda), O.ref_topk(u, k, order, grid=8), f"u32 n={n} k={k}")
