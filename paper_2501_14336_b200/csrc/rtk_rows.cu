@@ -817,7 +817,6 @@ __device__ __forceinline__ void rank_sort_desc(const unsigned long long* buf, ui
 constexpr int kRcCs = 16;
 constexpr int kRcCand = 8192;
 constexpr int kRcSample = 4096;
-constexpr int kRcU = 8;  // 16-byte loads in flight per thread in the streaming pass
 
 template <int KM>
 __global__ void __cluster_dims__(kRcCs, 1, 1) __launch_bounds__(kRowThreads, 1) k_row_cluster(RowsFusedArgs a) {
@@ -924,11 +923,13 @@ __global__ void __cluster_dims__(kRcCs, 1, 1) __launch_bounds__(kRowThreads, 1) 
                 ++o;
             }
     };
-    constexpr int NE = kRcU * VE;  // elements per thread per step (32)
-    for (uint64_t vb = v0; vb < v1; vb += static_cast<uint64_t>(kRcU) * kRowThreads) {
-        uint4 w[kRcU];
+    // 32 elements per thread per step (one 32-bit hit mask): 8 vectors of 4 f32/u32, 4 of 8 halves
+    constexpr int RU = 32 / VE;
+    constexpr int NE = RU * VE;
+    for (uint64_t vb = v0; vb < v1; vb += static_cast<uint64_t>(RU) * kRowThreads) {
+        uint4 w[RU];
 #pragma unroll
-        for (int u = 0; u < kRcU; ++u) {
+        for (int u = 0; u < RU; ++u) {
             const uint64_t v = vb + static_cast<uint64_t>(u) * kRowThreads + tid;
             w[u] = v < v1 ? __ldg(vrow + v) : make_uint4(0u, 0u, 0u, 0u);
         }
@@ -936,13 +937,13 @@ __global__ void __cluster_dims__(kRcCs, 1, 1) __launch_bounds__(kRowThreads, 1) 
         uint32_t mask = 0;
         // ties at T's key (index eT) are hits iff their index <= eT: decided once for the whole
         // step unless the step's index range straddles eT (at most one step per row)
-        const uint64_t lo_e = a0 + vb * VE, hi_e = a0 + (vb + static_cast<uint64_t>(kRcU) * kRowThreads) * VE - 1;
+        const uint64_t lo_e = a0 + vb * VE, hi_e = a0 + (vb + static_cast<uint64_t>(RU) * kRowThreads) * VE - 1;
         if (hi_e <= eT || lo_e > eT) {
             const bool tie_in = hi_e <= eT;
             if (!tie_in && thi == 0xffffffffu) continue;  // nothing above T's key
             const uint32_t ge = tie_in ? thi : thi + 1;
 #pragma unroll
-            for (int u = 0; u < kRcU; ++u) {
+            for (int u = 0; u < RU; ++u) {
                 const bool ok = vb + static_cast<uint64_t>(u) * kRowThreads + tid < v1;
                 const uint32_t wd[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
 #pragma unroll
@@ -955,7 +956,7 @@ __global__ void __cluster_dims__(kRcCs, 1, 1) __launch_bounds__(kRowThreads, 1) 
             }
         } else {
 #pragma unroll
-            for (int u = 0; u < kRcU; ++u) {
+            for (int u = 0; u < RU; ++u) {
                 const uint64_t v = vb + static_cast<uint64_t>(u) * kRowThreads + tid;
                 const uint32_t wd[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
 #pragma unroll

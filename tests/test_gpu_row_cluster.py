@@ -128,3 +128,24 @@ def test_row_cluster_replay(cuda):
     t.copy_(torch.from_numpy(y))
     r = rtk.topk(t, 256)
     assert_same((r.values, r.indices, r.pivot), O.ref_topk(y, 256, 0, grid=4), "rewritten input")
+
+
+@pytest.mark.parametrize("kind", ["bf16", "f16"])
+def test_row_cluster_16bit_every_lane_slot(cuda, kind):
+    # each 16-bit step of the stream covers 4 vectors of 8 halves per thread (one 32-bit hit
+    # mask); the maxima sit in every slot of a step (found by tools/fuzz_explore.py: with 8
+    # vectors per step the upper half of the 64 elements never reached the mask)
+    import torch
+    import paper_2501_14336_b200 as rtk
+    n = (1 << 20) + 6
+    rng = np.random.default_rng(5)
+    base = torch.from_numpy((rng.random(n, dtype=np.float32) * 0.5).astype(np.float32))
+    for pos in (24000, 24000 + 8 * 512 * 5 + 7, n - 3, 3):
+        x = base.clone()
+        x[pos] = 1000.0
+        t16 = x.to(torch.bfloat16 if kind == "bf16" else torch.float16)
+        for k in (1, 64):
+            r = rtk.topk(t16.to(cuda), k)
+            assert int(r.indices[0].item()) == pos, (kind, pos, k)
+        h = t16.view(torch.int16).numpy().view(np.uint16).copy()
+        _check16(h, t16, _widen16(h, kind), 200, 0, cuda, f"{kind} pos={pos}")
