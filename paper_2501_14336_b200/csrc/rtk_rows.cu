@@ -306,7 +306,8 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     // shared-memory ring with mbarrier completion; the first stages are in flight while the
     // threshold is being selected.
     const uintptr_t a0 = reinterpret_cast<uintptr_t>(rowb);
-    const uint32_t head = static_cast<uint32_t>(((16 - (a0 & 15)) & 15) / EB);  // to 16-B alignment
+    // elements before 16-byte alignment (a row shorter than that is all head)
+    const uint32_t head = static_cast<uint32_t>(min(static_cast<uint64_t>(((16 - (a0 & 15)) & 15) / EB), n));
     const uint64_t body = n > head ? n - head : 0;
     constexpr int U = km_is16<KM>() ? 2 * UU : UU;  // same stage BYTES for 16-bit rows
     constexpr uint32_t kChunk = static_cast<uint32_t>(U) * kRowChunk;  // elements per ring stage

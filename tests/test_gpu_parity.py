@@ -542,3 +542,34 @@ def test_sample_cluster_sizes(cuda, n):
         assert_same(gpu_topk(x, k, order, cuda), O.ref_topk(x, k, order, grid=8), f"n={n} k={k}")
         u = x.view(np.uint32)
         assert_same(gpu_topk(u, k, order, cuda), O.ref_topk(u, k, order, grid=8), f"u32 n={n} k={k}")
+
+
+def test_batch_tiny_misaligned_rows(cuda):
+    # rows shorter than their distance to 16-byte alignment (n = 1..7 at every misalignment,
+    # f32 / u32 / f16 / bf16): k_rows_fused's scalar head must stop at the row's end (found by
+    # tools/fuzz_explore.py: a 1-element row read its neighbours)
+    import torch
+    rtk = _rtk()
+    rng = np.random.default_rng(77)
+    lens = [n for n in range(1, 8) for _ in range(8)] + [3000]
+    offs, pos = [], 0
+    for t, n in enumerate(lens):
+        pos += t % 5
+        offs.append(pos)
+        pos += n
+    data = rng.standard_normal(pos).astype(np.float32)
+    ks = [1 + (t % n) for t, n in enumerate(lens)]
+    for order in (0, 1):
+        exp = _batch_expect(data, offs, lens, ks, order)
+        got = rtk.batch_topk(rtk.BatchInput(torch.from_numpy(data).to(cuda), offs, lens, ks), rtk.SelectionOrder(order))
+        for t in range(len(lens)):
+            assert_same((got[t].values, got[t].indices, got[t].pivot), exp[t], f"f32 row {t} n={lens[t]}")
+    for kind in ("bf16", "f16"):
+        t16 = torch.from_numpy(data).to(torch.bfloat16 if kind == "bf16" else torch.float16)
+        h = t16.view(torch.int16).numpy().view(np.uint16).copy()
+        x32 = _widen16(h, kind)
+        exp = _batch_expect(x32, offs, lens, ks, 0)
+        got = rtk.batch_topk(rtk.BatchInput(t16.to(cuda), offs, lens, ks))
+        for t in range(len(lens)):
+            gi = got[t].indices.cpu().numpy().astype(np.uint64)
+            assert np.array_equal(gi, exp[t][1].astype(np.uint64)), f"{kind} row {t} n={lens[t]}"
