@@ -26,12 +26,15 @@ for case in range(s0, s0 + cnt):
     order = int(rng.integers(0, 2))
     what = ""
     try:
-        mode = rng.integers(0, 4)
+        mode = rng.integers(0, 6)
+        force = rng.integers(0, 8)  # 1/8 of the cases on a forced rare path
+        rtk.set_option("force_exact", 1 if force == 0 else 0)
+        rtk.set_option("force_deep", 1 if force == 1 else 0)
         if mode == 0:  # single query
             n = int(rng.choice([rng.integers(1, 1 << 18), rng.integers((1 << 18) + 1, (1 << 21) + 1),
                                 rng.integers(1 << 21, 1 << 24)]))
             x = _row(rng, n, dtype)
-            k = int(rng.integers(1, 513)) if rng.integers(0, 2) else _k(rng, n)
+            k = min(n, int(rng.integers(1, 513))) if rng.integers(0, 2) else _k(rng, n)
             what = f"single n={n} k={k} order={order} {dtype.__name__}"
             assert_same(gpu_topk(x, k, order, dev), O.ref_topk(x, k, order, grid=16), what)
         elif mode == 1:  # batch
@@ -76,6 +79,30 @@ for case in range(s0, s0 + cnt):
                                 policy=rtk.ScalePolicy(rtk.ScaleMode(m), 0.5, seed), info=info)
             assert info.scaled == winfo["scaled"], what + " scaled flag"
             assert_same((r.values, r.indices, r.pivot), (wv, wi, wp), what)
+        elif mode == 4:  # ragged 16-bit batch: indices against the widened f32 rows, values = inputs
+            from tests.test_gpu_parity import _widen16
+            kind = "bf16" if rng.integers(0, 2) else "f16"
+            B = int(rng.integers(1, 20))
+            lens = [int(rng.choice([rng.integers(1, 5000), rng.integers(5000, 300000)])) for _ in range(B)]
+            ks = [_k(rng, n) for n in lens]
+            offs, pos = [], 0
+            for t in range(B):
+                pos += int(rng.integers(0, 9))
+                offs.append(pos)
+                pos += lens[t]
+            xf = torch.from_numpy(rng.standard_normal(pos).astype(np.float32) * float(rng.choice([1.0, 1e-2, 50.0])))
+            t16 = xf.to(torch.bfloat16 if kind == "bf16" else torch.float16)
+            h = t16.view(torch.int16).numpy().view(np.uint16).copy()
+            x32 = _widen16(h, kind)
+            what = f"{kind} batch B={B} order={order}"
+            exp = O.ref_batch_topk(x32, offs, lens, ks, order, grid=16)
+            got = rtk.batch_topk(rtk.BatchInput(t16.to(dev), offs, lens, ks), rtk.SelectionOrder(order))
+            for t in range(B):
+                gi = got[t].indices.cpu().numpy().astype(np.uint64)
+                wi = exp[t][1].astype(np.uint64)
+                assert np.array_equal(gi, wi), what + f" row {t} n={lens[t]} k={ks[t]}: indices"
+                gv = got[t].values.view(torch.int16).cpu().numpy().view(np.uint16)
+                assert np.array_equal(gv, h[offs[t] + wi.astype(np.int64)]), what + f" row {t}: values"
         else:  # 16-bit rows (indices against the exactly widened f32 input)
             from tests.test_gpu_parity import _check16, _widen16
             kind = "bf16" if rng.integers(0, 2) else "f16"
@@ -94,4 +121,6 @@ for case in range(s0, s0 + cnt):
         print(f"ERROR case {case} ({what}): {type(e).__name__}: {str(e)[:300]}", flush=True)
         if "cuda" in type(e).__name__.lower():
             break
+rtk.set_option("force_exact", 0)
+rtk.set_option("force_deep", 0)
 print(f"fuzz {s0}..{s0 + cnt}: {fails} failures", flush=True)
