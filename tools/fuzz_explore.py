@@ -26,7 +26,7 @@ for case in range(s0, s0 + cnt):
     order = int(rng.integers(0, 2))
     what = ""
     try:
-        mode = rng.integers(0, 6)
+        mode = rng.integers(0, 8)
         force = rng.integers(0, 8)  # 1/8 of the cases on a forced rare path
         rtk.set_option("force_exact", 1 if force == 0 else 0)
         rtk.set_option("force_deep", 1 if force == 1 else 0)
@@ -103,6 +103,24 @@ for case in range(s0, s0 + cnt):
                 assert np.array_equal(gi, wi), what + f" row {t} n={lens[t]} k={ks[t]}: indices"
                 gv = got[t].values.view(torch.int16).cpu().numpy().view(np.uint16)
                 assert np.array_equal(gv, h[offs[t] + wi.astype(np.int64)]), what + f" row {t}: values"
+        elif mode == 6:  # dense [B, V] rows (batch_topk_dense), f32
+            B = int(rng.integers(1, 64))
+            V = int(rng.choice([rng.integers(1, 4000), rng.integers(4000, 140000)]))
+            data = np.concatenate([_row(rng, V, np.float32) for _ in range(B)])
+            k = _k(rng, V)
+            what = f"dense B={B} V={V} k={k} order={order}"
+            exp = O.ref_batch_topk(data, [i * V for i in range(B)], [V] * B, [k] * B, order, grid=16)
+            r = rtk.batch_topk_dense(torch.from_numpy(data).to(dev).view(B, V), k, rtk.SelectionOrder(order))
+            gv, gi, gp = r.values.cpu().numpy(), r.indices.cpu().numpy(), r.pivot.cpu().numpy()
+            for t in range(B):
+                assert_same((gv[t], gi[t], gp[t]), exp[t], what + f" row {t}")
+        elif mode == 7:  # host entry points (numpy in, copies inside the call)
+            n = int(rng.integers(1, 1 << 22))
+            x = _row(rng, n, np.float32)
+            k = _k(rng, n)
+            what = f"host n={n} k={k} order={order}"
+            r = rtk.topk(x, k, rtk.SelectionOrder(order))
+            assert_same((r.values, r.indices, r.pivot), O.ref_topk(x, k, order, grid=16), what)
         else:  # 16-bit rows (indices against the exactly widened f32 input)
             from tests.test_gpu_parity import _check16, _widen16
             kind = "bf16" if rng.integers(0, 2) else "f16"
