@@ -88,6 +88,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* g = std::getenv("RTK_DYN")) dyn_per_cta_ = std::max(0, std::atoi(g));
     if (const char* g = std::getenv("RTK_LSD")) lsd_mode_ = std::strcmp(g, "16") == 0 ? 1 : std::strcmp(g, "off") == 0 ? 0 : 2;
     if (const char* g = std::getenv("RTK_ROWS_PF")) rows_pf_ = std::atoi(g);
+    if (const char* g = std::getenv("RTK_ROWS_PF0")) rows_pf0_ = std::atoi(g);
     if (const char* g = std::getenv("RTK_ROWS_TRACE")) rows_trace_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_LSD_TRACE")) lsd_trace_ = *g && *g != '0';
     if (const char* g = std::getenv("RTK_LSD_RR")) lsd_rr_ = *g != '0';
@@ -691,7 +692,7 @@ void Engine::enqueue(const uint32_t* d_base, int dtype, int smallest, bool scale
         RowsFusedArgs fa{at<uint32_t>(D, o_f[v][0]), at<uint64_t>(D, o_f[v][1]), at<uint64_t>(D, o_f[v][2]),
                          at<uint64_t>(D, o_f[v][3]), src, c.d_row_out, d_vals, d_idx, d_pivots,
                          row_fail_.as<uint32_t>(), ctl_.as<uint32_t>(), nullptr, CallTail{},
-                         static_cast<uint32_t>(rows_pf_)};
+                         static_cast<uint32_t>(rows_pf_) | (static_cast<uint32_t>(rows_pf0_) << 16)};
         if (profile_) {
             dbg_.ensure(4096);
             fa.dbg = dbg_.as<unsigned long long>();
@@ -1081,9 +1082,9 @@ void Engine::drain(Call& c, uint32_t (&ctl)[8]) {
         check(cudaHostAlloc(reinterpret_cast<void**>(&hcount_), 8 * hcount_cap_, cudaHostAllocDefault), "cudaHostAlloc");
     }
     if (sig_pending_ && !count_stats_) {
-        wait_signal(c.s);  // the last sort CTA published ctl[0..14]: no copy, no stream sync
+        wait_signal(c.s);  // the last CTA published ctl[0..7] and ctl[10..13]: no copy, no stream sync
         for (int i = 0; i < 8; ++i) ctl[i] = reinterpret_cast<volatile uint32_t*>(hmap_)[i];
-        for (int i = 0; i < 4; ++i) drain_trig_[i] = reinterpret_cast<volatile uint32_t*>(hmap_)[10 + i];
+        for (int i = 0; i < 4; ++i) drain_trig_[i] = reinterpret_cast<volatile uint32_t*>(hmap_)[8 + i];  // ctl[10..13]
     } else {
         check(cudaMemcpyAsync(hctl_, ctl_.p, 64, cudaMemcpyDeviceToHost, c.s), "d2h");
         if (count_stats_) check(cudaMemcpyAsync(hcount_, count_.p, 8 * c.R, cudaMemcpyDeviceToHost, c.s), "d2h");

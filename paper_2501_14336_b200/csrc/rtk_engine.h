@@ -266,6 +266,7 @@ private:
     uint32_t dense_bits_ = 0;       // RTK_DENSE_BITS: level-0 digit of dense rows (0: fine_bits)         // RTK_NO_DENSE=1: dense rows are compacted too         // RTK_NO_FUSED=1: short rows take the general path too
     int tile_contig_ = -1;          // RTK_TILE_CONTIG: force k_compact's tile order (-1: by row count)
     int msd_cs_ = 0;                // RTK_MSD_CS: force the level-0 MSD cluster size
+    int rows_pf0_ = 0;              // one-shot L2 prefetch at the row's start, chunks (RTK_ROWS_PF0)
     int rows_pf_ = 0;               // L2 prefetch distance of the per-row ring (RTK_ROWS_PF)
     bool lsd_rr_ = true;            // RTK_LSD_RR=0: LSD tiles claimed row by row (no round-robin order)
     bool lsd_trace_ = false;        // RTK_LSD_TRACE: per-tile phase timestamps of k_lsd_pass

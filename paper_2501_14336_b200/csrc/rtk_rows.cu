@@ -40,6 +40,9 @@ constexpr int kRowChunk = 2048;   // elements per TMA bulk chunk (8 KB)
 constexpr int kRowU = RTK_ROWS_U;    // 2048-element chunks per ring stage (one TMA copy each)
 constexpr int kRowStU = RTK_ROWS_SS; // stages of the small-k variant
 constexpr int kRowStLU = RTK_ROWS_SL;  // stages of the large-k variant
+#ifndef RTK_ROWS_SFIRST
+#define RTK_ROWS_SFIRST 1
+#endif
 
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
@@ -302,6 +305,22 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     }
     stamp();
 
+    // ---- sample loads first: issued ahead of the ring's bulk copies so they do not queue behind
+    // them in the memory system (the threshold is the critical path of the CTA's start)
+    constexpr int SQ = kRowSample / kRowThreads;
+    const bool sampled = n > static_cast<uint64_t>(kRowCand);
+    const uint64_t stride_fp = sampled ? ((n - 32) << 16) / (kRowSample / 32 - 1) : 0;
+    uint32_t raw[SQ];
+#if RTK_ROWS_SFIRST
+    if (sampled) {
+#pragma unroll
+        for (int q = 0; q < SQ; ++q) {
+            const int e = q * kRowThreads + tid;
+            raw[q] = ld(((static_cast<uint64_t>(e / 32) * stride_fp) >> 16) + (e & 31));
+        }
+    }
+#endif
+
     // ---- streaming ring: TMA 1-D bulk copies (cp.async.bulk) of 8 KB chunks into a 4-stage
     // shared-memory ring with mbarrier completion; the first stages are in flight while the
     // threshold is being selected.
@@ -332,23 +351,23 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     if (tid == 0) {
         for (uint64_t c = 0; c < nchunks && c < static_cast<uint64_t>(kRowStages); ++c)
             bulk_g2s(ring + c * kChunkBytes, bsrc + c * kChunkBytes, kChunkBytes, &bar[c]);
-        for (uint32_t p = 0; p < a.pf; ++p) prefetch(kRowStages + p);
+        // a.pf: L2 prefetch distance kept while streaming; a.pf >> 16: chunks beyond the ring
+        // pulled into L2 once at the start (HBM is otherwise idle while the threshold is selected)
+        for (uint32_t p = 0; p < (a.pf & 0xFFFFu) + (a.pf >> 16); ++p) prefetch(kRowStages + p);
     }
 
     // ---- 1. threshold -------------------------------------------------------------------
     stamp();
     unsigned long long T = 0;
-    if (n > static_cast<uint64_t>(kRowCand)) {
-        const uint64_t nseg = kRowSample / 32;
-        const uint64_t stride_fp = ((n - 32) << 16) / (nseg - 1);
+    if (sampled) {
+#if !RTK_ROWS_SFIRST
         // every sample load issued before the first is used (one memory round trip)
-        constexpr int SQ = kRowSample / kRowThreads;
-        uint32_t raw[SQ];
 #pragma unroll
         for (int q = 0; q < SQ; ++q) {
             const int e = q * kRowThreads + tid;
             raw[q] = ld(((static_cast<uint64_t>(e / 32) * stride_fp) >> 16) + (e & 31));
         }
+#endif
 #pragma unroll
         for (int q = 0; q < SQ; ++q) {
             const int e = q * kRowThreads + tid;
@@ -443,7 +462,7 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
                         if (c + kRowStages < nchunks)
                             bulk_g2s(ring + st * kChunkBytes, bsrc + (c + kRowStages) * kChunkBytes, kChunkBytes,
                                      &bar[st]);
-                        if (a.pf) prefetch(c + kRowStages + a.pf);
+                        if (a.pf & 0xFFFFu) prefetch(c + kRowStages + (a.pf & 0xFFFFu) + (a.pf >> 16));
                     }
                 }
             }

@@ -14,7 +14,11 @@ from paper_2501_14336_b200 import rtk as R
 which = sys.argv[1]
 k = int(sys.argv[2]) if len(sys.argv) > 2 else None
 dev = torch.device("cuda", 0)
-if which in ("c1", "c2"):
+if which == "tiny":
+    x = torch.from_numpy(np.random.default_rng(1).random(1000, dtype=np.float32)).to(dev)
+    for _ in range(3):
+        rtk.topk(x, k or 1)
+elif which in ("c1", "c2"):
     n = 1 << (20 if which == "c1" else 28)
     x = torch.from_numpy(np.random.default_rng(1).random(n, dtype=np.float32)).to(dev)
     for _ in range(3):
