@@ -1018,11 +1018,11 @@ void Engine::launch_sort(uint32_t max_groups, const SortArgs& a, cudaStream_t s)
 void Engine::wait_signal(cudaStream_t s) {
     const volatile uint32_t* f = hmap_;
     for (uint64_t spin = 0;; ++spin) {
-        if (f[15] == expected_seq_) return;
+        if (((f[15] ^ expected_seq_) & 0x7FFFFFFFu) == 0) return;
         if ((spin & 1023) == 1023) {
             const cudaError_t e = cudaStreamQuery(s);
             if (e == cudaSuccess) {
-                if (f[15] == expected_seq_) return;
+                if (((f[15] ^ expected_seq_) & 0x7FFFFFFFu) == 0) return;
                 throw Error{RTK_INTERNAL, "completion signal missing"};
             }
             if (e != cudaErrorNotReady) check(e, "kernel");
@@ -1083,8 +1083,12 @@ void Engine::drain(Call& c, uint32_t (&ctl)[8]) {
     }
     if (sig_pending_ && !count_stats_) {
         wait_signal(c.s);  // the last CTA published ctl[0..7] and ctl[10..13]: no copy, no stream sync
-        for (int i = 0; i < 8; ++i) ctl[i] = reinterpret_cast<volatile uint32_t*>(hmap_)[i];
-        for (int i = 0; i < 4; ++i) drain_trig_[i] = reinterpret_cast<volatile uint32_t*>(hmap_)[8 + i];  // ctl[10..13]
+        // bit 31 of the sequence word: the words were published; clear: the flags and the
+        // trigger counts were zero (the other words matter only under a flag)
+        const volatile uint32_t* hw = hmap_;
+        const bool words = (hw[15] >> 31) != 0;
+        for (int i = 0; i < 8; ++i) ctl[i] = words ? hw[i] : 0u;
+        for (int i = 0; i < 4; ++i) drain_trig_[i] = words ? hw[8 + i] : 0u;  // ctl[10..13]
     } else {
         check(cudaMemcpyAsync(hctl_, ctl_.p, 64, cudaMemcpyDeviceToHost, c.s), "d2h");
         if (count_stats_) check(cudaMemcpyAsync(hcount_, count_.p, 8 * c.R, cudaMemcpyDeviceToHost, c.s), "d2h");

@@ -13,9 +13,9 @@ from paper_2501_14336_b200 import rtk as R
 which, k = sys.argv[1], int(sys.argv[2])
 dev = torch.device("cuda", 0)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-if which == "tiny":  # the fixed per-call cost: one 1000-element row (one CTA)
+if which in ("tiny", "tinynf"):  # the fixed per-call cost: one 1000-element row (one CTA); nf: no L2 flush
     x = torch.from_numpy(np.random.default_rng(1).random(1000, dtype=np.float32)).to(dev)
-    b = R.bench_topk(x, k, 20, 5, flush=flush)
+    b = R.bench_topk(x, k, 20, 5, flush=flush if which == "tiny" else None)
 elif which in ("c1", "c2"):
     n = 1 << (20 if which == "c1" else 28)
     x = torch.from_numpy(np.random.default_rng(1).random(n, dtype=np.float32)).to(dev)
