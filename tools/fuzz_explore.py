@@ -141,4 +141,4 @@ for case in range(s0, s0 + cnt):
             break
 rtk.set_option("force_exact", 0)
 rtk.set_option("force_deep", 0)
-print(f"fuzz {s0}..{s0 + cnt}: {fails} failures", flush=True)
+print(f"fuzz {s0}..{case + 1}: {case + 1 - s0} cases, {fails} failures", flush=True)
