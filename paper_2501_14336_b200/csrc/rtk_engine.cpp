@@ -218,6 +218,10 @@ void Engine::report_rows_trace(size_t nrows, cudaStream_t s) {
         if (!cnt) continue;
         std::fprintf(stderr, "\n  rows on SMs with %d rows: %d, mean phase us:", load, cnt);
         for (int ph = 1; ph < nph; ++ph) std::fprintf(stderr, " %.1f", dur[ph] / cnt);
+        double wait = 0;  // slot 14: thread 0's ring-stage waits inside the stream phase
+        for (size_t b = 0; b < nrows; ++b)
+            if (per_sm[t[b * 16 + 15] & 1023] == load) wait += t[b * 16 + 14] * 1e-3;
+        std::fprintf(stderr, " (stream: thread 0 waited %.1f us for stages)", wait / cnt);
     }
     std::fprintf(stderr, "\n");
 }

@@ -271,6 +271,10 @@ template <int KM, int CAND, int STAGES, int SAMPLE, int UU>
 __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     constexpr int kRowCand = CAND;
     constexpr int kRowStages = STAGES;
+#ifndef RTK_ROWS_LANE_HITS
+#define RTK_ROWS_LANE_HITS 1
+#endif
+    constexpr bool kLaneHits = RTK_ROWS_LANE_HITS && CAND == kRowCandS;  // per-lane appends (small k)
     constexpr int kRowSample = SAMPLE;
     extern __shared__ unsigned long long cand[];  // kRowCand entries
     __shared__ uint32_t hist[kBins];
@@ -439,7 +443,15 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
     constexpr int G = U / UU;  // 16-bit rows: the stage is consumed in G groups of UU sub-chunks
     for (uint64_t c = 0; c < nchunks; ++c) {
         const int st = static_cast<int>(c % kRowStages);
-        mbar_wait(&bar[st], static_cast<uint32_t>((c / kRowStages) & 1));
+        if (a.trace && tid == 0) {  // RTK_ROWS_TRACE: thread 0's time waiting for ring stages
+            unsigned long long t0w, t1w;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0w));
+            mbar_wait(&bar[st], static_cast<uint32_t>((c / kRowStages) & 1));
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1w));
+            a.trace[blockIdx.x * 16ull + 14] += t1w - t0w;
+        } else {
+            mbar_wait(&bar[st], static_cast<uint32_t>((c / kRowStages) & 1));
+        }
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             uint32_t key[4 * UU];
@@ -477,6 +489,36 @@ __device__ __forceinline__ void rows_fused_body(const RowsFusedArgs& a) {
             for (int e = 0; e < 4 * UU; ++e) {
                 key[e] = key_of<KM>(key[e], a.in);
                 maybe |= key[e] >= Thi;
+            }
+            if constexpr (kLaneHits) {
+                // small k: a 512-element warp group holds ~2 candidates, so the warp-aggregated
+                // append below would run for nearly every group; here only the lanes that pass
+                // the pre-filter compute their composite mask and append with their own shared
+                // atomic (no shuffles, no warp-wide work)
+                if (!maybe) continue;
+                uint32_t mask = 0;
+#pragma unroll
+                for (int u = 0; u < UU; ++u) {
+                    const uint32_t nb = ~(head + static_cast<uint32_t>(c * kChunk + (g * UU + u) * 2048) + tid * 4);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const unsigned long long K = (static_cast<unsigned long long>(key[4 * u + i]) << 32) | (nb - i);
+                        mask |= static_cast<uint32_t>(K >= T) << (4 * u + i);
+                    }
+                }
+                if (!mask) continue;
+                uint32_t o = atomicAdd(&s_m, static_cast<uint32_t>(__popc(mask)));
+#pragma unroll
+                for (int u = 0; u < UU; ++u) {
+                    const uint32_t nb = ~(head + static_cast<uint32_t>(c * kChunk + (g * UU + u) * 2048) + tid * 4);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if ((mask >> (4 * u + i)) & 1u) {
+                            if (o < kRowCand) cand[o] = (static_cast<unsigned long long>(key[4 * u + i]) << 32) | (nb - i);
+                            ++o;
+                        }
+                }
+                continue;
             }
             if (!__any_sync(full, maybe)) continue;
             uint32_t mask = 0;
